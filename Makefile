@@ -1,0 +1,23 @@
+# Build the C-ABI shared library for sm_100a (B200).  `python -c "import __graft_entry__ as g; g.build()"`
+# runs the same recipe.
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude
+SRC     := paper_2401_10089_b200/csrc
+OUT     := paper_2401_10089_b200/_build
+OBJS    := $(OUT)/lgm_api.o $(OUT)/lgm_grid.o
+LIB     := $(OUT)/liblogmpoly_b200.so
+
+all: $(LIB)
+
+$(OUT)/%.o: $(SRC)/%.cu $(wildcard $(SRC)/*.cuh $(SRC)/*.h) include/logmpoly_b200.h
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+clean:
+	rm -rf $(OUT)
+
+.PHONY: all clean

@@ -1,0 +1,127 @@
+/*
+ * logmpoly_b200.h -- C ABI of the B200-native batched FP64 matrix logarithm.
+ *
+ * Drop-in boundary for the reference's Python hot path.  The
+ * reference exposes no FFI; each entry point below replaces one reference function
+ * (cited file:line, relative to /root/reference/pkg/src/logmpoly/):
+ *
+ *   lgm_logm_f64              <- logm(A, opts) -> (L, LogmReport)       (missing driver.py,
+ *                                 imported at __init__.py:55)
+ *   lgm_sqrt_db_f64           <- sqrt_db(A, tol, maxiter, counter)      (sqrtm.py:27-78)
+ *   lgm_est_power_norm_f64    <- est_power_norm(B, p, counter, itmax)   (matcore.py:300-311)
+ *   lgm_est_product_norm_f64  <- est_product_norm([(M1,p1),(M2,1)], ...) (matcore.py:234-297)
+ *   lgm_balance_f64           <- balance(A, max_sweeps)                 (matcore.py:180-215)
+ *   lgm_eval_degopt_f64       <- eval_degopt(builtin_scheme(k), A, counter, first_product)
+ *                                                                       (schemes.py:104-126, 337-350)
+ *
+ * Conventions: every matrix pointer is a DEVICE pointer to `batch` row-major n x n
+ * float64 matrices with row stride `ld` >= n and matrix stride n*ld elements;
+ * inputs are never written; outputs never alias inputs.  All calls are
+ * stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream), do no
+ * hidden allocation and return synchronously-detected argument / launch errors
+ * (< 0).  Per-matrix numerical outcomes are reported per matrix through status
+ * codes (LGM_OK ... LGM_NONFINITE), which the Python layer maps onto the
+ * reference's exceptions (exceptions.py:6-18).  Reentrant; no global mutable state.
+ */
+#ifndef LOGMPOLY_B200_H
+#define LOGMPOLY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* lgm_stream_t; /* identical to cudaStream_t */
+
+/* per-matrix status (lgm_report.status and the building blocks' status arrays) */
+enum {
+  LGM_OK = 0,
+  LGM_SINGULAR = 1,        /* exact zero pivot          -> SingularMatrixError (matcore.py:124-125) */
+  LGM_DB_NOCONV = 2,       /* DB maxiter / collapse     -> ConvergenceError   (sqrtm.py:69-78)    */
+  LGM_SCALING_MAXITER = 3, /* s reached opts.maxiter_s  -> ConvergenceError       */
+  LGM_NONFINITE = 4,       /* NaN/Inf input or iterate  -> ValueError         (matcore.py:64-65)  */
+  LGM_SPECTRUM = 5         /* reserved (spectrum pre-check, off)                                  */
+};
+
+/* call-level errors (return values) */
+enum {
+  LGM_ERR_ARG = -1,
+  LGM_ERR_CUDA = -2,
+  LGM_ERR_UNSUPPORTED = -3,
+  LGM_ERR_WORKSPACE = -4
+};
+
+typedef struct lgm_opts {
+  int32_t max_k;      /* highest scheme index, 1..5 (shipped coefficients)       default 5  */
+  int32_t maxiter_s;  /* square-root cap (LogmOptions.maxiter)       default 40 */
+  int32_t db_maxiter; /* sqrt_db maxiter (sqrtm.py:27)                            default 50 */
+  int32_t est_itmax;  /* est_power_norm itmax (matcore.py:300)                    default 5  */
+  int32_t balance;    /* LogmOptions.balance                                      default 1  */
+  int32_t reserved;
+  double db_tol;      /* sqrt_db tol; 0 -> 10 n u (sqrtm.py:44-45)                default 0  */
+  const double* theta;/* HOST pointer to max_k thresholds; NULL -> frozen table             */
+} lgm_opts;
+
+typedef struct lgm_report { /* per matrix, written to device memory */
+  int32_t status;
+  int32_t s;                 /* square roots taken                                  */
+  int32_t k;                 /* scheme index selected                               */
+  int32_t db_iters;          /* DB iterations summed over roots                     */
+  int32_t products;          /* OpCounter.products                                  */
+  int32_t divisions;         /* OpCounter.divisions (2 per DB iteration)            */
+  int32_t estimation_passes; /* OpCounter.estimation_passes                         */
+  int32_t norm_estimations;  /* est_* calls performed                               */
+  int32_t balanced;          /* balancing applied                                   */
+  int32_t balance_sweeps;
+  int32_t db_plateau;        /* DB stop tests taken with rel in [tol/10, 10 tol]: the    */
+                             /* iteration count is rounding-noise dependent */
+  int32_t reserved;
+  double alpha_used;         /* alpha certifying k (<= Theta_k on success)          */
+  double min_margin;         /* min |x - thr| / |thr| over every discrete decision  */
+} lgm_report;
+
+void lgm_default_opts(lgm_opts* opts);
+
+/* Workspace the caller must provide to lgm_logm_f64 (0 for the fused n <= 64 path). */
+int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes);
+
+/* Largest n handled by the fused one-CTA-per-matrix engine. */
+int lgm_max_fused_n(void);
+
+int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t ld,
+                 const lgm_opts* opts, lgm_report* rep_dev, void* workspace,
+                 size_t workspace_bytes, lgm_stream_t stream);
+
+/* X = A^(1/2) by the scaled coupled DB iteration; iters/status: int32[batch] device. */
+int lgm_sqrt_db_f64(const double* A, double* X, int64_t n, int64_t batch, int64_t ld,
+                    double tol, int32_t maxiter, int32_t* iters_dev, int32_t* status_dev,
+                    lgm_stream_t stream);
+
+/* est = lower bound of ||M^p||_1; passes = estimation_passes; double/int32[batch] device. */
+int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld, int32_t p,
+                           int32_t itmax, double* est_dev, int32_t* passes_dev,
+                           lgm_stream_t stream);
+
+/* est = lower bound of ||M1^p1 M2||_1 (M2 may be NULL: ||M1^p1||_1 without the zero shortcut). */
+int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int64_t n,
+                             int64_t batch, int64_t ld, int32_t itmax, double* est_dev,
+                             int32_t* passes_dev, lgm_stream_t stream);
+
+/* B = T^-1 A T with radix-2 scales; scale: double[batch*n] device; sweeps: int32[batch]. */
+int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_t batch,
+                    int64_t ld, int32_t max_sweeps, int32_t* sweeps_dev, lgm_stream_t stream);
+
+/* Z = z(X) for shipped scheme k; first_product (X^2, may be NULL) saves one product. */
+int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z, int64_t n,
+                        int64_t batch, int64_t ld, int32_t k, int32_t* products_dev,
+                        lgm_stream_t stream);
+
+const char* lgm_status_string(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOGMPOLY_B200_H */

@@ -188,6 +188,7 @@ def _report(st, status, k=0, balanced=True, sweeps=0, msg=""):
         "norm_estimations": st.norm_estimations, "balanced": bool(balanced),
         "balance_sweeps": sweeps,
         "min_margin": st.prims.min_margin() if hasattr(st.prims, "min_margin") else math.nan,
+        "db_plateau": st.prims.margins.db_plateau if hasattr(st.prims, "margins") else 0,
         "message": msg,
     }
 

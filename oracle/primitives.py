@@ -47,6 +47,7 @@ class Margins:
 
     def __init__(self):
         self.min_margin = math.inf
+        self.db_plateau = 0
 
     def cmp(self, x, thr):
         den = abs(thr)
@@ -274,6 +275,8 @@ def sqrt_db(A, tol=None, maxiter=50, counter=None, margins=None):
         if rel < SCALING_SWITCH:
             scaling = False
         _note(margins, rel, tol)
+        if margins is not None and tol / 10.0 <= rel <= 10.0 * tol:
+            margins.db_plateau += 1
         if rel <= tol:
             return X, it
     raise ConvergenceError(f"square root did not converge in {maxiter} iterations")

@@ -1,0 +1,269 @@
+// C-ABI entry points (include/logmpoly_b200.h) and the kernels behind them.
+//
+// n <= 64: Engine F (lgm_fused.cuh), one CTA per matrix, the whole pipeline in one launch.
+// n  > 64: Engine G (lgm_grid.cu), host-orchestrated batched kernels over a caller-owned
+//          workspace (lgm_workspace_bytes).
+#include <cstdio>
+#include <cstring>
+
+#include "lgm_fused.cuh"
+#include "lgm_grid.cuh"
+
+using namespace lgm;
+
+// ------------------------------------------------------------------------------ kernels
+
+template <int NMAX>
+__global__ void __launch_bounds__(Cfg<NMAX>::NT) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
+                                                                  lgm_report* rep, long long ld, int n, const __grid_constant__ LgmParams P) {
+  extern __shared__ __align__(16) double smem[];
+  Ctx<NMAX> c;
+  c.init(smem, n, &P);
+  const long long b = blockIdx.x;
+  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b);
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(Cfg<NMAX>::NT) sqrt_db_kernel(const double* __restrict__ A, double* __restrict__ X,
+                                                               long long ld, int n, double tol, int maxiter,
+                                                               int* iters, int* status, const __grid_constant__ LgmParams P) {
+  extern __shared__ __align__(16) double smem[];
+  Ctx<NMAX> c;
+  c.init(smem, n, &P);
+  const long long b = blockIdx.x;
+  c.zero_all();
+  __syncthreads();
+  int st = 0, its = 0;
+  if (c.load(0, A + b * n * ld, ld)) st = LGM_NONFINITE;
+  else st = c.sqrt_db(0, 1, tol > 0.0 ? tol : 10.0 * n * LGM_UNIT_ROUNDOFF, maxiter, its);
+  __syncthreads();
+  c.store(0, X + b * n * ld, ld);
+  if (c.tid == 0) { iters[b] = its; status[b] = st; }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(Cfg<NMAX>::NT) est_kernel(const double* __restrict__ M1, int p1,
+                                                           const double* __restrict__ M2, long long ld, int n,
+                                                           int itmax, int zero_shortcut, double* est, int* passes,
+                                                           const __grid_constant__ LgmParams P) {
+  extern __shared__ __align__(16) double smem[];
+  Ctx<NMAX> c;
+  c.init(smem, n, &P);
+  const long long b = blockIdx.x;
+  c.zero_all();
+  __syncthreads();
+  c.load(2, M1 + b * n * ld, ld);
+  if (M2) c.load(0, M2 + b * n * ld, ld);
+  int ps = 0;
+  double e = 0.0;
+  bool go = true;
+  if (zero_shortcut) go = c.any_nonzero(2, 0.0);  // matcore.py:309-310
+  if (go) e = c.estimate(2, 0.0, p1, M2 != nullptr, 0, 0.0, itmax, ps);
+  if (c.tid == 0) { est[b] = e; passes[b] = ps; }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(Cfg<NMAX>::NT) balance_kernel(const double* __restrict__ A, double* __restrict__ B,
+                                                               double* scale, long long ld, int n, int max_sweeps,
+                                                               int* sweeps, const __grid_constant__ LgmParams P) {
+  extern __shared__ __align__(16) double smem[];
+  Ctx<NMAX> c;
+  c.init(smem, n, &P);
+  const long long b = blockIdx.x;
+  c.zero_all();
+  __syncthreads();
+  c.load(0, A + b * n * ld, ld);
+  int sw = c.balance(0, max_sweeps);
+  c.store(0, B + b * n * ld, ld);
+  for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) scale[b * n + i] = c.scale()[i];
+  if (c.tid == 0) sweeps[b] = sw;
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(Cfg<NMAX>::NT) degopt_kernel(const double* __restrict__ X, const double* __restrict__ FP,
+                                                              double* __restrict__ Z, long long ld, int n, int k,
+                                                              int* products, const __grid_constant__ LgmParams P) {
+  extern __shared__ __align__(16) double smem[];
+  Ctx<NMAX> c;
+  c.init(smem, n, &P);
+  const long long b = blockIdx.x;
+  c.zero_all();
+  __syncthreads();
+  c.load(BUF_B, X + b * n * ld, ld);
+  if (FP) c.load(BUF_P, FP + b * n * ld, ld);
+  for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
+  __syncthreads();
+  int prods = 0;
+  const int bfree[3] = {BUF_4, BUF_5, BUF_6};
+  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, bfree, 1.0, false, Z + b * n * ld, ld, prods);
+  if (c.tid == 0) products[b] = prods;
+}
+
+// ------------------------------------------------------------------------------ host side
+
+static void fill_params(LgmParams& P, const lgm_opts* o) {
+  lgm_opts d;
+  lgm_default_opts(&d);
+  if (!o) o = &d;
+  P.max_k = o->max_k;
+  P.maxiter_s = o->maxiter_s;
+  P.db_maxiter = o->db_maxiter;
+  P.est_itmax = o->est_itmax;
+  P.balance = o->balance;
+  P.db_tol = o->db_tol;
+  for (int k = 0; k < LGM_K_MAX; ++k) {
+    P.theta[k] = (o->theta && k < o->max_k) ? o->theta[k] : LGM_THETA_DEFAULT[k];
+    P.order[k] = LGM_ORDER_DEFAULT[k];
+    P.coef_off[k] = LGM_COEF_OFFSET[k];
+  }
+  std::memcpy(P.coef, LGM_COEF_DEFAULT, sizeof(P.coef));
+}
+
+static int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "logmpoly_b200: CUDA error %s\n", cudaGetErrorString(e));
+    return LGM_ERR_CUDA;
+  }
+  return 0;
+}
+
+template <int NMAX, class K>
+static int prep(K kernel) {
+  static_assert(Cfg<NMAX>::SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Cfg<NMAX>::SMEM_BYTES);
+  return e == cudaSuccess ? 0 : LGM_ERR_CUDA;
+}
+
+static bool args_ok(const void* p, int64_t n, int64_t batch, int64_t ld) {
+  return p && n >= 1 && batch >= 0 && ld >= n && batch <= (int64_t)0x7fffffff;
+}
+
+extern "C" {
+
+void lgm_default_opts(lgm_opts* o) {
+  if (!o) return;
+  o->max_k = LGM_K_MAX;
+  o->maxiter_s = 40;
+  o->db_maxiter = 50;
+  o->est_itmax = 5;
+  o->balance = 1;
+  o->reserved = 0;
+  o->db_tol = 0.0;
+  o->theta = nullptr;
+}
+
+int lgm_max_fused_n(void) { return 64; }
+
+int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
+  if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
+  *bytes = n <= 64 ? 0 : lgm_grid_workspace_bytes(n, batch);
+  return 0;
+}
+
+const char* lgm_status_string(int code) {
+  switch (code) {
+    case LGM_OK: return "ok";
+    case LGM_SINGULAR: return "matrix is exactly singular (zero pivot) in a square-root step";
+    case LGM_DB_NOCONV: return "square root did not converge (eigenvalues on the negative real axis?)";
+    case LGM_SCALING_MAXITER: return "no convergence after maxiter square roots";
+    case LGM_NONFINITE: return "matrix has non-finite entries";
+    case LGM_SPECTRUM: return "spectrum check failed";
+    case LGM_ERR_ARG: return "invalid argument";
+    case LGM_ERR_CUDA: return "CUDA error";
+    case LGM_ERR_UNSUPPORTED: return "unsupported size";
+    case LGM_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t ld, const lgm_opts* opts,
+                 lgm_report* rep, void* ws, size_t ws_bytes, lgm_stream_t stream) {
+  if (!args_ok(A, n, batch, ld) || !L || !rep || (const void*)L == (const void*)A) return LGM_ERR_ARG;
+  LgmParams P;
+  fill_params(P, opts);
+  if (P.max_k < 1 || P.max_k > LGM_K_MAX || P.maxiter_s < 0 || P.db_maxiter < 1 || P.est_itmax < 1)
+    return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 32) {
+    if (prep<32>(logm_fused_kernel<32>)) return LGM_ERR_CUDA;
+    logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n, P);
+    return check_launch();
+  }
+  if (n <= 64) {
+    if (prep<64>(logm_fused_kernel<64>)) return LGM_ERR_CUDA;
+    logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n, P);
+    return check_launch();
+  }
+  size_t need = lgm_grid_workspace_bytes(n, batch);
+  if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
+  return lgm_grid_logm(A, L, n, batch, ld, P, rep, ws, s);
+}
+
+#define LGM_DISPATCH_SMALL(KERNEL, ...)                                                                  \
+  do {                                                                                                   \
+    if (n <= 32) {                                                                                       \
+      if (prep<32>(KERNEL<32>)) return LGM_ERR_CUDA;                                                     \
+      KERNEL<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
+      return check_launch();                                                                             \
+    }                                                                                                    \
+    if (n <= 64) {                                                                                       \
+      if (prep<64>(KERNEL<64>)) return LGM_ERR_CUDA;                                                     \
+      KERNEL<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
+      return check_launch();                                                                             \
+    }                                                                                                    \
+  } while (0)
+
+int lgm_sqrt_db_f64(const double* A, double* X, int64_t n, int64_t batch, int64_t ld, double tol, int32_t maxiter,
+                    int32_t* iters, int32_t* status, lgm_stream_t stream) {
+  if (!args_ok(A, n, batch, ld) || !X || !iters || !status || maxiter < 1) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  LgmParams P;
+  fill_params(P, nullptr);
+  LGM_DISPATCH_SMALL(sqrt_db_kernel, A, X, ld, (int)n, tol, maxiter, iters, status, P);
+  return lgm_grid_sqrt_db(A, X, n, batch, ld, tol, maxiter, iters, status, (cudaStream_t)stream);
+}
+
+int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld, int32_t p, int32_t itmax,
+                           double* est, int32_t* passes, lgm_stream_t stream) {
+  if (!args_ok(M, n, batch, ld) || !est || !passes || p < 1 || itmax < 1) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  LgmParams P;
+  fill_params(P, nullptr);
+  LGM_DISPATCH_SMALL(est_kernel, M, p, (const double*)nullptr, ld, (int)n, itmax, 1, est, passes, P);
+  return lgm_grid_est(M, p, nullptr, n, batch, ld, itmax, 1, est, passes, (cudaStream_t)stream);
+}
+
+int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int64_t n, int64_t batch, int64_t ld,
+                             int32_t itmax, double* est, int32_t* passes, lgm_stream_t stream) {
+  if (!args_ok(M1, n, batch, ld) || !est || !passes || p1 < 1 || itmax < 1) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  LgmParams P;
+  fill_params(P, nullptr);
+  LGM_DISPATCH_SMALL(est_kernel, M1, p1, M2, ld, (int)n, itmax, 0, est, passes, P);
+  return lgm_grid_est(M1, p1, M2, n, batch, ld, itmax, 0, est, passes, (cudaStream_t)stream);
+}
+
+int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_t batch, int64_t ld,
+                    int32_t max_sweeps, int32_t* sweeps, lgm_stream_t stream) {
+  if (!args_ok(A, n, batch, ld) || !B || !scale || !sweeps || max_sweeps < 1) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  LgmParams P;
+  fill_params(P, nullptr);
+  LGM_DISPATCH_SMALL(balance_kernel, A, B, scale, ld, (int)n, max_sweeps, sweeps, P);
+  return lgm_grid_balance(A, B, scale, n, batch, ld, max_sweeps, sweeps, (cudaStream_t)stream);
+}
+
+int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
+                        int32_t* products, lgm_stream_t stream) {
+  if (!args_ok(X, n, batch, ld) || !Z || !products || k < 1 || k > LGM_K_MAX) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  LgmParams P;
+  fill_params(P, nullptr);
+  LGM_DISPATCH_SMALL(degopt_kernel, X, FP, Z, ld, (int)n, k, products, P);
+  return lgm_grid_degopt(X, FP, Z, n, batch, ld, k, products, P, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,924 @@
+// Engine F: the whole logm pipeline for one matrix per CTA, n <= NMAX (32 or 64).
+//
+// Layout: the CTA is two *teams* of T = NMAX/32 warps; inside a
+// team thread `row` owns matrix row `row`.  Matrices live in shared memory with a padded
+// row stride LDM = NMAX + 1 doubles, which makes both row-per-thread accesses
+// (M[row][j], lanes = rows) and column-per-thread accesses (M[i][col], lanes = cols)
+// bank-conflict free.  The pivoted Gauss-Jordan inversion keeps the row being eliminated
+// in registers (NMAX doubles per thread, fully unrolled); the two teams invert X and Y of
+// the Denman-Beavers step concurrently, and the two columns of the block 1-norm
+// estimator run on the two teams.  All threads execute the (uniform) Algorithm-1 driver
+// code; data-dependent decisions are broadcast through shared memory.
+//
+// Reference (relative to /root/reference/pkg/src/logmpoly/): balance matcore.py:180-215;
+// onenorm :84-87; est_product_norm :234-297; est_power_norm :300-311; sqrt_db
+// sqrtm.py:27-78; eval_degopt schemes.py:91-126; driver SPEC.md:429-502 / PAPER.md:724-840
+// as restated in oracle/driver.py.
+#pragma once
+#include "lgm_common.cuh"
+
+namespace lgm {
+
+template <int NMAX>
+struct Cfg {
+  static constexpr int T = NMAX / 32;     // warps per team
+  static constexpr int NT = 64 * T;       // threads per CTA
+  static constexpr int LDM = NMAX + 1;    // padded row stride (doubles)
+  static constexpr int MAT = NMAX * LDM;  // doubles per matrix buffer
+  static constexpr int NBUF = 6;
+  // shared-memory carve-up (in doubles)
+  static constexpr int OFF_PROW = NBUF * MAT;                // [2 teams][2][NMAX+2]
+  static constexpr int PROW = NMAX + 2;
+  static constexpr int OFF_VEC = OFF_PROW + 2 * 2 * PROW;    // [8][NMAX]
+  static constexpr int OFF_SCALE = OFF_VEC + 8 * NMAX;       // [NMAX] balancing scales
+  static constexpr int OFF_RED = OFF_SCALE + NMAX;           // [64] reduction scratch
+  static constexpr int OFF_INT = OFF_RED + 64;               // ints: piv[2][NMAX], misc[64]
+  static constexpr int SMEM_DOUBLES = OFF_INT + (2 * NMAX + 64 + 1) / 2 + 1;
+  static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
+};
+
+// misc int slots
+enum { MI_STATUS = 0, MI_STATUS2, MI_J, MI_NPICK, MI_ORDER = 8 /* 9 slots */, MI_PICK = 20,
+       MI_FLAG = 24, MI_COUNT = 64 };
+// red double slots
+enum { RD_LOGDET = 0 /* 2 */, RD_KEY = 4 /* [2 teams][4 slots] */, RD_CN = 12 /* 2 */,
+       RD_CHANGE = 16, RD_SCALE = 20 /* [2 warps] */, RD_MARGIN = 24, RD_EST = 28,
+       RD_NORM = 32 /* [4] */, RD_H = 40 /* 9 sorted h values */ };
+
+template <int NMAX>
+struct Ctx {
+  using C = Cfg<NMAX>;
+  double* sm;      // dynamic shared memory base
+  int n;
+  int tid, warp, lane, team, wit, row;  // wit = warp index in team, row = wit*32 + lane
+  const LgmParams* P;
+  double mm;       // running min margin (uniform)
+  int plateau;     // DB stop tests in the noise band [tol/10, 10 tol] (uniform)
+
+  __device__ double* buf(int b) const { return sm + b * C::MAT; }
+  __device__ double* prow(int tm, int parity) const { return sm + C::OFF_PROW + (tm * 2 + parity) * C::PROW; }
+  __device__ double* vec(int v) const { return sm + C::OFF_VEC + v * NMAX; }
+  __device__ double* scale() const { return sm + C::OFF_SCALE; }
+  __device__ double* red() const { return sm + C::OFF_RED; }
+  __device__ int* ints() const { return reinterpret_cast<int*>(sm + C::OFF_INT); }
+  __device__ int* piv(int tm) const { return ints() + tm * NMAX; }
+  __device__ int* misc() const { return ints() + 2 * NMAX; }
+
+  __device__ void init(double* smem, int n_, const LgmParams* p) {
+    sm = smem; n = n_; P = p;
+    tid = threadIdx.x; warp = tid >> 5; lane = tid & 31;
+    team = warp / C::T; wit = warp % C::T; row = wit * 32 + lane;
+    mm = INFINITY;
+    plateau = 0;
+  }
+
+  __device__ __forceinline__ void team_sync() const {
+    if (C::T == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(C::T * 32) : "memory");
+  }
+
+  // ---- margins (uniform) -------------------------------------------------------------
+  __device__ __forceinline__ void note(double x, double thr) {
+    double den = fabs(thr);
+    double m = den > 0.0 ? fabs(x - thr) / den : fabs(x - thr);
+    mm = fmin(mm, m);
+  }
+  __device__ __forceinline__ void gap(double a, double b) {
+    double den = fmax(fabs(a), fabs(b));
+    mm = fmin(mm, den > 0.0 ? fabs(a - b) / den : 0.0);
+  }
+  __device__ __forceinline__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
+
+  // ---- elementwise helpers ------------------------------------------------------------
+  __device__ void zero_all() {
+    for (int i = tid; i < C::NBUF * C::MAT; i += C::NT) sm[i] = 0.0;
+  }
+  __device__ void copy_buf(int dst, int src) {
+    double* d = buf(dst);
+    const double* s = buf(src);
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      d[i * C::LDM + j] = s[i * C::LDM + j];
+    }
+  }
+  __device__ void set_identity(int b) {
+    double* d = buf(b);
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      d[i * C::LDM + j] = (i == j) ? 1.0 : 0.0;
+    }
+  }
+
+  // onenorm(M - shift*I) exactly as numpy: column sums accumulated over rows in order.
+  __device__ double onenorm(int b, double shift) {
+    const double* M = buf(b);
+    double cs = 0.0;
+    for (int j = tid; j < n; j += C::NT) {
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) {
+        double v = M[i * C::LDM + j];
+        if (i == j) v = v - shift;
+        acc = (i == 0) ? fabs(v) : acc + fabs(v);
+      }
+      cs = fmax(cs, acc);
+    }
+    cs = lgm_warp_max(cs);
+    __syncthreads();
+    if (lane == 0) red()[RD_NORM + warp] = cs;
+    __syncthreads();
+    double r = red()[RD_NORM];
+    for (int w = 1; w < C::NT / 32; ++w) r = fmax(r, red()[RD_NORM + w]);
+    __syncthreads();
+    return r;
+  }
+
+  // ---- balancing (matcore.py:180-215), bit-identical decisions --------------------------
+  __device__ int balance(int b, int max_sweeps) {
+    double* B = buf(b);
+    double* sc = scale();
+    for (int i = tid; i < n; i += C::NT) sc[i] = 1.0;
+    __syncthreads();
+    int sweeps = 0;
+    for (int sw = 0; sw < max_sweeps; ++sw) {
+      sweeps++;
+      bool moved = false;
+      for (int i = 0; i < n; ++i) {
+        // every thread evaluates the (pairwise-ordered) sums redundantly: uniform decisions
+        double dg = fabs(B[i * C::LDM + i]);
+        double c = lgm_pairwise_sum([&](int r) { return fabs(B[r * C::LDM + i]); }, n) - dg;
+        double r = lgm_pairwise_sum([&](int q) { return fabs(B[i * C::LDM + q]); }, n) - dg;
+        if (c == 0.0 || r == 0.0) continue;
+        double tot = c + r, f = 1.0;
+        while (true) {
+          note(c, r / 2.0);
+          if (!(c < r / 2.0)) break;
+          c *= 2.0; r /= 2.0; f *= 2.0;
+        }
+        while (true) {
+          note(c, r * 2.0);
+          if (!(c >= r * 2.0)) break;
+          c /= 2.0; r *= 2.0; f /= 2.0;
+        }
+        note(c + r, 0.95 * tot);
+        if (c + r < 0.95 * tot && 1e-300 < f && f < 1e300) {
+          __syncthreads();  // all threads finished reading column/row i
+          double inv = 1.0 / f;  // exact: f is a power of two in (1e-300, 1e300)
+          for (int q = tid; q < n; q += C::NT) B[q * C::LDM + i] *= f;
+          __syncthreads();
+          for (int q = tid; q < n; q += C::NT) B[i * C::LDM + q] *= inv;
+          if (tid == 0) sc[i] *= f;
+          moved = true;
+          __syncthreads();
+        }
+      }
+      if (!moved) break;
+    }
+    __syncthreads();
+    return sweeps;
+  }
+
+  // ---- pivoted Gauss-Jordan inversion of the team's matrix, row in registers -------------
+  // On entry r[] holds row `row` of M (zeros beyond n; rows >= n all zero).  On exit r[]
+  // holds storage row `row` of the in-place result: Minv[q(row)][p_j] = r[j], where p_j is
+  // the pivot row of step j (piv(team)[j]) and q(row) = my_step.  Returns 1 if an exact zero
+  // pivot is met (matcore.py:124-125), else 0; logabsdet = sum log|pivot| (team-uniform).
+  __device__ int gj_invert(double (&r)[NMAX], double& logabsdet, int& my_step) {
+    bool used = false;
+    my_step = -1;
+    double mylog = 0.0;
+    int* pv = piv(team);
+    double* kslot = red() + RD_KEY + team * 4;
+    int status = 0;
+#pragma unroll
+    for (int k = 0; k < NMAX; ++k) {
+      if (k < n) {
+        bool cand = (row < n) && !used;
+        uint64_t key = cand ? lgm_key(fabs(r[k])) : 0ull;
+        int wl;
+        uint64_t kmax = lgm_warp_argmax(key, wl);
+        int prow_idx = wit * 32 + wl;
+        if (C::T > 1) {
+          if (lane == 0) {
+            reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
+            reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
+          }
+          team_sync();
+          uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
+          uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
+          int r0 = reinterpret_cast<int*>(kslot + 2)[0];
+          int r1 = reinterpret_cast<int*>(kslot + 2)[1];
+          if (k1 > k0) { kmax = k1; prow_idx = r1; } else { kmax = k0; prow_idx = r0; }
+        }
+        if (kmax <= 1ull) { status = 1; break; }  // all remaining candidates exactly zero
+        double* pr = prow(team, k & 1);
+        if (row == prow_idx) {
+          used = true;
+          my_step = k;
+          double p = r[k];
+          mylog = log(fabs(p));
+          double inv = 1.0 / p;
+#pragma unroll
+          for (int j = 0; j < NMAX; ++j) r[j] = (j == k) ? inv : r[j] * inv;
+#pragma unroll
+          for (int j = 0; j < NMAX; j += 2)
+            *reinterpret_cast<double2*>(pr + j) = make_double2(r[j], r[j + 1]);
+          pv[k] = prow_idx;
+        }
+        team_sync();
+        if (row != prow_idx) {
+          double f = r[k];
+#pragma unroll
+          for (int j = 0; j < NMAX; j += 2) {
+            double2 p2 = *reinterpret_cast<const double2*>(pr + j);
+            if (j != k) r[j] = fma(-f, p2.x, r[j]);
+            if (j + 1 != k) r[j + 1] = fma(-f, p2.y, r[j + 1]);
+          }
+          r[k] = -f * pr[k];
+        }
+      }
+    }
+    // team sum of the pivots' log|.| (one per valid row)
+    double s = lgm_warp_sum(mylog);
+    if (C::T > 1) {
+      team_sync();
+      if (lane == 0) red()[RD_LOGDET + team * 2 + wit] = s;
+      team_sync();
+      s = red()[RD_LOGDET + team * 2] + red()[RD_LOGDET + team * 2 + 1];
+      team_sync();
+    }
+    logabsdet = s;
+    return status;
+  }
+
+  // butterfly reduce-scatter of v[NMAX] over the warp: lane l ends holding the sums of
+  // register indices {l*(NMAX/32) + e}; returns max over those per-lane sums (warp-reduced
+  // to a single value for the whole team).
+  __device__ double colsum_max(double (&v)[NMAX]) {
+#pragma unroll
+    for (int off = 16, len = NMAX; off >= 1; off >>= 1, len >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < NMAX / 2; ++i) {
+        if (i < len / 2) {
+          double send = up ? v[i] : v[i + len / 2];
+          double keep = up ? v[i + len / 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+    }
+    // lane holds NMAX/32 column partial sums in v[0..NMAX/32-1] (this warp's rows)
+    if (C::T == 1) {
+      double m = v[0];
+#pragma unroll
+      for (int e = 1; e < NMAX / 32; ++e) m = fmax(m, v[e]);
+      return lgm_warp_max(m);
+    }
+    // T == 2: add the other warp's partial column sums
+    double* scr = vec(6);  // [NMAX] scratch
+    team_sync();
+    if (wit == 1) {
+#pragma unroll
+      for (int e = 0; e < NMAX / 32; ++e) scr[lane * (NMAX / 32) + e] = v[e];
+    }
+    team_sync();
+    double m = 0.0;
+    if (wit == 0) {
+#pragma unroll
+      for (int e = 0; e < NMAX / 32; ++e) m = fmax(m, v[e] + scr[lane * (NMAX / 32) + e]);
+    }
+    m = lgm_warp_max(m);
+    team_sync();
+    return m;  // valid in warp wit == 0
+  }
+
+  // ---- scaled coupled Denman-Beavers square root (sqrtm.py:27-78) ------------------------
+  // X (buffer bx) is replaced by X^(1/2); buffer by is workspace (Y).  Returns status
+  // (0, LGM_SINGULAR, LGM_DB_NOCONV, LGM_NONFINITE); iters = iterations performed.
+  __device__ int sqrt_db(int bx, int by, double tol, int maxiter, int& iters) {
+    double* X = buf(bx);
+    double* Y = buf(by);
+    set_identity(by);
+    __syncthreads();
+    bool scaling = true;
+    const double two_n = 2.0 * n;
+    iters = 0;
+    for (int it = 1; it <= maxiter; ++it) {
+      iters = it;
+      double r[NMAX];
+      // team 0 loads X, team 1 loads Y (skipped at it == 1: Y = I, Y^-1 = I, log|det| = 0)
+      const bool active = (team == 0) || (it > 1);
+      bool bad = false;
+      if (!active) {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) r[j] = 0.0;
+      } else {
+        const double* S = team == 0 ? X : Y;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          double v = (row < n && j < n) ? S[row * C::LDM + j] : 0.0;
+          bad |= !isfinite(v);
+          r[j] = v;
+        }
+      }
+      int st = __syncthreads_or(bad) ? 4 : 0;
+      if (st) { iters = it - 1; return LGM_NONFINITE; }  // as_square inside lu_factor (matcore.py:122)
+      double logdet = 0.0;
+      int my_step = -1, sing = 0;
+      if (active) sing = gj_invert(r, logdet, my_step);
+      if (tid == 0) { misc()[MI_STATUS] = 0; }
+      __syncthreads();
+      if (active && row == 0 && wit == 0) {
+        red()[RD_LOGDET + 2 * team] = logdet;
+        if (sing) atomicOr(&misc()[MI_STATUS], 1);
+      }
+      if (!active && row == 0 && wit == 0) red()[RD_LOGDET + 2 * team] = 0.0;
+      __syncthreads();
+      if (misc()[MI_STATUS]) { iters = it - 1; return LGM_SINGULAR; }
+      const double lx = red()[RD_LOGDET], ly = red()[RD_LOGDET + 2];
+      double mu = 1.0;
+      if (scaling) mu = fmin(fmax(exp(-(lx + ly) / two_n), LGM_MU_MIN), LGM_MU_MAX);
+      const double inv_mu = 1.0 / mu;
+      // team 0 (holds X^-1, permuted) forms Y' = (mu Y + X^-1/mu)/2 in place;
+      // team 1 (holds Y^-1, permuted; or I at it == 1) forms X' = (mu X + Y^-1/mu)/2 in place
+      // and the column sums of |X' - X| and |X'|.
+      // (register-lean: the inverse row in r[] is overwritten by |X' - X|, then by |X'|)
+      const int* pv = piv(team);
+      if (team == 0) {
+        if (row < n) {
+          const int q = my_step;
+#pragma unroll
+          for (int j = 0; j < NMAX; ++j) {
+            if (j < n) {
+              double* y = &Y[q * C::LDM + pv[j]];
+              *y = 0.5 * (mu * *y + r[j] * inv_mu);
+            }
+          }
+        }
+      } else {
+        const int q = (it == 1) ? row : my_step;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          double dj = 0.0;
+          if (row < n && j < n) {
+            const int col = (it == 1) ? j : pv[j];
+            double* x = &X[q * C::LDM + col];
+            double xo = *x;
+            double yi = (it == 1) ? ((col == row) ? inv_mu : 0.0) : r[j] * inv_mu;
+            double xn = 0.5 * (mu * xo + yi);
+            *x = xn;
+            dj = fabs(xn - xo);
+          }
+          r[j] = dj;
+        }
+        double change = colsum_max(r);
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          double aj = 0.0;
+          if (row < n && j < n) aj = fabs(X[q * C::LDM + ((it == 1) ? j : pv[j])]);
+          r[j] = aj;
+        }
+        double size = colsum_max(r);
+        if (wit == 0 && lane == 0) { red()[RD_CHANGE] = change; red()[RD_SCALE] = size; }
+      }
+      __syncthreads();
+      const double change = red()[RD_CHANGE], size = red()[RD_SCALE];
+      __syncthreads();
+      if (size == 0.0) return LGM_DB_NOCONV;  // sqrtm.py:69-70
+      const double rel = change / size;
+      note(rel, LGM_SCALING_SWITCH);
+      if (rel < LGM_SCALING_SWITCH) scaling = false;
+      note(rel, tol);
+      if (tol / 10.0 <= rel && rel <= 10.0 * tol) plateau++;
+      if (rel <= tol) return 0;
+    }
+    return LGM_DB_NOCONV;  // sqrtm.py:76-78
+  }
+
+  // ---- block 1-norm estimator (matcore.py:234-311) -------------------------------------
+  // Operator = M1^p1 [* AmI] where M1 = buf(b1) - sh1*I and AmI = buf(bA) - I (if has2).
+  // Returns the estimate (uniform); passes += total_power per apply.
+  __device__ double mat_el(const double* M, int i, int j, double sh) const {
+    double v = M[i * C::LDM + j];
+    return (i == j) ? v - sh : v;
+  }
+
+  // y = M x (row-per-thread) or y = M^T x (column-per-thread) for the team's column, with
+  // M = buf - sh*I formed element-exactly like numpy's explicit B - I.
+  __device__ void thin(const double* M, double sh, bool trans, const double* x, double* y) {
+    if (row < n) {
+      double acc0 = 0.0, acc1 = 0.0;
+      const double dg = M[row * C::LDM + row] - sh;
+      const int rs = trans ? C::LDM : 1;                 // stride along the dot product
+      const double* Mr = trans ? M + row : M + row * C::LDM;
+      int j = 0;
+      for (; j + 1 < n; j += 2) {
+        double v0 = (j == row) ? dg : Mr[j * rs];
+        double v1 = (j + 1 == row) ? dg : Mr[(j + 1) * rs];
+        acc0 = fma(v0, x[j], acc0);
+        acc1 = fma(v1, x[j + 1], acc1);
+      }
+      if (j < n) acc0 = fma((j == row) ? dg : Mr[j * rs], x[j], acc0);
+      y[row] = acc0 + acc1;
+    }
+    team_sync();
+  }
+
+  __device__ bool any_nonzero(int b, double sh) {
+    bool nz = false;
+    const double* M = buf(b);
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      nz |= mat_el(M, i, j, sh) != 0.0;
+    }
+    return __syncthreads_or(nz);
+  }
+
+  __device__ double estimate(int b1, double sh1, int p1, bool has2, int bA, double sh2, int itmax, int& passes) {
+    const int t = n < 2 ? n : 2;
+    const int total = p1 + (has2 ? 1 : 0);
+    const double* M1 = buf(b1);
+    const double* MA = buf(bA);
+    // vec layout: col c uses vec(2c) / vec(2c+1) ping-pong; vec(4), vec(5) = Z cols; vec(7) = h
+    double* h = vec(7);
+    int* order = misc() + MI_ORDER;
+    // initial block X (matcore.py:265-271)
+    {
+      double rsum = lgm_pairwise_sum(
+          [&](int i) { return fabs(((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))); }, n);
+      for (int i = tid; i < n; i += C::NT) {
+        vec(0)[i] = 1.0 / n;
+        if (t > 1) vec(2)[i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
+      }
+    }
+    __syncthreads();
+    double est = 0.0;
+    int best_j = 0, ncols = t;
+    uint64_t hist = 0ull;
+    for (int sweep = 0; sweep < itmax; ++sweep) {
+      // ---- forward: Y = op(X), team c handles column c
+      int cur = 0;
+      if (team < ncols) {
+        double* xa = vec(2 * team);
+        double* xb = vec(2 * team + 1);
+        if (has2) { thin(MA, sh2, false, xa, xb); double* tt = xa; xa = xb; xb = tt; cur ^= 1; }
+        for (int q = 0; q < p1; ++q) { thin(M1, sh1, false, xa, xb); double* tt = xa; xa = xb; xb = tt; cur ^= 1; }
+        // column 1-norm (axis-0 sum); team reduction
+        double v = (row < n) ? fabs(xa[row]) : 0.0;
+        v = lgm_warp_sum(v);
+        if (lane == 0) red()[RD_CN + team * 2 + wit] = v;
+      }
+      passes += total;
+      __syncthreads();
+      double cn[2] = {0.0, 0.0};
+      for (int c = 0; c < ncols; ++c) {
+        cn[c] = red()[RD_CN + c * 2];
+        if (C::T > 1) cn[c] += red()[RD_CN + c * 2 + 1];
+      }
+      const int yb = cur;  // Y column c is in vec(2c + yb)
+      int j = (ncols > 1 && cn[1] > cn[0]) ? 1 : 0;
+      if (ncols > 1) gap(cn[0], cn[1]);
+      double cand = cn[j];
+      if (est > 0.0) gap(cand, est);
+      if (cand > est) { est = cand; best_j = j; }
+      else if (sweep > 0) break;
+      // ---- adjoint: Z = op^T(sign(Y))
+      if (team < ncols) {
+        double* ya = vec(2 * team + yb);
+        double* yb2 = vec(2 * team + (yb ^ 1));
+        if (row < n) ya[row] = (ya[row] >= 0.0) ? 1.0 : -1.0;  // matcore.py:231
+        team_sync();
+        double* xa = ya;
+        double* xb = yb2;
+        for (int q = 0; q < p1; ++q) { thin(M1, sh1, true, xa, xb); double* tt = xa; xa = xb; xb = tt; }
+        if (has2) { thin(MA, sh2, true, xa, xb); double* tt = xa; xa = xb; xb = tt; }
+        if (row < n) vec(4 + team)[row] = xa[row];
+      }
+      passes += total;
+      __syncthreads();
+      // h = row max |Z|, top-(4t+1) order (desc, ties -> lowest index) by warp 0
+      for (int i = tid; i < n; i += C::NT) {
+        double hv = fabs(vec(4)[i]);
+        if (ncols > 1) hv = fmax(hv, fabs(vec(5)[i]));
+        h[i] = hv;
+      }
+      __syncthreads();
+      const int ntop = n < 4 * t + 1 ? n : 4 * t + 1;
+      if (warp == 0) {
+        uint64_t taken = 0ull;
+        for (int q = 0; q < ntop; ++q) {
+          // lane examines rows lane and lane + 32
+          uint64_t kbest = 0ull;
+          int rbest = 1 << 30;
+#pragma unroll
+          for (int e = 0; e < NMAX / 32; ++e) {
+            int i = lane + 32 * e;
+            if (i < n && !((taken >> i) & 1ull)) {
+              uint64_t kk = lgm_key(h[i]);
+              if (kk > kbest) { kbest = kk; rbest = i; }
+            }
+          }
+          int wl;
+          uint64_t kmax = lgm_warp_argmax(kbest, wl);
+          unsigned tie = __ballot_sync(0xffffffffu, kbest == kmax);
+          int rsel = (kbest == kmax) ? rbest : (1 << 30);
+          rsel = __reduce_min_sync(0xffffffffu, (unsigned)rsel);
+          (void)tie; (void)wl;
+          taken |= 1ull << rsel;
+          if (lane == 0) { order[q] = rsel; red()[RD_H + q] = lgm_unkey(kmax); }
+        }
+      }
+      __syncthreads();
+      for (int a = 0; a + 1 < ntop && a < 4 * t; ++a) gap(red()[RD_H + a], red()[RD_H + a + 1]);
+      int picks[2], npick = 0;
+      for (int q = 0; q < (ntop < 4 * t ? ntop : 4 * t) && npick < t; ++q) {
+        int i = order[q];
+        if (!((hist >> i) & 1ull)) picks[npick++] = i;
+      }
+      const double h0 = h[order[0]], hb = h[best_j];
+      if (sweep > 0 && order[0] != best_j) gap(h0, hb);
+      if (npick == 0 || (sweep > 0 && h0 <= hb)) break;
+      __syncthreads();
+      for (int c = 0; c < npick; ++c) hist |= 1ull << picks[c];
+      ncols = npick;
+      for (int i = tid; i < n; i += C::NT) {
+        vec(0)[i] = (i == picks[0]) ? 1.0 : 0.0;
+        if (npick > 1) vec(2)[i] = (i == picks[1]) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    return est;
+  }
+
+  // ---- GEMM with fused left combination -------------------------------------------------
+  // acc[jj] = sum_kk L[row][kk] * R[kk][col0 + jj], col0 = team * NMAX/2, where
+  // L = sum_t lc[t] * buf(lb[t]) + l0 * I computed on the fly with numpy's _combine
+  // rounding (schemes.py:91-101: products and sums rounded separately, no FMA).
+  static constexpr int MAXT = 7;
+  __device__ void gemm_comb(int nterm, const double (&lc)[MAXT], const int (&lb)[MAXT], double l0,
+                            const double* R, double (&acc)[NMAX / 2]) {
+    const int col0 = team * (NMAX / 2);
+#pragma unroll
+    for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = 0.0;
+    if (row >= n) return;
+    const double* Lb[MAXT];
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) Lb[q] = buf(lb[q]) + row * C::LDM;
+    for (int kk = 0; kk < n; ++kk) {
+      double l = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXT; ++q)
+        if (q < nterm) l = __dadd_rn(l, __dmul_rn(lc[q], Lb[q][kk]));
+      if (kk == row && l0 != 0.0) l = __dadd_rn(l, l0);
+      const double* Rr = R + kk * C::LDM + col0;
+#pragma unroll
+      for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = fma(l, Rr[jj], acc[jj]);
+    }
+  }
+
+  // buf(dst)[i][j] = sum_t c[t] * buf(b[t])[i][j] + c0 * I (schemes.py:91-101 order)
+  __device__ void combine_into(int dst, int nterm, const double (&c)[MAXT], const int (&b)[MAXT], double c0) {
+    double* D = buf(dst);
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXT; ++q)
+        if (q < nterm) v = __dadd_rn(v, __dmul_rn(c[q], buf(b[q])[i * C::LDM + j]));
+      if (i == j && c0 != 0.0) v = __dadd_rn(v, c0);
+      D[i * C::LDM + j] = v;
+    }
+  }
+
+  // Gather the non-zero coefficients of a combination row over nodes P1..P_{nn}
+  // (P1 = I, P_t in buffer nodebuf[t]).
+  __device__ static int gather_terms(const double* row, int nn, const int* nodebuf, double (&c)[MAXT],
+                                     int (&b)[MAXT], double& c0) {
+    int q = 0;
+    c0 = row[0];
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) { c[t] = 0.0; b[t] = 0; }
+    for (int t = 2; t <= nn; ++t) {
+      if (row[t - 1] != 0.0) { c[q] = row[t - 1]; b[q] = nodebuf[t]; q++; }
+    }
+    return q;
+  }
+
+  // ---- degree-optimal polynomial (schemes.py:104-126) + fused epilogue ------------------
+  // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp, one product).
+  // Free buffers bR (combination temp) and bfree[0..2] hold P4..P6.  The last node stays in
+  // registers; the epilogue forms z, scales by `mult` (= -2^s), reverts the balancing
+  // (matcore.py:175-177) when `scales` is set and writes row-major to Lg (ld).
+  __device__ void degopt(int k, int bX, int b3, bool have_fp, int bR, const int (&bfree)[3], double mult,
+                         bool unbal, double* Lg, long long ldg, int& products) {
+    int nodebuf[8] = {0, 0, bX, b3, bfree[0], bfree[1], bfree[2], 0};
+    double acc[NMAX / 2];
+    double c[MAXT], c0;
+    int b[MAXT];
+    if (!have_fp) {  // P3 = P2 * P2
+      c[0] = 1.0; b[0] = bX;
+      for (int q = 1; q < MAXT; ++q) { c[q] = 0.0; b[q] = bX; }
+      gemm_comb(1, c, b, 0.0, buf(bX), acc);
+      products++;
+      __syncthreads();
+      if (row < n) {
+        double* D = buf(b3) + row * C::LDM + team * (NMAX / 2);
+#pragma unroll
+        for (int jj = 0; jj < NMAX / 2; ++jj) if (team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
+      }
+      __syncthreads();
+    }
+    int nn = 3;  // nodes P1..P3 available
+    bool last_in_regs = false;
+    for (int j = 1; j < k; ++j) {
+      const double* lrow = lgm_lhs(*P, k, j);
+      const double* rrow = lgm_rhs(*P, k, j);
+      int nt = gather_terms(rrow, nn, nodebuf, c, b, c0);
+      combine_into(bR, nt, c, b, c0);
+      __syncthreads();
+      nt = gather_terms(lrow, nn, nodebuf, c, b, c0);
+      gemm_comb(nt, c, b, c0, buf(bR), acc);
+      products++;
+      nn++;
+      __syncthreads();
+      if (j < k - 1) {
+        if (row < n) {
+          double* D = buf(nodebuf[nn]) + row * C::LDM + team * (NMAX / 2);
+#pragma unroll
+          for (int jj = 0; jj < NMAX / 2; ++jj) if (team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
+        }
+        __syncthreads();
+      } else {
+        last_in_regs = true;
+      }
+    }
+    // epilogue: z = sum out[t] P_t + out[0] I, L = mult * z * (scale_i / scale_j) into bR
+    const double* orow = lgm_out(*P, k);
+    const double* sc = scale();
+    double* S = buf(bR);
+    if (row < n) {
+      const int col0 = team * (NMAX / 2);
+#pragma unroll
+      for (int jj = 0; jj < NMAX / 2; ++jj) {
+        const int col = col0 + jj;
+        if (col < n) {
+          double v = 0.0;
+          for (int t = 2; t <= nn; ++t) {
+            double ct = orow[t - 1];
+            if (ct != 0.0) {
+              double pv = (t == nn && last_in_regs) ? acc[jj] : buf(nodebuf[t])[row * C::LDM + col];
+              v = __dadd_rn(v, __dmul_rn(ct, pv));
+            }
+          }
+          if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
+          v = mult * v;
+          if (unbal) v = v * (sc[row] / sc[col]);
+          S[row * C::LDM + col] = v;
+        }
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, jcol = idx - i * n;
+      Lg[(long long)i * ldg + jcol] = S[i * C::LDM + jcol];
+    }
+  }
+
+  // ---- load / store --------------------------------------------------------------------
+  __device__ bool load(int b, const double* Ag, long long ldg) {
+    double* D = buf(b);
+    bool bad = false;
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      double v = Ag[(long long)i * ldg + j];
+      bad |= !isfinite(v);
+      D[i * C::LDM + j] = v;
+    }
+    return __syncthreads_or(bad);
+  }
+  __device__ void store(int b, double* Dg, long long ldg) {
+    const double* S = buf(b);
+    for (int idx = tid; idx < n * n; idx += C::NT) {
+      int i = idx / n, j = idx - i * n;
+      Dg[(long long)i * ldg + j] = S[i * C::LDM + j];
+    }
+  }
+
+  // ---- Algorithm 1 (oracle/driver.py logm_status) ----------------------------------------
+  __device__ double alpha(int bB, bool have_ai2, int bAI2, double nA, int m, double theta,
+                          double (&cache)[16], unsigned& cvalid, int& nest, int& passes) {
+    const int itmax = P->est_itmax;
+    double t1, Pm;
+    if (have_ai2) {
+      double nI2 = onenorm(bAI2, 0.0);
+      double r2 = sqrt(nI2);
+      if (le(r2, theta)) {  // Eq. 27
+        t1 = r2;
+        Pm = pow(nI2, (double)(m / 2));
+      } else {
+        if (!((cvalid >> m) & 1u)) {
+          nest++;
+          double e = 0.0;
+          if (any_nonzero(bAI2, 0.0)) e = estimate(bAI2, 0.0, m / 2, false, bB, 1.0, itmax, passes);
+          cache[m] = e; cvalid |= 1u << m;
+        }
+        Pm = cache[m];
+        t1 = pow(Pm, 1.0 / m);
+      }
+    } else {
+      if (!((cvalid >> m) & 1u)) {
+        nest++;
+        double e = 0.0;
+        if (any_nonzero(bB, 1.0)) e = estimate(bB, 1.0, m, false, bB, 1.0, itmax, passes);
+        cache[m] = e; cvalid |= 1u << m;
+      }
+      Pm = cache[m];
+      t1 = pow(Pm, 1.0 / m);
+    }
+    note(t1, theta);
+    if (t1 > theta) return t1;
+    double bound = pow(Pm * nA, 1.0 / (m + 1));  // Eq. 28
+    double t2;
+    if (le(bound, theta)) {
+      t2 = bound;
+    } else {
+      if (!((cvalid >> (m + 1)) & 1u)) {
+        nest++;
+        double e;
+        if (have_ai2) {
+          e = estimate(bAI2, 0.0, m / 2, true, bB, 1.0, itmax, passes);
+        } else {
+          e = 0.0;
+          if (any_nonzero(bB, 1.0)) e = estimate(bB, 1.0, m + 1, false, bB, 1.0, itmax, passes);
+        }
+        cache[m + 1] = e; cvalid |= 1u << (m + 1);
+      }
+      t2 = pow(cache[m + 1], 1.0 / (m + 1));
+    }
+    return fmax(t1, t2);
+  }
+
+  __device__ int first_index(double x, int K) {
+    for (int j = 1; j <= K; ++j)
+      if (le(x, P->theta[j - 1])) return j;
+    return K;
+  }
+
+  // returns k; cert = alpha certifying k
+  __device__ int select(int bB, int bAI2, double nA, double alpha_loop, double (&cache)[16], unsigned& cvalid,
+                        int& nest, int& passes, double& cert) {
+    const int K = P->max_k;
+    const double* th = P->theta;
+    const int* mk = P->order;
+    double nI2 = onenorm(bAI2, 0.0);
+    double r2 = sqrt(nI2);
+    int mK = mk[K - 1];
+    int min_im;
+    if ((cvalid >> mK) & 1u) {
+      min_im = first_index(pow(cache[mK], 1.0 / mK), K);
+      if ((cvalid >> (mK + 1)) & 1u) {
+        int m2 = first_index(pow(cache[mK + 1], 1.0 / (mK + 1)), K);
+        min_im = min_im > m2 ? min_im : m2;
+      }
+    } else {
+      min_im = first_index(r2, K);
+    }
+    const int tabmin[5] = {1, 2, 3, 4, 4};
+    min_im = tabmin[min_im - 1];
+    note(r2, th[0]);
+    min_im = (r2 > th[0]) ? (min_im > 2 ? min_im : 2) : 1;
+    int max_in = K;
+    double max_bound = -1.0;
+    bool found = false;
+    for (int j = 1; j <= K; ++j) {
+      int m = mk[j - 1];
+      double bnd = pow(pow(nI2, (double)(m / 2)) * nA, 1.0 / (m + 1));
+      if (le(bnd, th[j - 1])) { max_in = j; max_bound = bnd; found = true; break; }
+    }
+    double cert_max = found ? max_bound : alpha_loop;
+    if (min_im >= max_in) { cert = cert_max; return max_in; }
+    for (int j = min_im; j < max_in; ++j) {
+      double a = alpha(bB, true, bAI2, nA, mk[j - 1], th[j - 1], cache, cvalid, nest, passes);
+      if (le(a, th[j - 1])) { cert = a; return j; }
+      if (le(a, th[j])) { cert = a; return j + 1; }
+    }
+    cert = cert_max;
+    return max_in;
+  }
+};
+
+// Buffer roles in the fused logm kernel
+enum { BUF_B = 0, BUF_Y = 1, BUF_P = 2, BUF_4 = 3, BUF_5 = 4, BUF_6 = 5 };
+
+template <int NMAX>
+__device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep) {
+  const LgmParams& P = *c.P;
+  lgm_report R = {};
+  R.balanced = P.balance;
+  int n = c.n;
+  c.zero_all();
+  __syncthreads();
+  if (c.load(BUF_B, Ag, ld)) {
+    R.status = LGM_NONFINITE;
+    if (c.tid == 0) *rep = R;
+    return;
+  }
+  if (P.balance) R.balance_sweeps = c.balance(BUF_B, 100);
+  else {
+    for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
+    __syncthreads();
+  }
+  const int K = P.max_k;
+  const double thK = P.theta[K - 1];
+  const int mK = P.order[K - 1];
+  const double tol = P.db_tol > 0.0 ? P.db_tol : 10.0 * n * LGM_UNIT_ROUNDOFF;
+  double cache[16];
+  unsigned cvalid = 0u;
+  int nest = 0, passes = 0, s = 0, db_iters = 0, products = 0;
+  bool have_ai2 = false;
+  double alpha_loop = c.onenorm(BUF_B, 1.0);
+  bool finish = c.le(alpha_loop, thK);
+  int status = 0;
+  while (!finish && s < P.maxiter_s) {
+    double nA = c.onenorm(BUF_B, 1.0);
+    double a = c.alpha(BUF_B, have_ai2, BUF_P, nA, mK, thK, cache, cvalid, nest, passes);
+    alpha_loop = a;
+    finish = c.le(a, thK);
+    if (!finish) {
+      c.copy_buf(BUF_P, BUF_B);
+      __syncthreads();
+      int its = 0;
+      status = c.sqrt_db(BUF_B, BUF_Y, tol, P.db_maxiter, its);
+      db_iters += its;
+      if (status) break;
+      s++;
+      // A_I2 = A_prev - 2 B + I, in place over A_prev
+      {
+        double* Pm = c.buf(BUF_P);
+        const double* Bm = c.buf(BUF_B);
+        for (int idx = c.tid; idx < n * n; idx += Cfg<NMAX>::NT) {
+          int i = idx / n, j = idx - i * n;
+          double v = Pm[i * Cfg<NMAX>::LDM + j] - 2.0 * Bm[i * Cfg<NMAX>::LDM + j];
+          if (i == j) v = v + 1.0;
+          Pm[i * Cfg<NMAX>::LDM + j] = v;
+        }
+      }
+      have_ai2 = true;
+      cvalid = 0u;
+      __syncthreads();
+    }
+  }
+  R.s = s;
+  R.db_iters = db_iters;
+  R.divisions = 2 * db_iters;
+  R.norm_estimations = nest;
+  R.estimation_passes = passes;
+  if (status || !finish) {
+    R.status = status ? status : LGM_SCALING_MAXITER;
+    R.min_margin = c.mm;
+    R.db_plateau = c.plateau;
+    if (c.tid == 0) *rep = R;
+    return;
+  }
+  const double nA = c.onenorm(BUF_B, 1.0);
+  if (!have_ai2) {  // s = 0: A_I2 = (B - I)(B - I), one product
+    double cc[Ctx<NMAX>::MAXT] = {1.0};
+    int bb[Ctx<NMAX>::MAXT] = {BUF_B};
+    double acc[NMAX / 2];
+    c.combine_into(BUF_Y, 1, cc, bb, -1.0);
+    __syncthreads();
+    c.gemm_comb(1, cc, bb, -1.0, c.buf(BUF_Y), acc);
+    products++;
+    if (c.row < n) {
+      double* D = c.buf(BUF_P) + c.row * Cfg<NMAX>::LDM + c.team * (NMAX / 2);
+#pragma unroll
+      for (int jj = 0; jj < NMAX / 2; ++jj) if (c.team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
+    }
+    __syncthreads();
+  }
+  double cert = 0.0;
+  const int k = c.select(BUF_B, BUF_P, nA, alpha_loop, cache, cvalid, nest, passes, cert);
+  // P2 = I - B (the schemes approximate -log(I - X), schemes.py:129-131); B is dead now.
+  {
+    double* Bm = c.buf(BUF_B);
+    for (int idx = c.tid; idx < n * n; idx += Cfg<NMAX>::NT) {
+      int i = idx / n, j = idx - i * n;
+      double v = Bm[i * Cfg<NMAX>::LDM + j];
+      Bm[i * Cfg<NMAX>::LDM + j] = (i == j) ? 1.0 - v : -v;
+    }
+  }
+  __syncthreads();
+  const int bfree[3] = {BUF_4, BUF_5, BUF_6};
+  c.degopt(k, BUF_B, BUF_P, true, BUF_Y, bfree, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
+  R.k = k;
+  R.alpha_used = cert;
+  R.products = products;
+  R.norm_estimations = nest;
+  R.estimation_passes = passes;
+  R.min_margin = c.mm;
+  R.db_plateau = c.plateau;
+  R.status = 0;
+  if (c.tid == 0) *rep = R;
+}
+
+}  // namespace lgm

@@ -1,0 +1,256 @@
+"""GPU parity: every CUDA building block and the fused logm vs the oracle / reference goldens.
+
+Run on a B200: ``python -m pytest tests -m gpu``.  All calls go through the C ABI
+(paper_2401_10089_b200/_build/liblogmpoly_b200.so).  Tolerances:
+* balance: bit-identical B and scales (same pairwise sums as numpy, exact radix-2 scaling);
+* estimator: equal pass counts, estimate within 1e-12 relative (thin products round
+  differently from OpenBLAS; the discrete picks must agree);
+* sqrt_db: equal iteration count, X within 1e-12 relative (Frobenius);
+* eval_degopt: equal product count, Z within 1e-13 relative;
+* logm: status/s/k/db_iters/counters equal except near-threshold exemptions (tests/parity.py),
+  ||L - L_oracle||_F / ||L_oracle||_F <= max(1e-12, 10 cond_log u).
+"""
+import numpy as np
+import pytest
+
+from tests.parity import classify, rel_err, tolerance
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU hosts
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2401_10089_b200 as lp  # noqa: E402
+from oracle import driver as D  # noqa: E402
+from oracle import primitives as P  # noqa: E402
+from paper_2401_10089_b200 import constants as C  # noqa: E402
+from paper_2401_10089_b200 import synth  # noqa: E402
+
+
+# ------------------------------------------------------------------------ building blocks
+
+@pytest.mark.parametrize("n", [1, 5, 17, 32, 64])
+def test_balance_bitwise_vs_reference(golden, n):
+    A = golden[f"prim/balance/{n}/A"]
+    B, sc, sw = lp.balance_batched(A)
+    assert np.array_equal(B, golden[f"prim/balance/{n}/B"])
+    assert np.array_equal(sc[0], golden[f"prim/balance/{n}/scale"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 32, 64])
+@pytest.mark.parametrize("p", [1, 2, 7, 14])
+def test_est_power_norm_vs_reference(golden, n, p):
+    key = f"prim/est_power/{n}/{p}"
+    c = lp.OpCounter()
+    v = lp.est_power_norm(golden[key + "/M"], p, counter=c)
+    ref = float(golden[key + "/val"])
+    assert v == pytest.approx(ref, rel=1e-12)
+    assert c.estimation_passes == int(golden[key + "/passes"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 32, 64])
+def test_est_product_norm_vs_reference(golden, n):
+    key = f"prim/est_product/{n}"
+    c = lp.OpCounter()
+    v = lp.est_product_norm([(golden[key + "/M1"], 7), (golden[key + "/M2"], 1)], counter=c)
+    assert v == pytest.approx(float(golden[key + "/val"]), rel=1e-12)
+    assert c.estimation_passes == int(golden[key + "/passes"])
+
+
+def test_est_power_norm_exact_cases():
+    D4 = np.diag([0.5, -2.0, 1.5, 0.1])                       # SPEC.md:90 diagonal exact
+    assert lp.est_power_norm(D4, 3) == pytest.approx(8.0, rel=1e-15)
+    assert lp.est_power_norm(np.zeros((5, 5)), 4) == 0.0
+    rng = np.random.default_rng(3)                             # SPEC.md:92 lower bound within 10x
+    Ms = rng.standard_normal((200, 8, 8))
+    est, _ = lp.primitives._est(Ms, 4, None, 5, True)
+    for M, e in zip(Ms, est):
+        true = np.abs(np.linalg.matrix_power(M, 4)).sum(axis=0).max()
+        assert true / 10 <= e <= true * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 32, 64])
+def test_sqrt_db_vs_reference(golden, n):
+    A = golden[f"prim/sqrt_db/{n}/A"]
+    X, its, st = lp.sqrt_db_batched(A)
+    assert st[0] == 0
+    assert 2 * its[0] == int(golden[f"prim/sqrt_db/{n}/divisions"])
+    assert rel_err(X, golden[f"prim/sqrt_db/{n}/X"]) <= 1e-12
+
+
+def test_sqrt_db_identity_and_diag():
+    X, its, st = lp.sqrt_db_batched(np.eye(6))
+    assert its[0] == 1 and st[0] == 0 and np.array_equal(X, np.eye(6))
+    X = lp.sqrt_db(np.diag([4.0, 9.0]))
+    assert np.abs(X - np.diag([2.0, 3.0])).max() <= 100 * 2.0 ** -53 * 3
+
+
+def test_sqrt_db_residual_acceptance_11():
+    rng = np.random.default_rng(11)                            # SPEC.md acceptance 11
+    As = []
+    for _ in range(30):
+        n = int(rng.integers(2, 65))
+        G = rng.standard_normal((n, n))
+        As.append(np.eye(n) * 2 + G / np.linalg.norm(G, 2))
+    for A in As:
+        X = lp.sqrt_db(A)
+        kappa = np.linalg.cond(A, 1)
+        assert np.abs(X @ X - A).sum(axis=0).max() / np.abs(A).sum(axis=0).max() <= 1e3 * 2.0 ** -53 * kappa
+
+
+def test_sqrt_db_failure_statuses():
+    _, its, st = lp.sqrt_db_batched(np.diag([-1.0, 2.0, 3.0]))
+    assert st[0] == 2 and its[0] == 50
+    Z = np.eye(4)
+    Z[2, :] = 0.0
+    _, its, st = lp.sqrt_db_batched(Z)
+    assert st[0] == 1 and its[0] == 0
+    _, its, st = lp.sqrt_db_batched(np.array([[1.0, np.inf], [0.0, 1.0]]))
+    assert st[0] == 4
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("n", [3, 32])
+def test_eval_degopt_vs_reference(golden, k, n):
+    key = f"prim/degopt/{k}/{n}"
+    X = golden[key + "/X"]
+    c1, c2 = lp.OpCounter(), lp.OpCounter()
+    Z = lp.eval_degopt(k, X, counter=c1)
+    Z2 = lp.eval_degopt(k, X, counter=c2, first_product=X @ X)
+    assert rel_err(Z, golden[key + "/Z"]) <= 1e-13
+    assert rel_err(Z2, golden[key + "/Zfp"]) <= 1e-13
+    assert [c1.products, c2.products] == list(golden[key + "/products"])
+
+
+# ------------------------------------------------------------------------ fused logm
+
+def _check_against_oracle(As, L, reps, allow_mismatch=0):
+    counts = {"match": 0, "exempt": 0, "db_plateau": 0, "mismatch": 0}
+    worst = 0.0
+    for b in range(As.shape[0]):
+        Lr, rr = D.logm_status(As[b], D.default_prims())
+        cls, g, o = classify(reps[b], rr)
+        counts[cls] += 1
+        if cls == "mismatch":
+            print("MISMATCH", b, "gpu", g, "oracle", o, "margins", float(reps[b]["min_margin"]), rr["min_margin"])
+        both_ok = rr["status"] == 0 and int(reps[b]["status"]) == 0
+        same_sk = (g["s"], g["k"]) == (o["s"], o["k"])
+        if both_ok and (cls == "match" or (cls == "db_plateau" and same_sk)):
+            e = rel_err(L[b], Lr)
+            tol = tolerance(As[b], Lr)
+            worst = max(worst, e / tol)
+            assert e <= tol, (b, e, tol)
+    print(counts, "worst err/tol", worst)
+    assert counts["mismatch"] <= allow_mismatch, counts
+    return counts
+
+
+def test_logm_golden_driver_cases(golden):
+    names = [str(s) for s in golden["drv_names"]]
+    fields = [str(f) for f in golden["drv_fields"]]
+    for name in names:
+        A = golden[f"drv/{name}/A"]
+        opts = lp.LogmOptions(raise_on_error=False)
+        L, reps = lp.logm_batched(A[None], opts)
+        rec = reps[0]
+        gold = dict(zip(fields, (int(v) for v in golden[f"drv/{name}/ints"])))
+        Lr, rr = D.logm_status(A, D.default_prims())
+        assert {f: rr[f] for f in fields} == gold, name       # oracle == reference composition
+        cls, g, o = classify(rec, rr)
+        assert cls != "mismatch", (name, g, o, float(rec["min_margin"]), rr["min_margin"])
+        if gold["status"] == 0 and cls == "match":  # (db_plateau cases: s, k still compared below)
+            Lg = golden[f"drv/{name}/L"]
+            assert rel_err(L[0], Lg) <= tolerance(A, Lg), name
+            assert float(rec["alpha_used"]) <= C.THETA[int(rec["k"]) - 1]
+
+
+def test_logm_config2_batch_vs_oracle():
+    A = synth.config(2, batch=256)
+    L, reps = lp.logm_batched(A)
+    _check_against_oracle(A, L, reps)
+
+
+def test_logm_config1_vs_oracle():
+    A = synth.config(1)
+    L, reps = lp.logm_batched(A)
+    _check_against_oracle(A, L, reps)
+
+
+@pytest.mark.parametrize("c,n", [("3b", 32), (4, 48), ("3b", 64), (4, 64)])
+def test_logm_small_config_shapes_vs_oracle(c, n):
+    A = synth.config(c, batch=16, n=n)
+    L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    _check_against_oracle(A, L, reps)
+
+
+def test_logm_ragged_sizes_vs_oracle():
+    rng = np.random.default_rng(99)
+    for n in (1, 2, 3, 7, 15, 31, 33, 47, 63):
+        A = np.stack([synth.near_identity(rng, n) for _ in range(4)])
+        L, reps = lp.logm_batched(A)
+        _check_against_oracle(A, L, reps)
+
+
+def test_logm_full_config2_properties():
+    """Full BASELINE config 2 (4096 x 32^2): size-independent properties -- all OK, k = 5 with
+    s >= 1, alpha_used <= Theta_k, product accounting, expm(L) round trip on the GPU."""
+    A = synth.config(2)
+    Ad = torch.from_numpy(A).cuda()
+    L, reps = lp.logm_batched(Ad)
+    assert (reps["status"] == 0).all()
+    assert (reps["alpha_used"] <= np.array(C.THETA)[reps["k"] - 1]).all()
+    assert (reps["products"] == np.where(reps["s"] >= 1, reps["k"] - 1, reps["k"])).all()
+    assert (reps["divisions"] == 2 * reps["db_iters"]).all()
+    E = torch.linalg.matrix_exp(L)
+    res = torch.linalg.matrix_norm(E - Ad) / torch.linalg.matrix_norm(Ad)
+    assert float(res.max()) <= 1e-13
+
+
+def test_logm_batch_invariance_and_determinism():
+    A = synth.config(2, batch=64)
+    L1, r1 = lp.logm_batched(A)
+    L2, r2 = lp.logm_batched(A[17:18])
+    L3, r3 = lp.logm_batched(A)
+    assert np.array_equal(L1[17], L2[0]) and r1[17].tobytes() == r2[0].tobytes()
+    assert np.array_equal(L1, L3)
+
+
+def test_logm_spec_examples():
+    L, rep = lp.logm(np.eye(5))
+    assert np.array_equal(L, np.zeros((5, 5))) and (rep.s, rep.k_selected, rep.alpha_used) == (0, 1, 0.0)
+    rng = np.random.default_rng(4)
+    for n in (16, 24, 40, 64):                                 # SPEC.md:453, acceptance 6
+        A, Lex = synth.known_log(rng, n, kappa=10.0)
+        L, rep = lp.logm(A)
+        assert np.linalg.norm(L - Lex, 2) / np.linalg.norm(Lex, 2) <= 1e3 * 100 * 2.0 ** -53
+    S = synth.spd(rng, 20, -1, 1)                              # logm(A^2) = 2 logm(A)
+    L1, _ = lp.logm(S)
+    L2, _ = lp.logm(S @ S)
+    assert np.linalg.norm(L2 - 2 * L1) / np.linalg.norm(2 * L1) <= 1e4 * 2.0 ** -53
+
+
+def test_logm_errors_map_to_reference_exceptions():
+    with pytest.raises(ValueError):
+        lp.logm(np.array([[1.0, np.nan], [0.0, 1.0]]))
+    with pytest.raises(lp.ConvergenceError) as ei:
+        lp.logm(np.diag([-1.0, 2.0, 3.0]))
+    assert ei.value.report is not None
+    Z = np.eye(4)
+    Z[2, :] = 0.0
+    with pytest.raises(lp.SingularMatrixError):
+        lp.logm(Z)
+    with pytest.raises(ValueError):
+        lp.logm(np.ones((2, 3)))
+    A = np.stack([np.eye(3), np.diag([-1.0, 2.0, 3.0])])
+    L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    assert list(reps["status"]) == [0, 2]
+
+
+def test_logm_torch_in_torch_out_and_options():
+    A = torch.from_numpy(synth.config(2, batch=8)).cuda()
+    L, reps = lp.logm_batched(A, lp.LogmOptions(balance=False))
+    assert L.is_cuda and L.dtype == torch.float64 and not reps["balanced"].any()
+    L5, _ = lp.logm_batched(A, lp.LogmOptions(max_k=4))
+    _, r4 = lp.logm_batched(A, lp.LogmOptions(max_k=4))
+    assert (r4["k"] <= 4).all()
