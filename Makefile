@@ -21,3 +21,13 @@ clean:
 	rm -rf $(OUT)
 
 .PHONY: all clean
+
+# phase-profiling variant (clock64 per Algorithm-1 phase; tools/phase_prof.py)
+PROF := $(OUT)/liblogmpoly_b200_prof.so
+prof: $(PROF)
+$(PROF): $(SRC)/lgm_api.cu $(SRC)/lgm_grid.cu $(wildcard $(SRC)/*.cuh $(SRC)/*.h) include/logmpoly_b200.h
+	@mkdir -p $(OUT)
+	$(NVCC) $(NVFLAGS) -DLGM_PHASE_PROF -c $(SRC)/lgm_api.cu -o $(OUT)/lgm_api_prof.o
+	$(NVCC) $(NVFLAGS) -DLGM_PHASE_PROF -c $(SRC)/lgm_grid.cu -o $(OUT)/lgm_grid_prof.o
+	$(NVCC) $(ARCH) -shared -o $@ $(OUT)/lgm_api_prof.o $(OUT)/lgm_grid_prof.o
+.PHONY: prof

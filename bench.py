@@ -1,0 +1,353 @@
+"""Benchmark: batched FP64 logm throughput (matrices/s) on B200, BASELINE.json's metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One *step* = one pass of the whole logm hot path (balance -> scaling loop with norm
+estimation and DB square roots -> order selection -> graph polynomial -> 2^s rescale ->
+unbalance) over one batch of matrices already resident in HBM.  Default workload is
+BASELINE.json configs[1] (config 2: 4096 float64 32x32 near-identity matrices per GPU,
+weak scaling: each rank owns its own 4096-matrix shard, no data-path collective).
+Under torchrun each rank drives one GPU; timings are CUDA events on the launching
+stream, the max over ranks is reported.  The L2 (126 MB) is flushed between timed steps
+(256 MiB write) since the config-2 batch (32 MiB) would otherwise stay L2 resident.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the oracle port
+of the reference primitives + restated driver, oracle/; the reference's own driver file
+is missing) on all host cores over a bounded sample of the same workload.
+"""
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fp64 logm matrices/sec (batched, n=32..4096); achieved FP64 tensor TFLOP/s"
+UNIT = "matrices/s"
+
+
+def _peak_fp64():
+    """Measured FP64 peak (tools/fp64_peak.cu): MEASURED_PEAKS.json has no FP64 entry."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+    try:
+        d = json.load(open(p))
+        return float(d["dmma_tflops"]), "measured: profiles/fp64_peak_r01.json dmma_tflops (DMMA.8x8x4 microbenchmark)"
+    except Exception:  # noqa: BLE001
+        return 36.9, "fallback: round-1 DMMA microbenchmark"
+
+
+def _peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+def workload(cfg, batch=None, n=None, seed_offset=0):
+    from paper_2401_10089_b200 import synth
+    name, n0, b0 = synth.CONFIGS[cfg]
+    n = n or n0
+    batch = batch or b0
+    seed = synth.SEEDS[cfg] + 7919 * seed_offset
+    return synth.config(cfg, batch=batch, n=n, seed=seed), name
+
+
+def flops_per_matrix(n, rec):
+    """F = 2n^3 [sum_r (2 it_r - 1) + (k - 1) + 1(s = 0)] + 4 n^2 E."""
+    s, its, k, E = int(rec["s"]), int(rec["db_iters"]), int(rec["k"]), int(rec["estimation_passes"])
+    if int(rec["status"]) != 0:
+        # failed matrices: the DB work actually done (every iteration after the first of a
+        # root inverts both X and Y)
+        return 2.0 * n ** 3 * max(2 * its - (s + 1), 0) + 4.0 * n * n * E
+    return 2.0 * n ** 3 * ((2 * its - s) + (k - 1) + (1 if s == 0 else 0)) + 4.0 * n * n * E
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled in the background (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [v for v in sm if v > 600] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU side
+
+def _cpu_worker_init():
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+
+
+def _cpu_worker(chunk):
+    from oracle import driver as D
+    prims = D.default_prims()
+    ok = 0
+    for A in chunk:
+        prims.margins = type(prims.margins)()
+        _, rep = D.logm_status(A, prims)
+        ok += rep["status"] == 0
+    return ok
+
+
+def cpu_time(As, cores):
+    """Time the oracle port over matrices As with a pool of `cores` single-BLAS-thread
+    workers (mode 2 of BASELINE.md section 2).  Returns wall seconds."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    chunks = [c for c in np.array_split(As, max(1, min(len(As), cores * 4))) if len(c)]
+    with ctx.Pool(cores, initializer=_cpu_worker_init) as pool:
+        pool.map(_cpu_worker, [chunks[0][:1]] * cores)          # warm the workers
+        t0 = time.perf_counter()
+        pool.map(_cpu_worker, chunks)
+        return time.perf_counter() - t0
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--batch", type=int, default=None, help="matrices per GPU (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=None)
+    args = ap.parse_args()
+    cfg = args.config if args.config in ("3b", "5b") else int(args.config)
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2401_10089_b200 as lp
+    from paper_2401_10089_b200 import _lib, driver
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    A_np, name = workload(cfg, batch=args.batch, seed_offset=rank)
+    B, n, _ = A_np.shape
+    A = torch.from_numpy(A_np).to(dev)
+    opts = lp.LogmOptions(raise_on_error=False)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def step():
+        return driver.run_device(A, opts, stream)
+
+    for _ in range(args.warmup):
+        L, rep, ws = step()
+    torch.cuda.synchronize()
+    reps = rep.cpu().numpy().view(_lib.REPORT_DTYPE)[:B]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    times = []
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            L, rep, ws = step()
+            e1.record(stream)
+            times.append((e0, e1))
+        barrier()
+    kernel_ms = [a.elapsed_time(b) for a, b in times]
+    total_ms = sum(kernel_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant (only) kernel: algorithmic FLOPs per launch / launch time
+    F = sum(flops_per_matrix(n, r) for r in reps)
+    peak, peak_src = _peak_fp64()
+    avg_launch_s = (sum(kernel_ms) / len(kernel_ms)) * 1e-3
+    achieved = F / avg_launch_s / 1e12
+    hbm_peak, hbm_src = _peak_hbm()
+    alg_bytes = B * (16.0 * n * n + _lib.REPORT_DTYPE.itemsize)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")))
+        traffic = tr.get(str(args.config), {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        pass
+
+    # end-to-end through the public API with host (pinned) buffers
+    A_host = torch.from_numpy(A_np).pin_memory()
+    for _ in range(2):
+        lp.logm_batched(A_host, opts)
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 20))):
+        barrier()
+        t0 = time.perf_counter()
+        Lh, rh = lp.logm_batched(A_host, opts)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B / float(te.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        sample = args.cpu_sample or (B if n <= 64 else max(4, min(B, 8)))
+        secs = cpu_time(A_np[:sample], cores)
+        cpu = {"value": sample / secs, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"first {sample} of the {B} config-{args.config} matrices, oracle port "
+                         f"(oracle/driver.py over numpy/scipy/OpenBLAS), process pool x{cores}, "
+                         f"OPENBLAS_NUM_THREADS=1, {secs:.2f} s wall"}
+
+    status_counts = {int(s): int(c) for s, c in zip(*np.unique(reps["status"], return_counts=True))}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy generator, synth.py)",
+        "config": {"workload": f"config{args.config}:{name}", "n": n, "batch_per_gpu": B,
+                   "global_batch": B * world, "parallelism": f"batch-sharded x{world} (no collective)",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "engine": "F (fused, 1 CTA/matrix)" if n <= 64 else "G (batched grid)"},
+        "achieved_tflops": achieved,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "logm_fused_kernel<32>" if n <= 32 else ("logm_fused_kernel<64>" if n <= 64 else "grid"),
+                     "alg_flops_per_launch": F,
+                     "hbm": {"achieved_gbs": alg_bytes / avg_launch_s / 1e9, "peak_gbs": hbm_peak,
+                             "frac": alg_bytes / avg_launch_s / 1e9 / hbm_peak, "alg_bytes_per_launch": alg_bytes,
+                             "peak_source": hbm_src}},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * n * n * 8),
+                "d2h_bytes_per_step": int(B * n * n * 8 + B * _lib.REPORT_DTYPE.itemsize)},
+        "gpu_launches": args.steps * (1 if n <= 64 else None or 1),
+        "clocks": clk.summary(),
+        "report_summary": {"status_counts": status_counts, "s_mean": float(reps["s"].mean()),
+                           "k_mean": float(reps["k"].mean()), "db_iters_mean": float(reps["db_iters"].mean()),
+                           "estimation_passes_mean": float(reps["estimation_passes"].mean())},
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, rank, world):
+    """The reference algorithm's CPU implementation on all host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    A_np, name = workload(cfg, batch=args.batch)
+    B, n, _ = A_np.shape
+    cores = host_cores()
+    sample = args.cpu_sample or (256 if n <= 64 else max(2, min(B, cores)))
+    sample = min(sample, B)
+    for _ in range(min(args.warmup, 1)):
+        cpu_time(A_np[:min(sample, cores)], cores)
+    secs = []
+    for s in range(args.steps):
+        lo = (s * sample) % B
+        chunk = A_np[lo:lo + sample] if lo + sample <= B else A_np[:sample]
+        secs.append(cpu_time(chunk, cores))
+    total = sum(secs)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generator, synth.py)",
+        "config": {"workload": f"config{args.config}:{name}", "n": n, "batch_per_gpu": B},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sample} matrices of config {args.config} per step, oracle port "
+                                   f"(oracle/driver.py: restated driver over the numpy/scipy restatement of the "
+                                   f"reference primitives), process pool x{cores}, OPENBLAS_NUM_THREADS=1"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

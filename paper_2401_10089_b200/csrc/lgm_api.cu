@@ -14,13 +14,14 @@ using namespace lgm;
 // ------------------------------------------------------------------------------ kernels
 
 template <int NMAX>
-__global__ void __launch_bounds__(Cfg<NMAX>::NT) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
-                                                                  lgm_report* rep, long long ld, int n, const __grid_constant__ LgmParams P) {
+__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 8 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
+                                                                  lgm_report* rep, long long ld, int n, double* ws,
+                                                                  const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];
   Ctx<NMAX> c;
   c.init(smem, n, &P);
   const long long b = blockIdx.x;
-  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b);
+  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 3 * n * n);
 }
 
 template <int NMAX>
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) est_kernel(const double* __rest
   double e = 0.0;
   bool go = true;
   if (zero_shortcut) go = c.any_nonzero(2, 0.0);  // matcore.py:309-310
-  if (go) e = c.estimate(2, 0.0, p1, M2 != nullptr, 0, 0.0, itmax, ps);
+  if (go) e = c.estimate(2, p1, M2 != nullptr, 0, itmax, ps);
   if (c.tid == 0) { est[b] = e; passes[b] = ps; }
 }
 
@@ -94,8 +95,9 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) degopt_kernel(const double* __r
   for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
   __syncthreads();
   int prods = 0;
-  const int bfree[3] = {BUF_4, BUF_5, BUF_6};
-  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, bfree, 1.0, false, Z + b * n * ld, ld, prods);
+  double* const extra[3] = {c.sm() + Cfg<NMAX>::SMEM_DOUBLES, c.sm() + Cfg<NMAX>::SMEM_DOUBLES + Cfg<NMAX>::MAT,
+                            c.sm() + Cfg<NMAX>::SMEM_DOUBLES + 2 * Cfg<NMAX>::MAT};
+  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, extra, Cfg<NMAX>::LDM, 1.0, false, Z + b * n * ld, ld, prods);
   if (c.tid == 0) products[b] = prods;
 }
 
@@ -129,10 +131,9 @@ static int check_launch() {
 }
 
 template <int NMAX, class K>
-static int prep(K kernel) {
-  static_assert(Cfg<NMAX>::SMEM_BYTES <= 227 * 1024, "shared memory budget");
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)Cfg<NMAX>::SMEM_BYTES);
+static int prep(K kernel, size_t bytes = Cfg<NMAX>::SMEM_BYTES) {
+  static_assert(Cfg<NMAX>::SMEM_BYTES_X <= 227 * 1024, "shared memory budget");
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   return e == cudaSuccess ? 0 : LGM_ERR_CUDA;
 }
 
@@ -158,7 +159,8 @@ int lgm_max_fused_n(void) { return 64; }
 
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
-  *bytes = n <= 64 ? 0 : lgm_grid_workspace_bytes(n, batch);
+  // n <= 64: one 3 n^2 slot per matrix for the polynomial nodes P4..P6 (L2 resident)
+  *bytes = n <= 64 ? (size_t)batch * 3 * n * n * sizeof(double) : lgm_grid_workspace_bytes(n, batch);
   return 0;
 }
 
@@ -187,18 +189,21 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
     return LGM_ERR_ARG;
   if (batch == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
+  size_t need = 0;
+  lgm_workspace_bytes(n, batch, &need);
+  if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
   if (n <= 32) {
     if (prep<32>(logm_fused_kernel<32>)) return LGM_ERR_CUDA;
-    logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n, P);
+    logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
+                                                                                    (double*)ws, P);
     return check_launch();
   }
   if (n <= 64) {
     if (prep<64>(logm_fused_kernel<64>)) return LGM_ERR_CUDA;
-    logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n, P);
+    logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
+                                                                                    (double*)ws, P);
     return check_launch();
   }
-  size_t need = lgm_grid_workspace_bytes(n, batch);
-  if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
   return lgm_grid_logm(A, L, n, batch, ld, P, rep, ws, s);
 }
 
@@ -262,8 +267,30 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
-  LGM_DISPATCH_SMALL(degopt_kernel, X, FP, Z, ld, (int)n, k, products, P);
+  if (n <= 32) {
+    if (prep<32>(degopt_kernel<32>, Cfg<32>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
+    degopt_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
+                                                                                                  k, products, P);
+    return check_launch();
+  }
+  if (n <= 64) {
+    if (prep<64>(degopt_kernel<64>, Cfg<64>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
+    degopt_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
+                                                                                                  k, products, P);
+    return check_launch();
+  }
   return lgm_grid_degopt(X, FP, Z, n, batch, ld, k, products, P, (cudaStream_t)stream);
 }
 
 }  // extern "C"
+
+#ifdef LGM_PHASE_PROF
+extern "C" int lgm_debug_phase_cycles(unsigned long long* out8, int reset) {
+  if (cudaMemcpyFromSymbol(out8, lgm::lgm_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess) return -2;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(lgm::lgm_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

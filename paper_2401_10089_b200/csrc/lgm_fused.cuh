@@ -19,13 +19,26 @@
 
 namespace lgm {
 
+#ifdef LGM_PHASE_PROF
+// cycles per phase summed over CTAs: 0 balance, 1 scaling-loop alpha, 2 sqrt_db, 3 select, 4 poly
+__device__ unsigned long long lgm_phase_cycles[8];
+#define LGM_PHASE_BEGIN(c) long long _lgm_t0 = clock64()
+#define LGM_PHASE_END(c, ph) do { if ((c).tid == 0) atomicAdd(&lgm_phase_cycles[ph], (unsigned long long)(clock64() - _lgm_t0)); } while (0)
+#else
+#define LGM_PHASE_BEGIN(c) do {} while (0)
+#define LGM_PHASE_END(c, ph) do {} while (0)
+#endif
+
+// Dynamic shared memory, referenced by symbol so every access compiles to LDS/STS.
+extern __shared__ __align__(16) double lgm_smem[];
+
 template <int NMAX>
 struct Cfg {
   static constexpr int T = NMAX / 32;     // warps per team
   static constexpr int NT = 64 * T;       // threads per CTA
   static constexpr int LDM = NMAX + 1;    // padded row stride (doubles)
   static constexpr int MAT = NMAX * LDM;  // doubles per matrix buffer
-  static constexpr int NBUF = 6;
+  static constexpr int NBUF = 3;          // B (X), Y, A_prev / A_I2
   // shared-memory carve-up (in doubles)
   static constexpr int OFF_PROW = NBUF * MAT;                // [2 teams][2][NMAX+2]
   static constexpr int PROW = NMAX + 2;
@@ -35,6 +48,8 @@ struct Cfg {
   static constexpr int OFF_INT = OFF_RED + 64;               // ints: piv[2][NMAX], misc[64]
   static constexpr int SMEM_DOUBLES = OFF_INT + (2 * NMAX + 64 + 1) / 2 + 1;
   static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
+  // kernels that keep the polynomial nodes P4..P6 in shared memory too (building blocks)
+  static constexpr size_t SMEM_BYTES_X = SMEM_BYTES + 3 * MAT * sizeof(double);
 };
 
 // misc int slots
@@ -48,24 +63,24 @@ enum { RD_LOGDET = 0 /* 2 */, RD_KEY = 4 /* [2 teams][4 slots] */, RD_CN = 12 /*
 template <int NMAX>
 struct Ctx {
   using C = Cfg<NMAX>;
-  double* sm;      // dynamic shared memory base
   int n;
   int tid, warp, lane, team, wit, row;  // wit = warp index in team, row = wit*32 + lane
   const LgmParams* P;
   double mm;       // running min margin (uniform)
   int plateau;     // DB stop tests in the noise band [tol/10, 10 tol] (uniform)
 
-  __device__ double* buf(int b) const { return sm + b * C::MAT; }
-  __device__ double* prow(int tm, int parity) const { return sm + C::OFF_PROW + (tm * 2 + parity) * C::PROW; }
-  __device__ double* vec(int v) const { return sm + C::OFF_VEC + v * NMAX; }
-  __device__ double* scale() const { return sm + C::OFF_SCALE; }
-  __device__ double* red() const { return sm + C::OFF_RED; }
-  __device__ int* ints() const { return reinterpret_cast<int*>(sm + C::OFF_INT); }
+  __device__ __forceinline__ static double* sm() { return lgm_smem; }
+  __device__ double* buf(int b) const { return sm() + b * C::MAT; }
+  __device__ double* prow(int tm, int parity) const { return sm() + C::OFF_PROW + (tm * 2 + parity) * C::PROW; }
+  __device__ double* vec(int v) const { return sm() + C::OFF_VEC + v * NMAX; }
+  __device__ double* scale() const { return sm() + C::OFF_SCALE; }
+  __device__ double* red() const { return sm() + C::OFF_RED; }
+  __device__ int* ints() const { return reinterpret_cast<int*>(sm() + C::OFF_INT); }
   __device__ int* piv(int tm) const { return ints() + tm * NMAX; }
   __device__ int* misc() const { return ints() + 2 * NMAX; }
 
   __device__ void init(double* smem, int n_, const LgmParams* p) {
-    sm = smem; n = n_; P = p;
+    (void)smem; n = n_; P = p;
     tid = threadIdx.x; warp = tid >> 5; lane = tid & 31;
     team = warp / C::T; wit = warp % C::T; row = wit * 32 + lane;
     mm = INFINITY;
@@ -91,20 +106,23 @@ struct Ctx {
 
   // ---- elementwise helpers ------------------------------------------------------------
   __device__ void zero_all() {
-    for (int i = tid; i < C::NBUF * C::MAT; i += C::NT) sm[i] = 0.0;
+    // matrices, pivot rows, estimator vectors and scales (padding must read as 0)
+    static_assert(C::OFF_RED % 2 == 0, "double2 zeroing");
+    double2* p = reinterpret_cast<double2*>(sm());
+    for (int i = tid; i < C::OFF_RED / 2; i += C::NT) p[i] = make_double2(0.0, 0.0);
   }
   __device__ void copy_buf(int dst, int src) {
     double* d = buf(dst);
     const double* s = buf(src);
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
       d[i * C::LDM + j] = s[i * C::LDM + j];
     }
   }
   __device__ void set_identity(int b) {
     double* d = buf(b);
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
       d[i * C::LDM + j] = (i == j) ? 1.0 : 0.0;
     }
   }
@@ -133,7 +151,28 @@ struct Ctx {
   }
 
   // ---- balancing (matcore.py:180-215), bit-identical decisions --------------------------
-  __device__ int balance(int b, int max_sweeps) {
+  // numpy pairwise sum of |p[i*stride]|, i < n <= 128 (lgm_common.cuh lgm_pairwise_block).
+  __device__ __forceinline__ double pw_abs_sum(const double* p, int stride) const {
+    if (n < 8) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += fabs(p[i * stride]);
+      return s;
+    }
+    double r0 = fabs(p[0]), r1 = fabs(p[stride]), r2 = fabs(p[2 * stride]), r3 = fabs(p[3 * stride]);
+    double r4 = fabs(p[4 * stride]), r5 = fabs(p[5 * stride]), r6 = fabs(p[6 * stride]), r7 = fabs(p[7 * stride]);
+    int i = 8;
+    const int m8 = n - (n % 8);
+    for (; i < m8; i += 8) {
+      const double* q = p + i * stride;
+      r0 += fabs(q[0]); r1 += fabs(q[stride]); r2 += fabs(q[2 * stride]); r3 += fabs(q[3 * stride]);
+      r4 += fabs(q[4 * stride]); r5 += fabs(q[5 * stride]); r6 += fabs(q[6 * stride]); r7 += fabs(q[7 * stride]);
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res += fabs(p[i * stride]);
+    return res;
+  }
+
+  __device__ __noinline__ int balance(int b, int max_sweeps) {
     double* B = buf(b);
     double* sc = scale();
     for (int i = tid; i < n; i += C::NT) sc[i] = 1.0;
@@ -145,8 +184,8 @@ struct Ctx {
       for (int i = 0; i < n; ++i) {
         // every thread evaluates the (pairwise-ordered) sums redundantly: uniform decisions
         double dg = fabs(B[i * C::LDM + i]);
-        double c = lgm_pairwise_sum([&](int r) { return fabs(B[r * C::LDM + i]); }, n) - dg;
-        double r = lgm_pairwise_sum([&](int q) { return fabs(B[i * C::LDM + q]); }, n) - dg;
+        double c = pw_abs_sum(B + i, C::LDM) - dg;
+        double r = pw_abs_sum(B + i * C::LDM, 1) - dg;
         if (c == 0.0 || r == 0.0) continue;
         double tot = c + r, f = 1.0;
         while (true) {
@@ -182,63 +221,95 @@ struct Ctx {
   // holds storage row `row` of the in-place result: Minv[q(row)][p_j] = r[j], where p_j is
   // the pivot row of step j (piv(team)[j]) and q(row) = my_step.  Returns 1 if an exact zero
   // pivot is met (matcore.py:124-125), else 0; logabsdet = sum log|pivot| (team-uniform).
+  // Rotate the register row left by KB columns (static moves; keeps code size bounded).
+  template <int KB>
+  __device__ __forceinline__ static void rotate_left(double (&r)[NMAX]) {
+    double t[KB];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) t[i] = r[i];
+#pragma unroll
+    for (int j = 0; j + KB < NMAX; ++j) r[j] = r[j + KB];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) r[NMAX - KB + i] = t[i];
+  }
+
+  // Implementation notes: the k loop runs over blocks of KB = 8 pivot steps; inside a block
+  // the pivot column is a static register (the row array is rotated left by KB after each
+  // block), so only one block's worth of code is emitted.  Row scaling is deferred: the
+  // pivot row is broadcast unscaled together with 1/pivot, the other rows fold 1/pivot into
+  // their multiplier, and the pivot row keeps raw values (its column-k entry set to 1) and
+  // is scaled once at the end -- the elimination is linear in each row, so this is the
+  // same Gauss-Jordan recurrence with different rounding.
   __device__ int gj_invert(double (&r)[NMAX], double& logabsdet, int& my_step) {
+    constexpr int KB = 8;
     bool used = false;
     my_step = -1;
-    double mylog = 0.0;
+    double mylog = 0.0, rowscale = 1.0;
     int* pv = piv(team);
     double* kslot = red() + RD_KEY + team * 4;
     int status = 0;
+    const int nblk = (n + KB - 1) / KB;
+#pragma unroll 1
+    for (int kb = 0; kb < NMAX / KB; ++kb) {
+      if (kb < nblk) {
 #pragma unroll
-    for (int k = 0; k < NMAX; ++k) {
-      if (k < n) {
-        bool cand = (row < n) && !used;
-        uint64_t key = cand ? lgm_key(fabs(r[k])) : 0ull;
-        int wl;
-        uint64_t kmax = lgm_warp_argmax(key, wl);
-        int prow_idx = wit * 32 + wl;
-        if (C::T > 1) {
-          if (lane == 0) {
-            reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
-            reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
+        for (int kk = 0; kk < KB; ++kk) {
+          const int k = kb * KB + kk;
+          const bool live = (k < n) && (status == 0);  // team-uniform
+          const bool cand = live && (row < n) && !used;
+          uint64_t key = cand ? lgm_key(fabs(r[kk])) : 0ull;
+          int wl;
+          uint64_t kmax = lgm_warp_argmax(key, wl);
+          int prow_idx = wit * 32 + wl;
+          if (C::T > 1) {
+            if (lane == 0) {
+              reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
+              reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
+            }
+            team_sync();
+            uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
+            uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
+            int r0 = reinterpret_cast<int*>(kslot + 2)[0];
+            int r1 = reinterpret_cast<int*>(kslot + 2)[1];
+            if (k1 > k0) { kmax = k1; prow_idx = r1; } else { kmax = k0; prow_idx = r0; }
           }
-          team_sync();
-          uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
-          uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
-          int r0 = reinterpret_cast<int*>(kslot + 2)[0];
-          int r1 = reinterpret_cast<int*>(kslot + 2)[1];
-          if (k1 > k0) { kmax = k1; prow_idx = r1; } else { kmax = k0; prow_idx = r0; }
-        }
-        if (kmax <= 1ull) { status = 1; break; }  // all remaining candidates exactly zero
-        double* pr = prow(team, k & 1);
-        if (row == prow_idx) {
-          used = true;
-          my_step = k;
-          double p = r[k];
-          mylog = log(fabs(p));
-          double inv = 1.0 / p;
+          if (live && kmax <= 1ull) status = 1;  // all remaining candidates exactly zero
+          if (live && status == 0) {  // team-uniform
+            double* pr = prow(team, k & 1);
+            const bool own = (row == prow_idx);
+            if (own) {  // one lane publishes its raw row and 1/pivot
+              used = true;
+              my_step = k;
+              const double p = r[kk];
+              mylog = p;  // log|p| taken once after the loop (one pivot per row)
+              rowscale = 1.0 / p;
 #pragma unroll
-          for (int j = 0; j < NMAX; ++j) r[j] = (j == k) ? inv : r[j] * inv;
+              for (int j = 0; j < NMAX; j += 2)
+                *reinterpret_cast<double2*>(pr + j) = make_double2(r[j], r[j + 1]);
+              pr[NMAX] = rowscale;
+              pv[k] = prow_idx;
+            }
+            team_sync();
+            // branch-free elimination: the owner uses g = 0 (row kept raw, scaled at the end)
+            const double g = own ? 0.0 : r[kk] * pr[NMAX];
 #pragma unroll
-          for (int j = 0; j < NMAX; j += 2)
-            *reinterpret_cast<double2*>(pr + j) = make_double2(r[j], r[j + 1]);
-          pv[k] = prow_idx;
-        }
-        team_sync();
-        if (row != prow_idx) {
-          double f = r[k];
-#pragma unroll
-          for (int j = 0; j < NMAX; j += 2) {
-            double2 p2 = *reinterpret_cast<const double2*>(pr + j);
-            if (j != k) r[j] = fma(-f, p2.x, r[j]);
-            if (j + 1 != k) r[j + 1] = fma(-f, p2.y, r[j + 1]);
+            for (int j = 0; j < NMAX; j += 2) {
+              double2 p2 = *reinterpret_cast<const double2*>(pr + j);
+              if (j != kk) r[j] = fma(-g, p2.x, r[j]);
+              if (j + 1 != kk) r[j + 1] = fma(-g, p2.y, r[j + 1]);
+            }
+            r[kk] = own ? 1.0 : -g;
           }
-          r[k] = -f * pr[k];
         }
       }
+      rotate_left<KB>(r);  // every block (also the skipped ones) -> net rotation NMAX = identity
+    }
+    if (rowscale != 1.0) {
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) r[j] *= rowscale;
     }
     // team sum of the pivots' log|.| (one per valid row)
-    double s = lgm_warp_sum(mylog);
+    double s = lgm_warp_sum(my_step >= 0 ? log(fabs(mylog)) : 0.0);
     if (C::T > 1) {
       team_sync();
       if (lane == 0) red()[RD_LOGDET + team * 2 + wit] = s;
@@ -294,7 +365,7 @@ struct Ctx {
   // ---- scaled coupled Denman-Beavers square root (sqrtm.py:27-78) ------------------------
   // X (buffer bx) is replaced by X^(1/2); buffer by is workspace (Y).  Returns status
   // (0, LGM_SINGULAR, LGM_DB_NOCONV, LGM_NONFINITE); iters = iterations performed.
-  __device__ int sqrt_db(int bx, int by, double tol, int maxiter, int& iters) {
+  __device__ __noinline__ int sqrt_db(int bx, int by, double tol, int maxiter, int& iters) {
     double* X = buf(bx);
     double* Y = buf(by);
     set_identity(by);
@@ -402,38 +473,58 @@ struct Ctx {
     return (i == j) ? v - sh : v;
   }
 
-  // y = M x (row-per-thread) or y = M^T x (column-per-thread) for the team's column, with
-  // M = buf - sh*I formed element-exactly like numpy's explicit B - I.
-  __device__ void thin(const double* M, double sh, bool trans, const double* x, double* y) {
-    if (row < n) {
-      double acc0 = 0.0, acc1 = 0.0;
-      const double dg = M[row * C::LDM + row] - sh;
-      const int rs = trans ? C::LDM : 1;                 // stride along the dot product
-      const double* Mr = trans ? M + row : M + row * C::LDM;
-      int j = 0;
-      for (; j + 1 < n; j += 2) {
-        double v0 = (j == row) ? dg : Mr[j * rs];
-        double v1 = (j + 1 == row) ? dg : Mr[(j + 1) * rs];
-        acc0 = fma(v0, x[j], acc0);
-        acc1 = fma(v1, x[j + 1], acc1);
+  // p successive thin products x <- M x (row-per-thread; M^T x: column-per-thread) for the
+  // team's estimator column.  The thread's row (column) of M is held in registers across
+  // the p products; x ping-pongs between xa and xb (smem, zero beyond n); on return xa
+  // holds the result.
+  __device__ __forceinline__ void apply_pow(const double* M, int p, bool trans, double*& xa, double*& xb) {
+    double m[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+      m[j] = (row < n && j < n) ? (trans ? M[j * C::LDM + row] : M[row * C::LDM + j]) : 0.0;
+    for (int q = 0; q < p; ++q) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int j = 0; j < NMAX; j += 4) {
+        const double2 x01 = *reinterpret_cast<const double2*>(xa + j);
+        const double2 x23 = *reinterpret_cast<const double2*>(xa + j + 2);
+        a0 = fma(m[j], x01.x, a0);
+        a1 = fma(m[j + 1], x01.y, a1);
+        a2 = fma(m[j + 2], x23.x, a2);
+        a3 = fma(m[j + 3], x23.y, a3);
       }
-      if (j < n) acc0 = fma((j == row) ? dg : Mr[j * rs], x[j], acc0);
-      y[row] = acc0 + acc1;
+      if (row < n) xb[row] = (a0 + a1) + (a2 + a3);
+      team_sync();
+      double* tt = xa;
+      xa = xb;
+      xb = tt;
     }
-    team_sync();
+  }
+
+  // buf(dst) = buf(src) - I, element-exact like numpy's B - I
+  __device__ void minus_identity(int dst, int src) {
+    double* D = buf(dst);
+    const double* S = buf(src);
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
+        double v = S[i * C::LDM + j];
+        D[i * C::LDM + j] = (i == j) ? v - 1.0 : v;
+      }
   }
 
   __device__ bool any_nonzero(int b, double sh) {
     bool nz = false;
     const double* M = buf(b);
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
       nz |= mat_el(M, i, j, sh) != 0.0;
     }
     return __syncthreads_or(nz);
   }
 
-  __device__ double estimate(int b1, double sh1, int p1, bool has2, int bA, double sh2, int itmax, int& passes) {
+  // Operator = M1^p1 [* MA] with M1 = buf(b1), MA = buf(bA) (matrices stored explicitly,
+  // e.g. A - I materialised like numpy's B - I).
+  __device__ __noinline__ double estimate(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
     const int t = n < 2 ? n : 2;
     const int total = p1 + (has2 ? 1 : 0);
     const double* M1 = buf(b1);
@@ -460,8 +551,9 @@ struct Ctx {
       if (team < ncols) {
         double* xa = vec(2 * team);
         double* xb = vec(2 * team + 1);
-        if (has2) { thin(MA, sh2, false, xa, xb); double* tt = xa; xa = xb; xb = tt; cur ^= 1; }
-        for (int q = 0; q < p1; ++q) { thin(M1, sh1, false, xa, xb); double* tt = xa; xa = xb; xb = tt; cur ^= 1; }
+        if (has2) { apply_pow(MA, 1, false, xa, xb); cur ^= 1; }
+        apply_pow(M1, p1, false, xa, xb);
+        cur ^= (p1 & 1);
         // column 1-norm (axis-0 sum); team reduction
         double v = (row < n) ? fabs(xa[row]) : 0.0;
         v = lgm_warp_sum(v);
@@ -489,8 +581,8 @@ struct Ctx {
         team_sync();
         double* xa = ya;
         double* xb = yb2;
-        for (int q = 0; q < p1; ++q) { thin(M1, sh1, true, xa, xb); double* tt = xa; xa = xb; xb = tt; }
-        if (has2) { thin(MA, sh2, true, xa, xb); double* tt = xa; xa = xb; xb = tt; }
+        apply_pow(M1, p1, true, xa, xb);
+        if (has2) apply_pow(MA, 1, true, xa, xb);
         if (row < n) vec(4 + team)[row] = xa[row];
       }
       passes += total;
@@ -551,11 +643,16 @@ struct Ctx {
   }
 
   // ---- GEMM with fused left combination -------------------------------------------------
+  // A polynomial node: row-major matrix at `p` with row stride `ld` (shared or global).
+  struct Node {
+    const double* p;
+    int ld;
+  };
   // acc[jj] = sum_kk L[row][kk] * R[kk][col0 + jj], col0 = team * NMAX/2, where
-  // L = sum_t lc[t] * buf(lb[t]) + l0 * I computed on the fly with numpy's _combine
+  // L = sum_t lc[t] * node[t] + l0 * I computed on the fly with numpy's _combine
   // rounding (schemes.py:91-101: products and sums rounded separately, no FMA).
   static constexpr int MAXT = 7;
-  __device__ void gemm_comb(int nterm, const double (&lc)[MAXT], const int (&lb)[MAXT], double l0,
+  __device__ void gemm_comb(int nterm, const double (&lc)[MAXT], const Node (&ln)[MAXT], double l0,
                             const double* R, double (&acc)[NMAX / 2]) {
     const int col0 = team * (NMAX / 2);
 #pragma unroll
@@ -563,7 +660,7 @@ struct Ctx {
     if (row >= n) return;
     const double* Lb[MAXT];
 #pragma unroll
-    for (int q = 0; q < MAXT; ++q) Lb[q] = buf(lb[q]) + row * C::LDM;
+    for (int q = 0; q < MAXT; ++q) Lb[q] = ln[q].p + row * ln[q].ld;
     for (int kk = 0; kk < n; ++kk) {
       double l = 0.0;
 #pragma unroll
@@ -572,60 +669,72 @@ struct Ctx {
       if (kk == row && l0 != 0.0) l = __dadd_rn(l, l0);
       const double* Rr = R + kk * C::LDM + col0;
 #pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = fma(l, Rr[jj], acc[jj]);
+      for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = fma(l, Rr[jj], acc[jj]);  // LDM odd: 8 B aligned
     }
   }
 
-  // buf(dst)[i][j] = sum_t c[t] * buf(b[t])[i][j] + c0 * I (schemes.py:91-101 order)
-  __device__ void combine_into(int dst, int nterm, const double (&c)[MAXT], const int (&b)[MAXT], double c0) {
-    double* D = buf(dst);
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
-      double v = 0.0;
+  // D[i][j] = sum_t c[t] * node[t][i][j] + c0 * I (schemes.py:91-101 order); D in smem.
+  __device__ void combine_into(double* D, int nterm, const double (&c)[MAXT], const Node (&nd)[MAXT], double c0) {
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
+        double v = 0.0;
 #pragma unroll
-      for (int q = 0; q < MAXT; ++q)
-        if (q < nterm) v = __dadd_rn(v, __dmul_rn(c[q], buf(b[q])[i * C::LDM + j]));
-      if (i == j && c0 != 0.0) v = __dadd_rn(v, c0);
-      D[i * C::LDM + j] = v;
-    }
+        for (int q = 0; q < MAXT; ++q)
+          if (q < nterm) v = __dadd_rn(v, __dmul_rn(c[q], nd[q].p[i * nd[q].ld + j]));
+        if (i == j && c0 != 0.0) v = __dadd_rn(v, c0);
+        D[i * C::LDM + j] = v;
+      }
   }
 
   // Gather the non-zero coefficients of a combination row over nodes P1..P_{nn}
-  // (P1 = I, P_t in buffer nodebuf[t]).
-  __device__ static int gather_terms(const double* row, int nn, const int* nodebuf, double (&c)[MAXT],
-                                     int (&b)[MAXT], double& c0) {
+  // (P1 = I, P_t = nodes[t]).
+  __device__ static int gather_terms(const double* crow, int nn, const Node* nodes, double (&c)[MAXT],
+                                     Node (&nd)[MAXT], double& c0) {
     int q = 0;
-    c0 = row[0];
+    c0 = crow[0];
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t) { c[t] = 0.0; b[t] = 0; }
+    for (int t = 0; t < MAXT; ++t) { c[t] = 0.0; nd[t] = nodes[2]; }
     for (int t = 2; t <= nn; ++t) {
-      if (row[t - 1] != 0.0) { c[q] = row[t - 1]; b[q] = nodebuf[t]; q++; }
+      if (crow[t - 1] != 0.0) { c[q] = crow[t - 1]; nd[q] = nodes[t]; q++; }
     }
     return q;
   }
 
+  __device__ void store_half_rows(double* D, int ld, const double (&acc)[NMAX / 2]) {
+    if (row < n) {
+      double* Dr = D + row * ld + team * (NMAX / 2);
+#pragma unroll
+      for (int jj = 0; jj < NMAX / 2; ++jj)
+        if (team * (NMAX / 2) + jj < n) Dr[jj] = acc[jj];
+    }
+  }
+
   // ---- degree-optimal polynomial (schemes.py:104-126) + fused epilogue ------------------
-  // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp, one product).
-  // Free buffers bR (combination temp) and bfree[0..2] hold P4..P6.  The last node stays in
-  // registers; the epilogue forms z, scales by `mult` (= -2^s), reverts the balancing
-  // (matcore.py:175-177) when `scales` is set and writes row-major to Lg (ld).
-  __device__ void degopt(int k, int bX, int b3, bool have_fp, int bR, const int (&bfree)[3], double mult,
-                         bool unbal, double* Lg, long long ldg, int& products) {
-    int nodebuf[8] = {0, 0, bX, b3, bfree[0], bfree[1], bfree[2], 0};
+  // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp: one product), R is
+  // the shared combination temp; P4..P6 live in `extra` (shared or a global workspace slot,
+  // row stride extra_ld).  The last node stays in registers; the epilogue forms z, scales
+  // by `mult` (= -2^s), reverts the balancing (matcore.py:175-177) when `unbal` is set,
+  // stages through R and writes row-major to Lg (ld).
+  __device__ __noinline__ void degopt(int k, int bX, int b3, bool have_fp, int bR, double* const (&extra)[3],
+                                      int extra_ld, double mult, bool unbal, double* Lg, long long ldg,
+                                      int& products) {
+    Node nodes[8];
+    nodes[0] = nodes[1] = nodes[7] = Node{buf(bX), C::LDM};
+    nodes[2] = Node{buf(bX), C::LDM};
+    nodes[3] = Node{buf(b3), C::LDM};
+    for (int t = 0; t < 3; ++t) nodes[4 + t] = Node{extra[t], extra_ld};
+    double* R = buf(bR);
     double acc[NMAX / 2];
     double c[MAXT], c0;
-    int b[MAXT];
+    Node nd[MAXT];
     if (!have_fp) {  // P3 = P2 * P2
-      c[0] = 1.0; b[0] = bX;
-      for (int q = 1; q < MAXT; ++q) { c[q] = 0.0; b[q] = bX; }
-      gemm_comb(1, c, b, 0.0, buf(bX), acc);
+      c[0] = 1.0;
+      for (int q = 1; q < MAXT; ++q) c[q] = 0.0;
+      for (int q = 0; q < MAXT; ++q) nd[q] = nodes[2];
+      gemm_comb(1, c, nd, 0.0, buf(bX), acc);
       products++;
       __syncthreads();
-      if (row < n) {
-        double* D = buf(b3) + row * C::LDM + team * (NMAX / 2);
-#pragma unroll
-        for (int jj = 0; jj < NMAX / 2; ++jj) if (team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
-      }
+      store_half_rows(buf(b3), C::LDM, acc);
       __syncthreads();
     }
     int nn = 3;  // nodes P1..P3 available
@@ -633,29 +742,24 @@ struct Ctx {
     for (int j = 1; j < k; ++j) {
       const double* lrow = lgm_lhs(*P, k, j);
       const double* rrow = lgm_rhs(*P, k, j);
-      int nt = gather_terms(rrow, nn, nodebuf, c, b, c0);
-      combine_into(bR, nt, c, b, c0);
+      int nt = gather_terms(rrow, nn, nodes, c, nd, c0);
+      combine_into(R, nt, c, nd, c0);
       __syncthreads();
-      nt = gather_terms(lrow, nn, nodebuf, c, b, c0);
-      gemm_comb(nt, c, b, c0, buf(bR), acc);
+      nt = gather_terms(lrow, nn, nodes, c, nd, c0);
+      gemm_comb(nt, c, nd, c0, R, acc);
       products++;
       nn++;
       __syncthreads();
       if (j < k - 1) {
-        if (row < n) {
-          double* D = buf(nodebuf[nn]) + row * C::LDM + team * (NMAX / 2);
-#pragma unroll
-          for (int jj = 0; jj < NMAX / 2; ++jj) if (team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
-        }
+        store_half_rows(const_cast<double*>(nodes[nn].p), nodes[nn].ld, acc);
         __syncthreads();
       } else {
         last_in_regs = true;
       }
     }
-    // epilogue: z = sum out[t] P_t + out[0] I, L = mult * z * (scale_i / scale_j) into bR
+    // epilogue: z = sum out[t] P_t + out[0] I, L = mult * z * (scale_i / scale_j) into R
     const double* orow = lgm_out(*P, k);
     const double* sc = scale();
-    double* S = buf(bR);
     if (row < n) {
       const int col0 = team * (NMAX / 2);
 #pragma unroll
@@ -666,30 +770,28 @@ struct Ctx {
           for (int t = 2; t <= nn; ++t) {
             double ct = orow[t - 1];
             if (ct != 0.0) {
-              double pv = (t == nn && last_in_regs) ? acc[jj] : buf(nodebuf[t])[row * C::LDM + col];
+              double pv = (t == nn && last_in_regs) ? acc[jj] : nodes[t].p[row * nodes[t].ld + col];
               v = __dadd_rn(v, __dmul_rn(ct, pv));
             }
           }
           if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
           v = mult * v;
           if (unbal) v = v * (sc[row] / sc[col]);
-          S[row * C::LDM + col] = v;
+          R[row * C::LDM + col] = v;
         }
       }
     }
     __syncthreads();
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, jcol = idx - i * n;
-      Lg[(long long)i * ldg + jcol] = S[i * C::LDM + jcol];
-    }
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int jcol = lane; jcol < n; jcol += 32) Lg[(long long)i * ldg + jcol] = R[i * C::LDM + jcol];
   }
 
   // ---- load / store --------------------------------------------------------------------
   __device__ bool load(int b, const double* Ag, long long ldg) {
     double* D = buf(b);
     bool bad = false;
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
       double v = Ag[(long long)i * ldg + j];
       bad |= !isfinite(v);
       D[i * C::LDM + j] = v;
@@ -698,14 +800,14 @@ struct Ctx {
   }
   __device__ void store(int b, double* Dg, long long ldg) {
     const double* S = buf(b);
-    for (int idx = tid; idx < n * n; idx += C::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) {
       Dg[(long long)i * ldg + j] = S[i * C::LDM + j];
     }
   }
 
   // ---- Algorithm 1 (oracle/driver.py logm_status) ----------------------------------------
-  __device__ double alpha(int bB, bool have_ai2, int bAI2, double nA, int m, double theta,
+  __device__ __noinline__ double alpha(int bB, bool have_ai2, int bAI2, double nA, int m, double theta,
                           double (&cache)[16], unsigned& cvalid, int& nest, int& passes) {
     const int itmax = P->est_itmax;
     double t1, Pm;
@@ -719,7 +821,7 @@ struct Ctx {
         if (!((cvalid >> m) & 1u)) {
           nest++;
           double e = 0.0;
-          if (any_nonzero(bAI2, 0.0)) e = estimate(bAI2, 0.0, m / 2, false, bB, 1.0, itmax, passes);
+          if (any_nonzero(bAI2, 0.0)) e = estimate(bAI2, m / 2, false, bB, itmax, passes);
           cache[m] = e; cvalid |= 1u << m;
         }
         Pm = cache[m];
@@ -729,7 +831,7 @@ struct Ctx {
       if (!((cvalid >> m) & 1u)) {
         nest++;
         double e = 0.0;
-        if (any_nonzero(bB, 1.0)) e = estimate(bB, 1.0, m, false, bB, 1.0, itmax, passes);
+        if (any_nonzero(bB, 0.0)) e = estimate(bB, m, false, bB, itmax, passes);
         cache[m] = e; cvalid |= 1u << m;
       }
       Pm = cache[m];
@@ -746,10 +848,10 @@ struct Ctx {
         nest++;
         double e;
         if (have_ai2) {
-          e = estimate(bAI2, 0.0, m / 2, true, bB, 1.0, itmax, passes);
+          e = estimate(bAI2, m / 2, true, bB, itmax, passes);
         } else {
           e = 0.0;
-          if (any_nonzero(bB, 1.0)) e = estimate(bB, 1.0, m + 1, false, bB, 1.0, itmax, passes);
+          if (any_nonzero(bB, 0.0)) e = estimate(bB, m + 1, false, bB, itmax, passes);
         }
         cache[m + 1] = e; cvalid |= 1u << (m + 1);
       }
@@ -765,7 +867,7 @@ struct Ctx {
   }
 
   // returns k; cert = alpha certifying k
-  __device__ int select(int bB, int bAI2, double nA, double alpha_loop, double (&cache)[16], unsigned& cvalid,
+  __device__ __noinline__ int select(int bB, int bAI2, double nA, double alpha_loop, double (&cache)[16], unsigned& cvalid,
                         int& nest, int& passes, double& cert) {
     const int K = P->max_k;
     const double* th = P->theta;
@@ -808,10 +910,10 @@ struct Ctx {
 };
 
 // Buffer roles in the fused logm kernel
-enum { BUF_B = 0, BUF_Y = 1, BUF_P = 2, BUF_4 = 3, BUF_5 = 4, BUF_6 = 5 };
+enum { BUF_B = 0, BUF_Y = 1, BUF_P = 2 };
 
 template <int NMAX>
-__device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep) {
+__device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep, double* ws) {
   const LgmParams& P = *c.P;
   lgm_report R = {};
   R.balanced = P.balance;
@@ -823,8 +925,11 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
     if (c.tid == 0) *rep = R;
     return;
   }
-  if (P.balance) R.balance_sweeps = c.balance(BUF_B, 100);
-  else {
+  if (P.balance) {
+    LGM_PHASE_BEGIN(c);
+    R.balance_sweeps = c.balance(BUF_B, 100);
+    LGM_PHASE_END(c, 0);
+  } else {
     for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
     __syncthreads();
   }
@@ -841,14 +946,25 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   int status = 0;
   while (!finish && s < P.maxiter_s) {
     double nA = c.onenorm(BUF_B, 1.0);
-    double a = c.alpha(BUF_B, have_ai2, BUF_P, nA, mK, thK, cache, cvalid, nest, passes);
+    double a;
+    {
+      LGM_PHASE_BEGIN(c);
+      c.minus_identity(BUF_Y, BUF_B);  // A - I materialised as numpy does (estimator operand)
+      __syncthreads();
+      a = c.alpha(BUF_Y, have_ai2, BUF_P, nA, mK, thK, cache, cvalid, nest, passes);
+      LGM_PHASE_END(c, 1);
+    }
     alpha_loop = a;
     finish = c.le(a, thK);
     if (!finish) {
       c.copy_buf(BUF_P, BUF_B);
       __syncthreads();
       int its = 0;
-      status = c.sqrt_db(BUF_B, BUF_Y, tol, P.db_maxiter, its);
+      {
+        LGM_PHASE_BEGIN(c);
+        status = c.sqrt_db(BUF_B, BUF_Y, tol, P.db_maxiter, its);
+        LGM_PHASE_END(c, 2);
+      }
       db_iters += its;
       if (status) break;
       s++;
@@ -856,8 +972,8 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
       {
         double* Pm = c.buf(BUF_P);
         const double* Bm = c.buf(BUF_B);
-        for (int idx = c.tid; idx < n * n; idx += Cfg<NMAX>::NT) {
-          int i = idx / n, j = idx - i * n;
+        for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+          for (int j = c.lane; j < n; j += 32) {
           double v = Pm[i * Cfg<NMAX>::LDM + j] - 2.0 * Bm[i * Cfg<NMAX>::LDM + j];
           if (i == j) v = v + 1.0;
           Pm[i * Cfg<NMAX>::LDM + j] = v;
@@ -881,13 +997,14 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
     return;
   }
   const double nA = c.onenorm(BUF_B, 1.0);
+  c.minus_identity(BUF_Y, BUF_B);  // A - I: estimator operand in select, GEMM operand below
+  __syncthreads();
   if (!have_ai2) {  // s = 0: A_I2 = (B - I)(B - I), one product
     double cc[Ctx<NMAX>::MAXT] = {1.0};
-    int bb[Ctx<NMAX>::MAXT] = {BUF_B};
+    typename Ctx<NMAX>::Node bb[Ctx<NMAX>::MAXT];
+    for (int q = 0; q < Ctx<NMAX>::MAXT; ++q) bb[q] = {c.buf(BUF_Y), Cfg<NMAX>::LDM};
     double acc[NMAX / 2];
-    c.combine_into(BUF_Y, 1, cc, bb, -1.0);
-    __syncthreads();
-    c.gemm_comb(1, cc, bb, -1.0, c.buf(BUF_Y), acc);
+    c.gemm_comb(1, cc, bb, 0.0, c.buf(BUF_Y), acc);
     products++;
     if (c.row < n) {
       double* D = c.buf(BUF_P) + c.row * Cfg<NMAX>::LDM + c.team * (NMAX / 2);
@@ -897,19 +1014,28 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
     __syncthreads();
   }
   double cert = 0.0;
-  const int k = c.select(BUF_B, BUF_P, nA, alpha_loop, cache, cvalid, nest, passes, cert);
+  int k;
+  {
+    LGM_PHASE_BEGIN(c);
+    k = c.select(BUF_Y, BUF_P, nA, alpha_loop, cache, cvalid, nest, passes, cert);
+    LGM_PHASE_END(c, 3);
+  }
   // P2 = I - B (the schemes approximate -log(I - X), schemes.py:129-131); B is dead now.
   {
     double* Bm = c.buf(BUF_B);
-    for (int idx = c.tid; idx < n * n; idx += Cfg<NMAX>::NT) {
-      int i = idx / n, j = idx - i * n;
+    for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+      for (int j = c.lane; j < n; j += 32) {
       double v = Bm[i * Cfg<NMAX>::LDM + j];
       Bm[i * Cfg<NMAX>::LDM + j] = (i == j) ? 1.0 - v : -v;
     }
   }
   __syncthreads();
-  const int bfree[3] = {BUF_4, BUF_5, BUF_6};
-  c.degopt(k, BUF_B, BUF_P, true, BUF_Y, bfree, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
+  double* const extra[3] = {ws, ws + n * n, ws + 2 * n * n};  // P4..P6: this matrix's workspace slot
+  {
+    LGM_PHASE_BEGIN(c);
+    c.degopt(k, BUF_B, BUF_P, true, BUF_Y, extra, n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
+    LGM_PHASE_END(c, 4);
+  }
   R.k = k;
   R.alpha_used = cert;
   R.products = products;
