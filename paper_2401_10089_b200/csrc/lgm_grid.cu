@@ -13,7 +13,9 @@
 //     the A-tile load (schemes.py:91-126);
 //   * balance_kernel / onenorm_kernel: numpy-order reductions (bit-identical decisions).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -21,6 +23,30 @@
 #include "lgm_grid.cuh"
 
 namespace {
+
+// Optional host-side phase timing (LGM_GRID_PROFILE=1): stream-synchronised wall time per
+// phase, read back with lgm_debug_grid_phase_ms (tools/grid_prof.py).  Off by default.
+enum { PH_BALANCE = 0, PH_ALPHA, PH_INVERT, PH_DBUPD, PH_SELECT, PH_POLY, PH_OTHER, PH_N };
+double g_phase_ms[PH_N];
+bool prof_on() {
+  static int on = -1;
+  if (on < 0) on = std::getenv("LGM_GRID_PROFILE") ? 1 : 0;
+  return on == 1;
+}
+struct PhaseTimer {
+  int ph;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  PhaseTimer(int p, cudaStream_t s) : ph(p), st(s) {
+    if (prof_on()) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
+  }
+  ~PhaseTimer() {
+    if (prof_on()) {
+      cudaStreamSynchronize(st);
+      g_phase_ms[ph] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+};
 
 constexpr int NB = 32;      // Gauss-Jordan panel width
 constexpr int NBUF = 8;     // n x n slots per matrix
@@ -115,6 +141,186 @@ struct InvJob {
 };
 // After all panels, storage R satisfies R[piv[k]][j] = Minv[k][piv[j]], i.e.
 // Minv[a][c] = R[piv[a]][rowstep[c]].
+
+// ------------------------------------------------------------------------------------------
+// G1: the whole blocked Gauss-Jordan inversion of one matrix per CTA (64 < n <= NT <= 512).
+// Thread `tid` owns row `tid` of the current 32-column panel in registers (static register
+// indexing: the 32 pivot steps are unrolled); pivots by block argmax; the factored panel is
+// staged in shared memory as the A operand of the trailing rank-32 update, which each warp
+// applies to its 32 rows with DMMA (mma.sync m8n8k4 f64), column block by column block,
+// with the pivot rows of the block snapshotted to shared memory first.  No host round trip
+// or grid-level synchronisation per panel; one launch inverts every job of the batch.
+constexpr int G1_LDA = 36;  // A panel row stride (bank-conflict free fragment loads)
+constexpr int G1_LDW = 36;  // W chunk row stride
+
+template <int NT>
+struct G1Smem {
+  static constexpr size_t A = (size_t)NT * G1_LDA;  // doubles
+  static constexpr size_t W = 32 * G1_LDW;
+  static constexpr size_t PR = 2 * 40;
+  static constexpr size_t bytes = (A + W + PR) * 8 + 2 * (size_t)NT * 4 + 64 * 16;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* jobs, int n) {
+  extern __shared__ __align__(16) double g1sm[];
+  double* As = g1sm;
+  double* Ws = As + G1Smem<NT>::A;
+  double* prow = Ws + G1Smem<NT>::W;                       // [2][40]: pivot row (32) + inv
+  int* rstep = reinterpret_cast<int*>(prow + G1Smem<NT>::PR);  // [NT] rowstep
+  int* piv = rstep + NT;                                   // [NT]
+  unsigned long long* wkey = reinterpret_cast<unsigned long long*>(piv + NT);  // [2][16]
+  int* widx = reinterpret_cast<int*>(wkey + 32);           // [2][16]
+
+  const InvJob J = jobs[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  double* M = J.M;
+  for (int i = tid; i < NT; i += NT) rstep[i] = -1;
+  int my_step = -1;
+  double logsum = 0.0;  // sum of log|pivot| of this thread's pivot (at most one)
+  int status = 0;
+  __syncthreads();
+  for (int k0 = 0; k0 < n && status == 0; k0 += 32) {
+    const int nb = min(32, n - k0);
+    double r[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
+    double rowscale = 1.0;
+    bool piv_here = false;
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk) {
+      if (kk < nb && status == 0) {
+        const int par = kk & 1;
+        const bool cand = (tid < n) && (my_step < 0);
+        uint64_t key = cand ? dkey(fabs(r[kk])) : 0ull;
+        // warp argmax (ties -> lowest lane = lowest row)
+        unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(key >> 32));
+        unsigned lo = __reduce_max_sync(0xffffffffu, ((unsigned)(key >> 32) == hi) ? (unsigned)key : 0u);
+        const uint64_t wmax = ((uint64_t)hi << 32) | lo;
+        const int wl = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
+        if (lane == 0) { wkey[par * 16 + warp] = wmax; widx[par * 16 + warp] = warp * 32 + wl; }
+        __syncthreads();
+        uint64_t kb = wkey[par * 16];
+        int p = widx[par * 16];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const uint64_t kw = wkey[par * 16 + w];
+          if (kw > kb) { kb = kw; p = widx[par * 16 + w]; }
+        }
+        if (kb <= 1ull) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
+        double* pr = prow + par * 40;
+        const bool own = (tid == p);
+        if (own) {
+          my_step = k0 + kk;
+          piv_here = true;
+          const double pv = r[kk];
+          logsum = log(fabs(pv));
+          rowscale = 1.0 / pv;
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pr + c) = make_double2(r[c], r[c + 1]);
+          pr[32] = rowscale;
+          rstep[tid] = k0 + kk;
+          piv[k0 + kk] = tid;
+        }
+        __syncthreads();
+        const double g = own ? 0.0 : r[kk] * pr[32];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
+          if (c != kk) r[c] = fma(-g, p2.x, r[c]);
+          if (c + 1 != kk) r[c + 1] = fma(-g, p2.y, r[c + 1]);
+        }
+        r[kk] = own ? 1.0 : -g;
+      }
+    }
+    if (status) break;
+    if (piv_here) {  // deferred scaling of this panel's pivot row
+#pragma unroll
+      for (int c = 0; c < 32; ++c) r[c] *= rowscale;
+    }
+    // factored panel -> global (K columns) and shared (A operand)
+    if (tid < n) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c < nb) M[(size_t)tid * n + k0 + c] = r[c];
+        As[tid * G1_LDA + c] = (c < nb) ? r[c] : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) As[tid * G1_LDA + c] = 0.0;
+    }
+    __syncthreads();
+    // trailing update, column blocks of 32 outside the panel
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int r0 = warp * 32;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      if (j0 == k0) continue;  // the panel itself (panels are 32-aligned)
+      // snapshot pivot rows' block: Ws[c][jj] = M[piv[k0+c]][j0+jj]
+      for (int idx = tid; idx < 32 * 32; idx += NT) {
+        const int c = idx >> 5, jj = idx & 31;
+        Ws[c * G1_LDW + jj] = (c < nb && j0 + jj < n) ? M[(size_t)piv[k0 + c] * n + j0 + jj] : 0.0;
+      }
+      __syncthreads();
+      if (r0 < n) {
+        double acc[4][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int i = r0 + mi * 8 + g8;
+          const int rs = (i < n) ? rstep[i] : -1;
+          const bool zero_row = (rs >= k0 && rs < k0 + nb);
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int j = j0 + ni * 8 + 2 * t4 + e;
+              acc[mi][ni][e] = (i < n && j < n && !zero_row) ? M[(size_t)i * n + j] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) a[mi] = As[(r0 + mi * 8 + g8) * G1_LDA + k + t4];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) b[ni] = Ws[(k + t4) * G1_LDW + ni * 8 + g8];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int i = r0 + mi * 8 + g8;
+          if (i >= n) continue;
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int j = j0 + ni * 8 + 2 * t4 + e;
+              if (j < n) M[(size_t)i * n + j] = acc[mi][ni][e];
+            }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // publish pivots, log|det|, status
+  for (int i = tid; i < n; i += NT) { J.piv[i] = piv[i]; J.rowstep[i] = rstep[i]; }
+  double s = logsum;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(prow);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < NW; ++w) tot += red[w];
+    *J.logdet = tot;
+    *J.status = status;
+  }
+}
 
 __global__ void gj_init_kernel(const InvJob* jobs, int n) {
   const InvJob J = jobs[blockIdx.y];
@@ -882,6 +1088,15 @@ struct Grid {
   }
 
   // ---- batched inversion of slot `k` of the listed matrices (jobs: which = 0 for X, 1 for Y)
+  template <int NT>
+  int launch_g1(int nj) {
+    const size_t sm = G1Smem<NT>::bytes;
+    CK(cudaFuncSetAttribute(gj_inv_cta_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(d_jobs, n);
+    CK(cudaGetLastError());
+    return 0;
+  }
+
   int invert(const std::vector<int>& mats, const std::vector<int>& which, const std::vector<int>& slot) {
     const int nj = (int)mats.size();
     if (!nj) return 0;
@@ -897,6 +1112,11 @@ struct Grid {
       J.status = d_istat + w * batch + b;
     }
     CK(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(InvJob), cudaMemcpyHostToDevice, st));
+    if (n <= 512) {  // G1: one CTA per inversion, no per-panel launches
+      if (n <= 128) return launch_g1<128>(nj);
+      if (n <= 256) return launch_g1<256>(nj);
+      return launch_g1<512>(nj);
+    }
     gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
     const size_t psmem = (size_t)n * (NB + 1) * 8;
     const int in_smem = psmem <= 200 * 1024;
@@ -1009,7 +1229,10 @@ struct Grid {
       if (upload_ids(act)) return LGM_ERR_CUDA;
       CK(cudaMemsetAsync(d_iflag, 0, batch * 4, st));
       // reuse load_kernel's finiteness test via any_nonfinite on XI/YI
-      if (invert(mats2, which, slot)) return LGM_ERR_CUDA;
+      {
+        PhaseTimer pt(PH_INVERT, st);
+        if (invert(mats2, which, slot)) return LGM_ERR_CUDA;
+      }
       std::vector<int> ist(2 * batch);
       std::vector<double> lds(2 * batch);
       CK(cudaMemcpyAsync(ist.data(), d_istat, 2 * batch * 4, cudaMemcpyDeviceToHost, st));
@@ -1043,6 +1266,7 @@ struct Grid {
       a.first = it == 1;
       a.change = d_scal;
       a.size = d_scal2;
+      PhaseTimer pt(PH_DBUPD, st);
       db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
       CK(cudaGetLastError());
       std::vector<double> ch(batch), sz(batch);
@@ -1222,6 +1446,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     CK(cudaMemcpyAsync(G.d_scale, ones.data(), ones.size() * 8, cudaMemcpyHostToDevice, st));
     if (P.balance && !live.empty()) {
       if (G.upload_ids(live)) return LGM_ERR_CUDA;
+      PhaseTimer pt(PH_BALANCE, st);
       balance_kernel_g<<<(int)live.size(), 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
       CK(cudaGetLastError());
       std::vector<int> sw(batch);
@@ -1253,7 +1478,10 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     for (int b : act) ms[b].nA = nrm[b];
     std::vector<int> mv(act.size(), mK);
     std::vector<double> th(act.size(), thK), al;
-    if (alpha_batched(G, ms, act, mv, th, P.est_itmax, al)) return LGM_ERR_CUDA;
+    {
+      PhaseTimer pt(PH_ALPHA, st);
+      if (alpha_batched(G, ms, act, mv, th, P.est_itmax, al)) return LGM_ERR_CUDA;
+    }
     std::vector<int> roots;
     for (size_t q = 0; q < act.size(); ++q) {
       MState& M = ms[act[q]];
@@ -1345,6 +1573,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
       std::vector<int> mv;
       std::vector<double> th, al;
       for (int b : cur) { mv.push_back(P.order[jcur[b] - 1]); th.push_back(P.theta[jcur[b] - 1]); }
+      PhaseTimer pt(PH_SELECT, st);
       if (alpha_batched(G, ms, cur, mv, th, P.est_itmax, al)) return LGM_ERR_CUDA;
       std::vector<int> next;
       for (size_t q = 0; q < cur.size(); ++q) {
@@ -1359,6 +1588,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     }
   }
   // polynomial: P2 = I - B (slot G_B), P3 = A_I2 (G_AP), R temp (G_Y), P4.. in G_XI, G_YI, G_P6, G_P7
+  PhaseTimer pt_poly(PH_POLY, st);
   if (G.ew(sel, 4, G_B, G_B, G_B)) return LGM_ERR_CUDA;
   const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
   for (int kk = 1; kk <= K; ++kk) {
@@ -1585,4 +1815,12 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
   CK(cudaMemcpyAsync(products, pr.data(), batch * 4, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return 0;
+}
+
+extern "C" int lgm_debug_grid_phase_ms(double* out, int reset) {
+  for (int i = 0; i < PH_N; ++i) {
+    out[i] = g_phase_ms[i];
+    if (reset) g_phase_ms[i] = 0.0;
+  }
+  return PH_N;
 }
