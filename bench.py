@@ -218,6 +218,7 @@ def main():
         torch.cuda.synchronize()
 
     times = []
+    launches0 = _lib.launch_count()
     with ClockSampler(local_rank) as clk:
         barrier()
         for _ in range(args.steps):
@@ -229,6 +230,7 @@ def main():
             e1.record(stream)
             times.append((e0, e1))
         barrier()
+    launches = _lib.launch_count() - launches0
     kernel_ms = [a.elapsed_time(b) for a, b in times]
     total_ms = sum(kernel_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -296,7 +298,8 @@ def main():
         "achieved_tflops": achieved,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "logm_fused_kernel<32>" if n <= 32 else ("logm_fused_kernel<64>" if n <= 64 else "grid"),
+                     "kernel": ("logm_fused_kernel<32>" if n <= 32 else "logm_fused_kernel<64>") if n <= 64
+                     else "whole Engine-G step (gj_inv_cta_kernel dominant; achieved = step FLOPs / step time)",
                      "alg_flops_per_launch": F,
                      "hbm": {"achieved_gbs": alg_bytes / avg_launch_s / 1e9, "peak_gbs": hbm_peak,
                              "frac": alg_bytes / avg_launch_s / 1e9 / hbm_peak, "alg_bytes_per_launch": alg_bytes,
@@ -304,7 +307,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * n * n * 8),
                 "d2h_bytes_per_step": int(B * n * n * 8 + B * _lib.REPORT_DTYPE.itemsize)},
-        "gpu_launches": args.steps * (1 if n <= 64 else None or 1),
+        "gpu_launches": launches,
         "clocks": clk.summary(),
         "report_summary": {"status_counts": status_counts, "s_mean": float(reps["s"].mean()),
                            "k_mean": float(reps["k"].mean()), "db_iters_mean": float(reps["db_iters"].mean()),

@@ -120,6 +120,10 @@ int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z,
 
 const char* lgm_status_string(int code);
 
+/* Number of CUDA kernels this library has launched so far (process-wide, monotonic);
+ * bench.py reports the difference across its timed region as gpu_launches. */
+long long lgm_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,6 +3,7 @@
 // n <= 64: Engine F (lgm_fused.cuh), one CTA per matrix, the whole pipeline in one launch.
 // n  > 64: Engine G (lgm_grid.cu), host-orchestrated batched kernels over a caller-owned
 //          workspace (lgm_workspace_bytes).
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -10,6 +11,9 @@
 #include "lgm_grid.cuh"
 
 using namespace lgm;
+
+static std::atomic<long long> g_lgm_launches{0};
+int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed); return 0; }
 
 // ------------------------------------------------------------------------------ kernels
 
@@ -157,6 +161,8 @@ void lgm_default_opts(lgm_opts* o) {
 
 int lgm_max_fused_n(void) { return 64; }
 
+long long lgm_launch_count(void) { return g_lgm_launches.load(std::memory_order_relaxed); }
+
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
   // n <= 64: one 3 n^2 slot per matrix for the polynomial nodes P4..P6 (L2 resident)
@@ -194,13 +200,13 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
   if (n <= 32) {
     if (prep<32>(logm_fused_kernel<32>)) return LGM_ERR_CUDA;
-    logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
+    lgm_count_launch(), logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
                                                                                     (double*)ws, P);
     return check_launch();
   }
   if (n <= 64) {
     if (prep<64>(logm_fused_kernel<64>)) return LGM_ERR_CUDA;
-    logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
+    lgm_count_launch(), logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
                                                                                     (double*)ws, P);
     return check_launch();
   }
@@ -211,12 +217,12 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   do {                                                                                                   \
     if (n <= 32) {                                                                                       \
       if (prep<32>(KERNEL<32>)) return LGM_ERR_CUDA;                                                     \
-      KERNEL<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
+      lgm_count_launch(), KERNEL<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
       return check_launch();                                                                             \
     }                                                                                                    \
     if (n <= 64) {                                                                                       \
       if (prep<64>(KERNEL<64>)) return LGM_ERR_CUDA;                                                     \
-      KERNEL<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
+      lgm_count_launch(), KERNEL<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, (cudaStream_t)stream>>>(__VA_ARGS__); \
       return check_launch();                                                                             \
     }                                                                                                    \
   } while (0)
@@ -269,13 +275,13 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
   fill_params(P, nullptr);
   if (n <= 32) {
     if (prep<32>(degopt_kernel<32>, Cfg<32>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
-    degopt_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
+    lgm_count_launch(), degopt_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
                                                                                                   k, products, P);
     return check_launch();
   }
   if (n <= 64) {
     if (prep<64>(degopt_kernel<64>, Cfg<64>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
-    degopt_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
+    lgm_count_launch(), degopt_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
                                                                                                   k, products, P);
     return check_launch();
   }

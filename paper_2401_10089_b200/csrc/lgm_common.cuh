@@ -6,6 +6,9 @@
 #include "../../include/logmpoly_b200.h"
 #include "lgm_constants.h"
 
+// process-wide count of kernels launched by this library (lgm_launch_count in the ABI)
+int lgm_count_launch();
+
 #define LGM_UNIT_ROUNDOFF 1.1102230246251565e-16  // 2^-53 (matcore.py:19-20)
 #define LGM_SCALING_SWITCH 1e-2                   // sqrtm.py:21
 #define LGM_MU_MIN 1e-8                           // sqrtm.py:24

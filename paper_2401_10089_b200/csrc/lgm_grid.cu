@@ -1092,7 +1092,7 @@ struct Grid {
   int launch_g1(int nj) {
     const size_t sm = G1Smem<NT>::bytes;
     CK(cudaFuncSetAttribute(gj_inv_cta_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(d_jobs, n);
+    lgm_count_launch(), gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(d_jobs, n);
     CK(cudaGetLastError());
     return 0;
   }
@@ -1117,16 +1117,16 @@ struct Grid {
       if (n <= 256) return launch_g1<256>(nj);
       return launch_g1<512>(nj);
     }
-    gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
+    lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
     const size_t psmem = (size_t)n * (NB + 1) * 8;
     const int in_smem = psmem <= 200 * 1024;
     if (in_smem) CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     const int tiles = (n + TM - 1) / TM;
     for (int k0 = 0; k0 < n; k0 += NB) {
       const int nb = std::min(NB, n - k0);
-      gj_panel_kernel<<<nj, 512, in_smem ? psmem : 0, st>>>(d_jobs, n, k0, nb, in_smem);
-      gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb);
-      gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb);
+      lgm_count_launch(), gj_panel_kernel<<<nj, 512, in_smem ? psmem : 0, st>>>(d_jobs, n, k0, nb, in_smem);
+      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb);
+      lgm_count_launch(), gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb);
     }
     CK(cudaGetLastError());
     return 0;
@@ -1158,15 +1158,15 @@ struct Grid {
     }
     CK(cudaMemcpyAsync(d_est, jobs.data(), nj * sizeof(EstJob), cudaMemcpyHostToDevice, st));
     const double rsum = host_pairwise_abs_ramp(n);
-    est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, rsum);
+    lgm_count_launch(), est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, rsum);
     for (int sweep = 0; sweep < itmax; ++sweep) {
-      for (int q = 0; q < maxtot; ++q) est_fwd_kernel<<<dim3((n + 7) / 8, nj), 256, 0, st>>>(d_est, n, q);
-      est_after_fwd_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
+      for (int q = 0; q < maxtot; ++q) lgm_count_launch(), est_fwd_kernel<<<dim3((n + 7) / 8, nj), 256, 0, st>>>(d_est, n, q);
+      lgm_count_launch(), est_after_fwd_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
       for (int q = 0; q < maxtot; ++q) {
-        est_adj_kernel<<<dim3((n + 255) / 256, splits, nj), 256, 0, st>>>(d_est, n, q);
-        est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
+        lgm_count_launch(), est_adj_kernel<<<dim3((n + 255) / 256, splits, nj), 256, 0, st>>>(d_est, n, q);
+        lgm_count_launch(), est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
       }
-      est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
+      lgm_count_launch(), est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(jobs.data(), d_est, nj * sizeof(EstJob), cudaMemcpyDeviceToHost, st));
@@ -1185,7 +1185,7 @@ struct Grid {
     if (!c) return 0;
     if (upload_ids(mats)) return LGM_ERR_CUDA;
     CK(cudaMemsetAsync(d_scal, 0, batch * 8, st));
-    onenorm_kernel<<<dim3((n + 127) / 128, c), 128, 0, st>>>(S, d_ids, k, d_scal);
+    lgm_count_launch(), onenorm_kernel<<<dim3((n + 127) / 128, c), 128, 0, st>>>(S, d_ids, k, d_scal);
     CK(cudaMemcpyAsync(out.data(), d_scal, batch * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return 0;
@@ -1196,7 +1196,7 @@ struct Grid {
     if (mats.empty()) return 0;
     if (upload_ids(mats)) return LGM_ERR_CUDA;
     CK(cudaMemsetAsync(d_iflag, 0, batch * 4, st));
-    any_nonzero_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, k, d_iflag);
+    lgm_count_launch(), any_nonzero_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, k, d_iflag);
     CK(cudaMemcpyAsync(out.data(), d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return 0;
@@ -1205,7 +1205,7 @@ struct Grid {
   int ew(const std::vector<int>& mats, int op, int dk, int sk, int s2k) {
     if (mats.empty()) return 0;
     if (upload_ids(mats)) return LGM_ERR_CUDA;
-    ew_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, op, dk, sk, s2k);
+    lgm_count_launch(), ew_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, op, dk, sk, s2k);
     CK(cudaGetLastError());
     return 0;
   }
@@ -1267,7 +1267,7 @@ struct Grid {
       a.change = d_scal;
       a.size = d_scal2;
       PhaseTimer pt(PH_DBUPD, st);
-      db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
+      lgm_count_launch(), db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
       CK(cudaGetLastError());
       std::vector<double> ch(batch), sz(batch);
       CK(cudaMemcpyAsync(ch.data(), d_scal, batch * 8, cudaMemcpyDeviceToHost, st));
@@ -1429,7 +1429,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
   // load + finiteness (as_square, matcore.py:64-65)
   CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
+  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
   std::vector<int> bad(batch);
   CK(cudaMemcpyAsync(bad.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1447,7 +1447,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     if (P.balance && !live.empty()) {
       if (G.upload_ids(live)) return LGM_ERR_CUDA;
       PhaseTimer pt(PH_BALANCE, st);
-      balance_kernel_g<<<(int)live.size(), 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
+      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
       CK(cudaGetLastError());
       std::vector<int> sw(batch);
       CK(cudaMemcpyAsync(sw.data(), G.d_sweeps, batch * 4, cudaMemcpyDeviceToHost, st));
@@ -1529,7 +1529,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     cs.node[0] = G_AM;
     cs.coef[0] = 1.0;
     const int tiles = (n + TM - 1) / TM;
-    gemm_comb_kernel<<<dim3(tiles, tiles, (int)need_ai2.size()), 128, 0, st>>>(G.S, G.d_ids, cs, G_AM, G_AP);
+    lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, (int)need_ai2.size()), 128, 0, st>>>(G.S, G.d_ids, cs, G_AM, G_AP);
     CK(cudaGetLastError());
     for (int b : need_ai2) { ms[b].products++; ms[b].have_ai2 = true; }
   }
@@ -1611,9 +1611,9 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
       const double* rrow = base + kk * (kk + 3) / 2 + j * (j + 3) / 2;
       if (G.upload_ids(grp)) return LGM_ERR_CUDA;
       CombSpec rs = spec(rrow, nn);
-      combine_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
+      lgm_count_launch(), combine_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
       CombSpec ls = spec(lrow, nn);
-      gemm_comb_kernel<<<dim3(tiles, tiles, (int)grp.size()), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
+      lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, (int)grp.size()), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
       CK(cudaGetLastError());
       nn++;
       for (int b : grp) ms[b].products++;
@@ -1624,7 +1624,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     for (int b : grp) mult[b] = -std::ldexp(1.0, ms[b].s);
     CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
     if (G.upload_ids(grp)) return LGM_ERR_CUDA;
-    final_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, P.balance, L, ld);
+    lgm_count_launch(), final_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, P.balance, L, ld);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
   }
@@ -1678,7 +1678,7 @@ int lgm_grid_sqrt_db(const double* A, double* X, int64_t n64, int64_t batch64, i
   for (int b = 0; b < batch; ++b) all[b] = b;
   CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
+  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
   std::vector<int> bad(batch);
   CK(cudaMemcpyAsync(bad.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1690,7 +1690,7 @@ int lgm_grid_sqrt_db(const double* A, double* X, int64_t n64, int64_t batch64, i
   }
   if (G.sqrt_db(live, tol, maxiter, dst, dit, mm, plat)) return LGM_ERR_CUDA;
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, X, ld);
+  lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, X, ld);
   CK(cudaMemcpyAsync(iters, dit.data(), batch * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(status, dst.data(), batch * 4, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
@@ -1708,10 +1708,10 @@ int lgm_grid_est(const double* M1, int p1, const double* M2, int64_t n64, int64_
   std::vector<int> all(batch);
   for (int b = 0; b < batch; ++b) all[b] = b;
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M1, ld, G.S, G.d_ids, G.d_iflag);
+  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M1, ld, G.S, G.d_ids, G.d_iflag);
   if (M2) {  // second operand into slot G_AM via the B slot
     G.ew(all, 1, G_AP, G_B, G_B);
-    load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M2, ld, G.S, G.d_ids, G.d_iflag);
+    lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M2, ld, G.S, G.d_ids, G.d_iflag);
     G.ew(all, 1, G_AM, G_B, G_B);
     G.ew(all, 1, G_B, G_AP, G_AP);
   }
@@ -1749,11 +1749,11 @@ int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n64, int
   std::vector<int> all(batch);
   for (int b = 0; b < batch; ++b) all[b] = b;
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
+  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
   std::vector<double> mm0(batch, INFINITY);
   CK(cudaMemcpyAsync(G.d_margin, mm0.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  balance_kernel_g<<<batch, 256, 0, st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
-  store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, B, ld);
+  lgm_count_launch(), balance_kernel_g<<<batch, 256, 0, st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
+  lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, B, ld);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
   return 0;
@@ -1770,12 +1770,12 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
   std::vector<int> all(batch);
   for (int b = 0; b < batch; ++b) all[b] = b;
   if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(X, ld, G.S, G.d_ids, G.d_iflag);
+  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(X, ld, G.S, G.d_ids, G.d_iflag);
   int prods = 0;
   const int tiles = (n + TM - 1) / TM;
   if (FP) {
     G.ew(all, 1, G_Y, G_B, G_B);
-    load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(FP, ld, G.S, G.d_ids, G.d_iflag);
+    lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(FP, ld, G.S, G.d_ids, G.d_iflag);
     G.ew(all, 1, G_AP, G_B, G_B);
     G.ew(all, 1, G_B, G_Y, G_Y);
   } else {
@@ -1783,7 +1783,7 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
     cs.nterm = 1;
     cs.node[0] = G_B;
     cs.coef[0] = 1.0;
-    gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, cs, G_B, G_AP);
+    lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, cs, G_B, G_AP);
     prods++;
   }
   const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
@@ -1800,16 +1800,16 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
     const double* lrow = base + j * (j + 3) / 2;
     const double* rrow = base + k * (k + 3) / 2 + j * (j + 3) / 2;
     CombSpec rs = spec(rrow, nn);
-    combine_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
+    lgm_count_launch(), combine_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
     CombSpec ls = spec(lrow, nn);
-    gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
+    lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
     nn++;
     prods++;
   }
   CombSpec os = spec(base + k * (k + 3), nn);
   std::vector<double> mult(batch, 1.0);
   CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  final_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, 0, Z, ld);
+  lgm_count_launch(), final_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, 0, Z, ld);
   CK(cudaGetLastError());
   std::vector<int> pr(batch, prods);
   CK(cudaMemcpyAsync(products, pr.data(), batch * 4, cudaMemcpyHostToDevice, st));

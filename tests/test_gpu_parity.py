@@ -254,3 +254,16 @@ def test_logm_torch_in_torch_out_and_options():
     L5, _ = lp.logm_batched(A, lp.LogmOptions(max_k=4))
     _, r4 = lp.logm_batched(A, lp.LogmOptions(max_k=4))
     assert (r4["k"] <= 4).all()
+
+
+def test_logm_multi_device_sharding_bitwise():
+    """Sharding by matrix changes nothing per matrix: two shards on the
+    same device (stand-in for 2 GPUs) reproduce the single-call result bit for bit."""
+    A = synth.config(2, batch=37)
+    L1, r1 = lp.logm_batched(A)
+    L2, r2 = lp.logm_batched(A, devices=["cuda:0", "cuda:0"])
+    assert np.array_equal(L1, L2) and r1.tobytes() == r2.tobytes()
+    A = synth.config(4, batch=3, n=96)
+    L1, r1 = lp.logm_batched(A)
+    L2, r2 = lp.logm_batched(A, devices=["cuda:0", "cuda:0", "cuda:0"])
+    assert np.array_equal(L1, L2) and r1.tobytes() == r2.tobytes()
