@@ -221,88 +221,70 @@ struct Ctx {
   // holds storage row `row` of the in-place result: Minv[q(row)][p_j] = r[j], where p_j is
   // the pivot row of step j (piv(team)[j]) and q(row) = my_step.  Returns 1 if an exact zero
   // pivot is met (matcore.py:124-125), else 0; logabsdet = sum log|pivot| (team-uniform).
-  // Rotate the register row left by KB columns (static moves; keeps code size bounded).
-  template <int KB>
-  __device__ __forceinline__ static void rotate_left(double (&r)[NMAX]) {
-    double t[KB];
-#pragma unroll
-    for (int i = 0; i < KB; ++i) t[i] = r[i];
-#pragma unroll
-    for (int j = 0; j + KB < NMAX; ++j) r[j] = r[j + KB];
-#pragma unroll
-    for (int i = 0; i < KB; ++i) r[NMAX - KB + i] = t[i];
-  }
-
-  // Implementation notes: the k loop runs over blocks of KB = 8 pivot steps; inside a block
-  // the pivot column is a static register (the row array is rotated left by KB after each
-  // block), so only one block's worth of code is emitted.  Row scaling is deferred: the
-  // pivot row is broadcast unscaled together with 1/pivot, the other rows fold 1/pivot into
-  // their multiplier, and the pivot row keeps raw values (its column-k entry set to 1) and
-  // is scaled once at the end -- the elimination is linear in each row, so this is the
-  // same Gauss-Jordan recurrence with different rounding.
+  // Implementation notes: every pivot step reads the pivot column from r[0] and writes the
+  // eliminated row back shifted by one register (r[j] <- r[j+1] - g * prow[j+1]), so the
+  // pivot column of the next step is again r[0]: static register indexing inside a small
+  // runtime loop (no unrolling over steps, no rotation moves -- the shift rides in the FMA's
+  // destination).  After NMAX steps (steps k >= n are pure rotations) the frame is back to
+  // the identity.  Row scaling is deferred: the pivot row is broadcast unscaled together with
+  // 1/pivot, the other rows fold 1/pivot into their multiplier, and the pivot row keeps raw
+  // values (its column-k entry set to 1) and is scaled once at the end -- the elimination is
+  // linear in each row, so this is the same Gauss-Jordan recurrence with different rounding.
   __device__ int gj_invert(double (&r)[NMAX], double& logabsdet, int& my_step) {
-    constexpr int KB = 8;
     bool used = false;
     my_step = -1;
     double mylog = 0.0, rowscale = 1.0;
     int* pv = piv(team);
     double* kslot = red() + RD_KEY + team * 4;
     int status = 0;
-    const int nblk = (n + KB - 1) / KB;
 #pragma unroll 1
-    for (int kb = 0; kb < NMAX / KB; ++kb) {
-      if (kb < nblk) {
-#pragma unroll
-        for (int kk = 0; kk < KB; ++kk) {
-          const int k = kb * KB + kk;
-          const bool live = (k < n) && (status == 0);  // team-uniform
-          const bool cand = live && (row < n) && !used;
-          uint64_t key = cand ? lgm_key(fabs(r[kk])) : 0ull;
-          int wl;
-          uint64_t kmax = lgm_warp_argmax(key, wl);
-          int prow_idx = wit * 32 + wl;
-          if (C::T > 1) {
-            if (lane == 0) {
-              reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
-              reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
-            }
-            team_sync();
-            uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
-            uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
-            int r0 = reinterpret_cast<int*>(kslot + 2)[0];
-            int r1 = reinterpret_cast<int*>(kslot + 2)[1];
-            if (k1 > k0) { kmax = k1; prow_idx = r1; } else { kmax = k0; prow_idx = r0; }
+    for (int k = 0; k < NMAX; ++k) {
+      const double r0 = r[0];
+      double g = 0.0, last = r0;        // defaults: pure rotation (steps k >= n)
+      const double* pr = prow(team, k & 1);
+      if (k < n) {                      // team-uniform
+        const bool cand = (row < n) && !used;
+        uint64_t key = cand ? lgm_key(fabs(r0)) : 0ull;
+        int wl;
+        uint64_t kmax = lgm_warp_argmax(key, wl);
+        int prow_idx = wit * 32 + wl;
+        if (C::T > 1) {
+          if (lane == 0) {
+            reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
+            reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
           }
-          if (live && kmax <= 1ull) status = 1;  // all remaining candidates exactly zero
-          if (live && status == 0) {  // team-uniform
-            double* pr = prow(team, k & 1);
-            const bool own = (row == prow_idx);
-            if (own) {  // one lane publishes its raw row and 1/pivot
-              used = true;
-              my_step = k;
-              const double p = r[kk];
-              mylog = p;  // log|p| taken once after the loop (one pivot per row)
-              rowscale = 1.0 / p;
-#pragma unroll
-              for (int j = 0; j < NMAX; j += 2)
-                *reinterpret_cast<double2*>(pr + j) = make_double2(r[j], r[j + 1]);
-              pr[NMAX] = rowscale;
-              pv[k] = prow_idx;
-            }
-            team_sync();
-            // branch-free elimination: the owner uses g = 0 (row kept raw, scaled at the end)
-            const double g = own ? 0.0 : r[kk] * pr[NMAX];
-#pragma unroll
-            for (int j = 0; j < NMAX; j += 2) {
-              double2 p2 = *reinterpret_cast<const double2*>(pr + j);
-              if (j != kk) r[j] = fma(-g, p2.x, r[j]);
-              if (j + 1 != kk) r[j + 1] = fma(-g, p2.y, r[j + 1]);
-            }
-            r[kk] = own ? 1.0 : -g;
-          }
+          team_sync();
+          uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
+          uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
+          int i0 = reinterpret_cast<int*>(kslot + 2)[0];
+          int i1 = reinterpret_cast<int*>(kslot + 2)[1];
+          if (k1 > k0) { kmax = k1; prow_idx = i1; } else { kmax = k0; prow_idx = i0; }
         }
+        if (kmax <= 1ull) { status = 1; break; }  // all remaining candidates exactly zero
+        double* pw = prow(team, k & 1);
+        const bool own = (row == prow_idx);
+        if (own) {  // one lane publishes its raw row (current frame) and 1/pivot
+          used = true;
+          my_step = k;
+          mylog = r0;  // log|p| taken once after the loop (one pivot per row)
+          rowscale = 1.0 / r0;
+#pragma unroll
+          for (int j = 0; j < NMAX; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(r[j], r[j + 1]);
+          pw[NMAX] = rowscale;
+          pv[k] = prow_idx;
+        }
+        team_sync();
+        g = own ? 0.0 : r0 * pr[NMAX];  // branch-free: the owner keeps its raw row
+        last = own ? 1.0 : -g;
       }
-      rotate_left<KB>(r);  // every block (also the skipped ones) -> net rotation NMAX = identity
+      // shifted elimination: r[j] <- r[j+1] - g * prow[j+1]; g == 0 -> exact rotation
+#pragma unroll
+      for (int j = 0; j < NMAX; j += 2) {
+        const double2 p2 = *reinterpret_cast<const double2*>(pr + j);  // prow[j], prow[j+1]
+        if (j > 0) r[j - 1] = fma(-g, p2.x, r[j]);
+        r[j] = fma(-g, p2.y, r[j + 1 < NMAX ? j + 1 : j]);
+      }
+      r[NMAX - 1] = last;
     }
     if (rowscale != 1.0) {
 #pragma unroll
@@ -477,7 +459,12 @@ struct Ctx {
   // team's estimator column.  The thread's row (column) of M is held in registers across
   // the p products; x ping-pongs between xa and xb (smem, zero beyond n); on return xa
   // holds the result.
-  __device__ __forceinline__ void apply_pow(const double* M, int p, bool trans, double*& xa, double*& xb) {
+  // (not inlined: called from four sites; shared-memory operands passed as offsets so the
+  // accesses stay LDS/STS)
+  __device__ __noinline__ void apply_pow_off(int mb, int p, bool trans, int oa, int ob) {
+    const double* M = buf(mb);
+    double* xa = sm() + oa;
+    double* xb = sm() + ob;
     double m[NMAX];
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
@@ -495,6 +482,14 @@ struct Ctx {
       }
       if (row < n) xb[row] = (a0 + a1) + (a2 + a3);
       team_sync();
+      double* tt = xa;
+      xa = xb;
+      xb = tt;
+    }
+  }
+  __device__ __forceinline__ void apply_pow(int mb, int p, bool trans, double*& xa, double*& xb) {
+    apply_pow_off(mb, p, trans, (int)(xa - sm()), (int)(xb - sm()));
+    if (p & 1) {
       double* tt = xa;
       xa = xb;
       xb = tt;
@@ -527,8 +522,6 @@ struct Ctx {
   __device__ __noinline__ double estimate(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
     const int t = n < 2 ? n : 2;
     const int total = p1 + (has2 ? 1 : 0);
-    const double* M1 = buf(b1);
-    const double* MA = buf(bA);
     // vec layout: col c uses vec(2c) / vec(2c+1) ping-pong; vec(4), vec(5) = Z cols; vec(7) = h
     double* h = vec(7);
     int* order = misc() + MI_ORDER;
@@ -551,8 +544,8 @@ struct Ctx {
       if (team < ncols) {
         double* xa = vec(2 * team);
         double* xb = vec(2 * team + 1);
-        if (has2) { apply_pow(MA, 1, false, xa, xb); cur ^= 1; }
-        apply_pow(M1, p1, false, xa, xb);
+        if (has2) { apply_pow(bA, 1, false, xa, xb); cur ^= 1; }
+        apply_pow(b1, p1, false, xa, xb);
         cur ^= (p1 & 1);
         // column 1-norm (axis-0 sum); team reduction
         double v = (row < n) ? fabs(xa[row]) : 0.0;
@@ -581,8 +574,8 @@ struct Ctx {
         team_sync();
         double* xa = ya;
         double* xb = yb2;
-        apply_pow(M1, p1, true, xa, xb);
-        if (has2) apply_pow(MA, 1, true, xa, xb);
+        apply_pow(b1, p1, true, xa, xb);
+        if (has2) apply_pow(bA, 1, true, xa, xb);
         if (row < n) vec(4 + team)[row] = xa[row];
       }
       passes += total;

@@ -22,7 +22,8 @@ ap.add_argument("--config", default="2")
 ap.add_argument("--batch", type=int, default=None)
 args = ap.parse_args()
 cfg = args.config if args.config in ("3b", "5b") else int(args.config)
-_lib.load(os.path.join(ROOT, "paper_2401_10089_b200", "_build", "liblogmpoly_b200_prof.so"))
+_lib.load(os.environ.get("LGM_PROF_LIB", os.path.join(ROOT, "paper_2401_10089_b200", "_build",
+                                                      "liblogmpoly_b200_prof.so")))
 lib = _lib._lib
 lib.lgm_debug_phase_cycles.argtypes = [ctypes.c_void_p, ctypes.c_int]
 A = torch.from_numpy(synth.config(cfg, batch=args.batch)).cuda()
