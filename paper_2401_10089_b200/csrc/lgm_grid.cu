@@ -20,6 +20,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "lgm_grid.cuh"
 
 namespace {
@@ -331,6 +333,119 @@ __global__ void gj_init_kernel(const InvJob* jobs, int n) {
 // Factor the panel columns [k0, k0+nb) of every job: GJ elimination of the panel over all
 // rows with partial pivoting among rows not yet used (ties -> lowest row).  The panel
 // lives in shared memory (row stride NB+1) when it fits, else is updated in place.
+// G2 panel (n > 512): one 8-CTA thread-block cluster per inversion.  CTA q of the cluster
+// owns rows [q*rpc, (q+1)*rpc) of the 32-column panel, one row per thread in registers
+// (shift-in-FMA pivot frame as in Engine F).  Per pivot step: block argmax, each CTA
+// publishes its candidate (key, row values) in its own shared memory, one cluster barrier,
+// every CTA reads the 8 candidates over DSMEM and applies the winner.  No grid-wide sync.
+constexpr int CL = 8;
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
+    gj_panel_cluster_kernel(const InvJob* jobs, int n, int k0, int nb) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ unsigned long long s_key[2];
+  __shared__ double s_cand[2][34];  // candidate row (32) + its pivot value
+  __shared__ double s_prow[2][34];  // winner row, local copy
+  __shared__ int s_win[2];
+  __shared__ uint64_t wkey[16];
+  __shared__ int widx[16];
+  const int part = (int)cl.block_rank();
+  const InvJob J = jobs[blockIdx.x / CL];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rpc = (n + CL - 1) / CL;
+  const int row = part * rpc + tid;
+  const bool valid = tid < rpc && row < n;
+  const int st0 = *J.status;
+  if (tid < 2 * 34) (&s_prow[0][0])[tid] = 0.0;  // pure-rotation steps read it with g = 0
+  cl.sync();
+  if (st0) return;  // whole cluster = this job: uniform
+  double r[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) r[c] = (valid && c < nb) ? J.M[(size_t)row * n + k0 + c] : 0.0;
+  bool used = valid ? (J.rowstep[row] >= 0) : true;
+  bool piv_here = false;
+  double rowscale = 1.0;
+  int status = 0;
+#pragma unroll 1
+  for (int kk = 0; kk < 32; ++kk) {
+    const double r0 = r[0];
+    double g = 0.0, last = r0;
+    const int par = kk & 1;
+    const double* pr = s_prow[par];
+    if (kk < nb) {
+      uint64_t key = (valid && !used) ? dkey(fabs(r0)) : 0ull;
+      int idx = (valid && !used) ? row : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        uint64_t k2 = __shfl_xor_sync(0xffffffffu, key, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (k2 > key || (k2 == key && i2 < idx)) { key = k2; idx = i2; }
+      }
+      if (lane == 0) { wkey[warp] = key; widx[warp] = idx; }
+      __syncthreads();
+      if (tid == 0) {
+        uint64_t kb = wkey[0];
+        int ib = widx[0];
+        for (int w = 1; w < 16; ++w)
+          if (wkey[w] > kb || (wkey[w] == kb && widx[w] < ib)) { kb = wkey[w]; ib = widx[w]; }
+        s_key[par] = kb;
+        s_win[par] = ib;
+      }
+      __syncthreads();
+      if (row == s_win[par] && s_key[par] > 0ull) {  // publish this CTA's candidate row
+#pragma unroll
+        for (int c = 0; c < 32; ++c) s_cand[par][c] = r[c];
+      }
+      cl.sync();
+      // winner over the cluster (ties -> lowest row: CTAs own increasing row ranges)
+      uint64_t kb = 0ull;
+      int qb = 0;
+      for (int q = 0; q < CL; ++q) {
+        const uint64_t kq = *cl.map_shared_rank(&s_key[par], q);
+        if (kq > kb) { kb = kq; qb = q; }
+      }
+      if (kb <= 1ull) { status = 1; break; }
+      const int p = *cl.map_shared_rank(&s_win[par], qb);
+      if (tid < 32) s_prow[par][tid] = cl.map_shared_rank(&s_cand[par][0], qb)[tid];
+      __syncthreads();
+      const bool own = valid && (row == p);  // (idle threads' row ids alias other CTAs' rows)
+      const double inv = 1.0 / pr[0];
+      if (own) {
+        used = true;
+        piv_here = true;
+        rowscale = inv;
+        J.rowstep[row] = k0 + kk;
+        J.piv[k0 + kk] = row;
+        *J.logdet += log(fabs(r0));
+      }
+      g = own ? 0.0 : r0 * inv;
+      last = own ? 1.0 : -g;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const double x = pr[j], y = pr[j + 1];
+      if (j > 0) r[j - 1] = fma(-g, x, r[j]);
+      r[j] = fma(-g, y, r[j + 1]);
+    }
+    r[31] = last;
+  }
+  if (status) {
+    if (part == 0 && tid == 0) *J.status = 1;
+    cl.sync();
+    return;
+  }
+  if (piv_here) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] *= rowscale;
+  }
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < nb) J.M[(size_t)row * n + k0 + c] = r[c];
+  }
+  cl.sync();  // keep peers' shared memory alive until every DSMEM read is done
+}
+
 __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n, int k0, int nb, int in_smem) {
   extern __shared__ __align__(16) double psm[];
   __shared__ uint64_t skey[16];
@@ -1118,13 +1233,14 @@ struct Grid {
       return launch_g1<512>(nj);
     }
     lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
-    const size_t psmem = (size_t)n * (NB + 1) * 8;
-    const int in_smem = psmem <= 200 * 1024;
-    if (in_smem) CK(cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     const int tiles = (n + TM - 1) / TM;
     for (int k0 = 0; k0 < n; k0 += NB) {
       const int nb = std::min(NB, n - k0);
-      lgm_count_launch(), gj_panel_kernel<<<nj, 512, in_smem ? psmem : 0, st>>>(d_jobs, n, k0, nb, in_smem);
+      if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
+        lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, st>>>(d_jobs, n, k0, nb);
+      } else {
+        lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, st>>>(d_jobs, n, k0, nb, 0);
+      }
       lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb);
       lgm_count_launch(), gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb);
     }
