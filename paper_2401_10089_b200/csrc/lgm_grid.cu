@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   constexpr int NW = NT / 32;
   double* M = J.M;
   for (int i = tid; i < NT; i += NT) rstep[i] = -1;
+  if (tid < 80) prow[tid] = 0.0;  // pure-rotation steps read it with g = 0
   int my_step = -1;
   double logsum = 0.0;  // sum of log|pivot| of this thread's pivot (at most one)
   int status = 0;
@@ -190,12 +191,15 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     for (int c = 0; c < 32; ++c) r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
     double rowscale = 1.0;
     bool piv_here = false;
-#pragma unroll
-    for (int kk = 0; kk < 32; ++kk) {
-      if (kk < nb && status == 0) {
-        const int par = kk & 1;
+#pragma unroll 1
+    for (int kk = 0; kk < 32; ++kk) {  // shift-in-FMA pivot frame: the pivot column is r[0]
+      const int par = kk & 1;
+      const double* pr = prow + par * 40;
+      const double r0 = r[0];
+      double g = 0.0, last = r0;       // kk >= nb: pure rotation
+      if (kk < nb) {
         const bool cand = (tid < n) && (my_step < 0);
-        uint64_t key = cand ? dkey(fabs(r[kk])) : 0ull;
+        uint64_t key = cand ? dkey(fabs(r0)) : 0ull;
         // warp argmax (ties -> lowest lane = lowest row)
         unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(key >> 32));
         unsigned lo = __reduce_max_sync(0xffffffffu, ((unsigned)(key >> 32) == hi) ? (unsigned)key : 0u);
@@ -211,30 +215,30 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
           if (kw > kb) { kb = kw; p = widx[par * 16 + w]; }
         }
         if (kb <= 1ull) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
-        double* pr = prow + par * 40;
+        double* pw = prow + par * 40;
         const bool own = (tid == p);
         if (own) {
           my_step = k0 + kk;
           piv_here = true;
-          const double pv = r[kk];
-          logsum = log(fabs(pv));
-          rowscale = 1.0 / pv;
+          logsum = log(fabs(r0));
+          rowscale = 1.0 / r0;
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pr + c) = make_double2(r[c], r[c + 1]);
-          pr[32] = rowscale;
+          for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
+          pw[32] = rowscale;
           rstep[tid] = k0 + kk;
           piv[k0 + kk] = tid;
         }
         __syncthreads();
-        const double g = own ? 0.0 : r[kk] * pr[32];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
-          if (c != kk) r[c] = fma(-g, p2.x, r[c]);
-          if (c + 1 != kk) r[c + 1] = fma(-g, p2.y, r[c + 1]);
-        }
-        r[kk] = own ? 1.0 : -g;
+        g = own ? 0.0 : r0 * pr[32];
+        last = own ? 1.0 : -g;
       }
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
+        if (c > 0) r[c - 1] = fma(-g, p2.x, r[c]);
+        r[c] = fma(-g, p2.y, r[c + 1]);
+      }
+      r[31] = last;
     }
     if (status) break;
     if (piv_here) {  // deferred scaling of this panel's pivot row
