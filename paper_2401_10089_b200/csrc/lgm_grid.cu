@@ -158,7 +158,7 @@ constexpr int G1_LDW = 36;  // W chunk row stride
 template <int NT>
 struct G1Smem {
   static constexpr size_t A = (size_t)NT * G1_LDA;  // doubles
-  static constexpr size_t W = 32 * G1_LDW;
+  static constexpr size_t W = 2 * 32 * G1_LDW;  // double-buffered pivot-row snapshot
   static constexpr size_t PR = 2 * 40;
   static constexpr size_t bytes = (A + W + PR) * 8 + 2 * (size_t)NT * 4 + 64 * 16;
 };
@@ -257,31 +257,47 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       for (int c = 0; c < 32; ++c) As[tid * G1_LDA + c] = 0.0;
     }
     __syncthreads();
-    // trailing update, column blocks of 32 outside the panel
+    // trailing update, column blocks of 32 outside the panel.  The pivot-row snapshot of
+    // the next block is taken into the other half of Ws while the current block is updated
+    // (one barrier per block); C fragments move as 16-byte accesses when n is even.
     const int g8 = lane >> 2, t4 = lane & 3;
     const int r0 = warp * 32;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      if (j0 == k0) continue;  // the panel itself (panels are 32-aligned)
-      // snapshot pivot rows' block: Ws[c][jj] = M[piv[k0+c]][j0+jj]
+    const bool vec = (n & 1) == 0;
+    auto snap = [&](int jb, double* W) {
       for (int idx = tid; idx < 32 * 32; idx += NT) {
         const int c = idx >> 5, jj = idx & 31;
-        Ws[c * G1_LDW + jj] = (c < nb && j0 + jj < n) ? M[(size_t)piv[k0 + c] * n + j0 + jj] : 0.0;
+        W[c * G1_LDW + jj] = (c < nb && jb + jj < n) ? M[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
       }
-      __syncthreads();
+    };
+    int jcur = (k0 == 0) ? 32 : 0;
+    int buf = 0;
+    if (jcur < n) snap(jcur, Ws);
+    __syncthreads();
+    while (jcur < n) {
+      int jnext = jcur + 32;
+      if (jnext == k0) jnext += 32;
+      if (jnext < n) snap(jnext, Ws + (buf ^ 1) * 32 * G1_LDW);
+      const double* Wc = Ws + buf * 32 * G1_LDW;
+      const int j0 = jcur;
       if (r0 < n) {
         double acc[4][4][2];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
           const int i = r0 + mi * 8 + g8;
           const int rs = (i < n) ? rstep[i] : -1;
-          const bool zero_row = (rs >= k0 && rs < k0 + nb);
+          const bool live_row = i < n && !(rs >= k0 && rs < k0 + nb);
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
+          for (int ni = 0; ni < 4; ++ni) {
+            const int j = j0 + ni * 8 + 2 * t4;
+            if (vec && live_row && j + 1 < n) {
+              const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)i * n + j]);
+              acc[mi][ni][0] = v.x;
+              acc[mi][ni][1] = v.y;
+            } else {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int j = j0 + ni * 8 + 2 * t4 + e;
-              acc[mi][ni][e] = (i < n && j < n && !zero_row) ? M[(size_t)i * n + j] : 0.0;
+              for (int e = 0; e < 2; ++e) acc[mi][ni][e] = (live_row && j + e < n) ? M[(size_t)i * n + j + e] : 0.0;
             }
+          }
         }
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
@@ -289,7 +305,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi) a[mi] = As[(r0 + mi * 8 + g8) * G1_LDA + k + t4];
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) b[ni] = Ws[(k + t4) * G1_LDW + ni * 8 + g8];
+          for (int ni = 0; ni < 4; ++ni) b[ni] = Wc[(k + t4) * G1_LDW + ni * 8 + g8];
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -300,15 +316,21 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
           const int i = r0 + mi * 8 + g8;
           if (i >= n) continue;
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
+          for (int ni = 0; ni < 4; ++ni) {
+            const int j = j0 + ni * 8 + 2 * t4;
+            if (vec && j + 1 < n) {
+              *reinterpret_cast<double2*>(&M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            } else {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int j = j0 + ni * 8 + 2 * t4 + e;
-              if (j < n) M[(size_t)i * n + j] = acc[mi][ni][e];
+              for (int e = 0; e < 2; ++e)
+                if (j + e < n) M[(size_t)i * n + j + e] = acc[mi][ni][e];
             }
+          }
         }
       }
       __syncthreads();
+      jcur = jnext;
+      buf ^= 1;
     }
   }
   // publish pivots, log|det|, status
