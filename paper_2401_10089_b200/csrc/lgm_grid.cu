@@ -157,7 +157,7 @@ constexpr int G1_LDW = 36;  // W chunk row stride
 
 template <int NT>
 struct G1Smem {
-  static constexpr size_t A = (size_t)NT * G1_LDA;  // doubles
+  static constexpr size_t A = 32 * (size_t)(NT + 4);  // doubles: panel stored transposed, row stride NT+4
   static constexpr size_t W = 2 * 32 * G1_LDW;  // double-buffered pivot-row snapshot
   static constexpr size_t PR = 2 * 40;
   static constexpr size_t bytes = (A + W + PR) * 8 + 2 * (size_t)NT * 4 + 64 * 16;
@@ -250,11 +250,11 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         if (c < nb) M[(size_t)tid * n + k0 + c] = r[c];
-        As[tid * G1_LDA + c] = (c < nb) ? r[c] : 0.0;
+        As[c * (NT + 4) + tid] = (c < nb) ? r[c] : 0.0;  // transposed: conflict-free row writes
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) As[tid * G1_LDA + c] = 0.0;
+      for (int c = 0; c < 32; ++c) As[c * (NT + 4) + tid] = 0.0;
     }
     __syncthreads();
     // trailing update, column blocks of 32 outside the panel.  The pivot-row snapshot of
@@ -269,6 +269,22 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
         W[c * G1_LDW + jj] = (c < nb && jb + jj < n) ? M[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
       }
     };
+    // next block's snapshot: loads issued before the block's DMMA work, stored after it
+    constexpr int SNP = (32 * 32 + NT - 1) / NT;
+    auto snap_load = [&](int jb, double (&v)[SNP]) {
+#pragma unroll
+      for (int q = 0; q < SNP; ++q) {
+        const int idx = tid + q * NT, c = idx >> 5, jj = idx & 31;
+        v[q] = (idx < 1024 && c < nb && jb + jj < n) ? M[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
+      }
+    };
+    auto snap_store = [&](const double (&v)[SNP], double* W) {
+#pragma unroll
+      for (int q = 0; q < SNP; ++q) {
+        const int idx = tid + q * NT;
+        if (idx < 1024) W[(idx >> 5) * G1_LDW + (idx & 31)] = v[q];
+      }
+    };
     int jcur = (k0 == 0) ? 32 : 0;
     int buf = 0;
     if (jcur < n) snap(jcur, Ws);
@@ -276,7 +292,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     while (jcur < n) {
       int jnext = jcur + 32;
       if (jnext == k0) jnext += 32;
-      if (jnext < n) snap(jnext, Ws + (buf ^ 1) * 32 * G1_LDW);
+      double sv[SNP];
+      if (jnext < n) snap_load(jnext, sv);
       const double* Wc = Ws + buf * 32 * G1_LDW;
       const int j0 = jcur;
       if (r0 < n) {
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
         for (int k = 0; k < 32; k += 4) {
           double a[4], b[4];
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) a[mi] = As[(r0 + mi * 8 + g8) * G1_LDA + k + t4];
+          for (int mi = 0; mi < 4; ++mi) a[mi] = As[(k + t4) * (NT + 4) + r0 + mi * 8 + g8];
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) b[ni] = Wc[(k + t4) * G1_LDW + ni * 8 + g8];
 #pragma unroll
@@ -328,6 +345,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
           }
         }
       }
+      if (jnext < n) snap_store(sv, Ws + (buf ^ 1) * 32 * G1_LDW);
       __syncthreads();
       jcur = jnext;
       buf ^= 1;
