@@ -187,8 +187,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   for (int k0 = 0; k0 < n && status == 0; k0 += 32) {
     const int nb = min(32, n - k0);
     double r[32];
+    // (per-thread row loads: measured faster than staging through shared memory)
 #pragma unroll
-    for (int c = 0; c < 32; ++c) r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
+    for (int c = 0; c < 32; c += 2) {
+      if (tid < n && c + 1 < nb && (n & 1) == 0) {
+        const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)tid * n + k0 + c]);
+        r[c] = v.x;
+        r[c + 1] = v.y;
+      } else {
+        r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
+        r[c + 1] = (tid < n && c + 1 < nb) ? M[(size_t)tid * n + k0 + c + 1] : 0.0;
+      }
+    }
     double rowscale = 1.0;
     bool piv_here = false;
 #pragma unroll 1
