@@ -913,8 +913,10 @@ __global__ void __launch_bounds__(256) est_fwd_kernel(EstJob* jobs, int n, int q
   }
 }
 
-constexpr int ADJ_ROWS = 256;
-__global__ void __launch_bounds__(256) est_adj_kernel(EstJob* jobs, int n, int q) {
+constexpr int ADJ_ROWS = 64;
+// z = M^T x: thread per column, a 64-row slab per CTA (partials reduced in fixed order by
+// est_adj_reduce_kernel), 4 independent accumulators per column.
+__global__ void __launch_bounds__(128) est_adj_kernel(EstJob* jobs, int n, int q) {
   EstJob& J = jobs[blockIdx.z];
   if (J.done || q >= J.total) return;
   const double* M = (q < J.p1) ? J.M1 : J.M2;
@@ -922,15 +924,24 @@ __global__ void __launch_bounds__(256) est_adj_kernel(EstJob* jobs, int n, int q
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int r0 = blockIdx.y * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
   if (j >= n) return;
-  const int nc = J.ncols;
-  double a0 = 0.0, a1 = 0.0;
-  for (int r = r0; r < r1; ++r) {
-    const double m = M[(size_t)r * n + j];
-    a0 = fma(m, x[r], a0);
-    if (nc > 1) a1 = fma(m, x[n + r], a1);
+  const bool two = J.ncols > 1;
+  double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double m = M[(size_t)(r + u) * n + j];
+      a0[u] = fma(m, x[r + u], a0[u]);
+      if (two) a1[u] = fma(m, x[n + r + u], a1[u]);
+    }
   }
-  J.part[((size_t)blockIdx.y * 2 + 0) * n + j] = a0;
-  J.part[((size_t)blockIdx.y * 2 + 1) * n + j] = a1;
+  for (; r < r1; ++r) {
+    const double m = M[(size_t)r * n + j];
+    a0[0] = fma(m, x[r], a0[0]);
+    if (two) a1[0] = fma(m, x[n + r], a1[0]);
+  }
+  J.part[((size_t)blockIdx.y * 2 + 0) * n + j] = (a0[0] + a0[1]) + (a0[2] + a0[3]);
+  J.part[((size_t)blockIdx.y * 2 + 1) * n + j] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
 }
 
 __global__ void est_adj_reduce_kernel(EstJob* jobs, int n, int q, int splits) {
@@ -1333,7 +1344,7 @@ struct Grid {
       for (int q = 0; q < maxtot; ++q) lgm_count_launch(), est_fwd_kernel<<<dim3((n + 7) / 8, nj), 256, 0, st>>>(d_est, n, q);
       lgm_count_launch(), est_after_fwd_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
       for (int q = 0; q < maxtot; ++q) {
-        lgm_count_launch(), est_adj_kernel<<<dim3((n + 255) / 256, splits, nj), 256, 0, st>>>(d_est, n, q);
+        lgm_count_launch(), est_adj_kernel<<<dim3((n + 127) / 128, splits, nj), 128, 0, st>>>(d_est, n, q);
         lgm_count_launch(), est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
       }
       lgm_count_launch(), est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
