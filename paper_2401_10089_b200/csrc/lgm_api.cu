@@ -18,7 +18,7 @@ int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed);
 // ------------------------------------------------------------------------------ kernels
 
 template <int NMAX>
-__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 8 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
+__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 7 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
                                                                   lgm_report* rep, long long ld, int n, double* ws,
                                                                   const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];
@@ -99,9 +99,8 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) degopt_kernel(const double* __r
   for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
   __syncthreads();
   int prods = 0;
-  double* const extra[3] = {c.sm() + Cfg<NMAX>::SMEM_DOUBLES, c.sm() + Cfg<NMAX>::SMEM_DOUBLES + Cfg<NMAX>::MAT,
-                            c.sm() + Cfg<NMAX>::SMEM_DOUBLES + 2 * Cfg<NMAX>::MAT};
-  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, extra, Cfg<NMAX>::LDM, 1.0, false, Z + b * n * ld, ld, prods);
+  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, c.sm() + Cfg<NMAX>::SMEM_DOUBLES, Cfg<NMAX>::LDM, Cfg<NMAX>::MAT, 1.0,
+           false, Z + b * n * ld, ld, prods);
   if (c.tid == 0) products[b] = prods;
 }
 

@@ -172,7 +172,15 @@ struct Ctx {
     return res;
   }
 
+  // Non-inlined entry points work on a register copy of the context: member accesses
+  // through `this` would otherwise be local-memory loads inside the hot loops.
   __device__ __noinline__ int balance(int b, int max_sweeps) {
+    Ctx s = *this;
+    const int r = s.balance_impl(b, max_sweeps);
+    mm = s.mm;
+    return r;
+  }
+  __device__ __forceinline__ int balance_impl(int b, int max_sweeps) {
     double* B = buf(b);
     double* sc = scale();
     for (int i = tid; i < n; i += C::NT) sc[i] = 1.0;
@@ -348,6 +356,15 @@ struct Ctx {
   // X (buffer bx) is replaced by X^(1/2); buffer by is workspace (Y).  Returns status
   // (0, LGM_SINGULAR, LGM_DB_NOCONV, LGM_NONFINITE); iters = iterations performed.
   __device__ __noinline__ int sqrt_db(int bx, int by, double tol, int maxiter, int& iters) {
+    Ctx s = *this;
+    int it = 0;
+    const int r = s.sqrt_db_impl(bx, by, tol, maxiter, it);
+    iters = it;
+    mm = s.mm;
+    plateau = s.plateau;
+    return r;
+  }
+  __device__ __forceinline__ int sqrt_db_impl(int bx, int by, double tol, int maxiter, int& iters) {
     double* X = buf(bx);
     double* Y = buf(by);
     set_identity(by);
@@ -461,8 +478,11 @@ struct Ctx {
   // holds the result.
   // (not inlined: called from four sites; shared-memory operands passed as offsets so the
   // accesses stay LDS/STS)
-  __device__ __noinline__ void apply_pow_off(int mb, int p, bool trans, int oa, int ob) {
-    const double* M = buf(mb);
+  // (static: the context values come in as arguments, so callers working on a register copy
+  // of the context never have its address taken)
+  __device__ __noinline__ static void apply_pow_off(int mb, int p, bool trans, int oa, int ob, int n, int row,
+                                                    int team) {
+    const double* M = sm() + mb * C::MAT;
     double* xa = sm() + oa;
     double* xb = sm() + ob;
     double m[NMAX];
@@ -481,14 +501,15 @@ struct Ctx {
         a3 = fma(m[j + 3], x23.y, a3);
       }
       if (row < n) xb[row] = (a0 + a1) + (a2 + a3);
-      team_sync();
+      if (C::T == 1) __syncwarp();
+      else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(C::T * 32) : "memory");
       double* tt = xa;
       xa = xb;
       xb = tt;
     }
   }
   __device__ __forceinline__ void apply_pow(int mb, int p, bool trans, double*& xa, double*& xb) {
-    apply_pow_off(mb, p, trans, (int)(xa - sm()), (int)(xb - sm()));
+    apply_pow_off(mb, p, trans, (int)(xa - sm()), (int)(xb - sm()), n, row, team);
     if (p & 1) {
       double* tt = xa;
       xa = xb;
@@ -520,6 +541,14 @@ struct Ctx {
   // Operator = M1^p1 [* MA] with M1 = buf(b1), MA = buf(bA) (matrices stored explicitly,
   // e.g. A - I materialised like numpy's B - I).
   __device__ __noinline__ double estimate(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
+    Ctx s = *this;
+    int ps = passes;
+    const double e = s.estimate_impl(b1, p1, has2, bA, itmax, ps);
+    passes = ps;
+    mm = s.mm;
+    return e;
+  }
+  __device__ __forceinline__ double estimate_impl(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
     const int t = n < 2 ? n : 2;
     const int total = p1 + (has2 ? 1 : 0);
     // vec layout: col c uses vec(2c) / vec(2c+1) ping-pong; vec(4), vec(5) = Z cols; vec(7) = h
@@ -635,30 +664,44 @@ struct Ctx {
     return est;
   }
 
-  // ---- GEMM with fused left combination -------------------------------------------------
-  // A polynomial node: row-major matrix at `p` with row stride `ld` (shared or global).
-  struct Node {
-    const double* p;
-    int ld;
+  // ---- degree-optimal polynomial (schemes.py:104-126) -----------------------------------
+  // Nodes P1 = I, P2 = buf(bX), P3 = buf(b3), P4..P6 = ext + (t-4)*ext_stride (row stride
+  // ext_ld; shared or a global workspace slot).  All node addressing is arithmetic on the
+  // (compile-time) slot index t, so no local-memory arrays are involved.
+  struct Nodes {
+    const double* p2;
+    const double* p3;
+    double* ext;
+    int ext_ld, ext_stride;
+    __device__ __forceinline__ const double* ptr(int t) const {
+      return t == 2 ? p2 : (t == 3 ? p3 : ext + (t - 4) * ext_stride);
+    }
+    __device__ __forceinline__ int ld(int t) const { return t <= 3 ? C::LDM : ext_ld; }
   };
-  // acc[jj] = sum_kk L[row][kk] * R[kk][col0 + jj], col0 = team * NMAX/2, where
-  // L = sum_t lc[t] * node[t] + l0 * I computed on the fly with numpy's _combine
-  // rounding (schemes.py:91-101: products and sums rounded separately, no FMA).
-  static constexpr int MAXT = 7;
-  __device__ void gemm_comb(int nterm, const double (&lc)[MAXT], const Node (&ln)[MAXT], double l0,
-                            const double* R, double (&acc)[NMAX / 2]) {
+  static constexpr int TMAX = 7;  // nodes P2..P7
+
+  // acc[jj] = sum_kk L[row][kk] * R[kk][col0 + jj], col0 = team * NMAX/2, with
+  // L = sum_{t=2..nn} crow[t-1] * P_t + crow[0] * I formed on the fly with numpy's _combine
+  // rounding (schemes.py:91-101: sequential over t, zero coefficients skipped, products and
+  // sums rounded separately).
+  __device__ void gemm_comb(const Nodes& nd, int nn, const double* crow, const double* R, double (&acc)[NMAX / 2]) {
     const int col0 = team * (NMAX / 2);
 #pragma unroll
     for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = 0.0;
     if (row >= n) return;
-    const double* Lb[MAXT];
+    const double* Lr[TMAX - 1];
+    double cf[TMAX - 1];
 #pragma unroll
-    for (int q = 0; q < MAXT; ++q) Lb[q] = ln[q].p + row * ln[q].ld;
+    for (int t = 2; t <= TMAX; ++t) {
+      cf[t - 2] = (t <= nn) ? crow[t - 1] : 0.0;
+      Lr[t - 2] = nd.ptr(t) + row * nd.ld(t);
+    }
+    const double l0 = crow[0];
     for (int kk = 0; kk < n; ++kk) {
       double l = 0.0;
 #pragma unroll
-      for (int q = 0; q < MAXT; ++q)
-        if (q < nterm) l = __dadd_rn(l, __dmul_rn(lc[q], Lb[q][kk]));
+      for (int t = 2; t <= TMAX; ++t)
+        if (cf[t - 2] != 0.0) l = __dadd_rn(l, __dmul_rn(cf[t - 2], Lr[t - 2][kk]));
       if (kk == row && l0 != 0.0) l = __dadd_rn(l, l0);
       const double* Rr = R + kk * C::LDM + col0;
 #pragma unroll
@@ -666,31 +709,21 @@ struct Ctx {
     }
   }
 
-  // D[i][j] = sum_t c[t] * node[t][i][j] + c0 * I (schemes.py:91-101 order); D in smem.
-  __device__ void combine_into(double* D, int nterm, const double (&c)[MAXT], const Node (&nd)[MAXT], double c0) {
+  // D[i][j] = sum_{t=2..nn} crow[t-1] P_t[i][j] + crow[0] I (schemes.py:91-101 order)
+  __device__ void combine_into(double* D, const Nodes& nd, int nn, const double* crow) {
+    double cf[TMAX - 1];
+#pragma unroll
+    for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? crow[t - 1] : 0.0;
+    const double c0 = crow[0];
     for (int i = warp; i < n; i += C::NT / 32)
       for (int j = lane; j < n; j += 32) {
         double v = 0.0;
 #pragma unroll
-        for (int q = 0; q < MAXT; ++q)
-          if (q < nterm) v = __dadd_rn(v, __dmul_rn(c[q], nd[q].p[i * nd[q].ld + j]));
+        for (int t = 2; t <= TMAX; ++t)
+          if (cf[t - 2] != 0.0) v = __dadd_rn(v, __dmul_rn(cf[t - 2], nd.ptr(t)[i * nd.ld(t) + j]));
         if (i == j && c0 != 0.0) v = __dadd_rn(v, c0);
         D[i * C::LDM + j] = v;
       }
-  }
-
-  // Gather the non-zero coefficients of a combination row over nodes P1..P_{nn}
-  // (P1 = I, P_t = nodes[t]).
-  __device__ static int gather_terms(const double* crow, int nn, const Node* nodes, double (&c)[MAXT],
-                                     Node (&nd)[MAXT], double& c0) {
-    int q = 0;
-    c0 = crow[0];
-#pragma unroll
-    for (int t = 0; t < MAXT; ++t) { c[t] = 0.0; nd[t] = nodes[2]; }
-    for (int t = 2; t <= nn; ++t) {
-      if (crow[t - 1] != 0.0) { c[q] = crow[t - 1]; nd[q] = nodes[t]; q++; }
-    }
-    return q;
   }
 
   __device__ void store_half_rows(double* D, int ld, const double (&acc)[NMAX / 2]) {
@@ -702,29 +735,25 @@ struct Ctx {
     }
   }
 
-  // ---- degree-optimal polynomial (schemes.py:104-126) + fused epilogue ------------------
-  // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp: one product), R is
-  // the shared combination temp; P4..P6 live in `extra` (shared or a global workspace slot,
-  // row stride extra_ld).  The last node stays in registers; the epilogue forms z, scales
-  // by `mult` (= -2^s), reverts the balancing (matcore.py:175-177) when `unbal` is set,
-  // stages through R and writes row-major to Lg (ld).
-  __device__ __noinline__ void degopt(int k, int bX, int b3, bool have_fp, int bR, double* const (&extra)[3],
-                                      int extra_ld, double mult, bool unbal, double* Lg, long long ldg,
+  // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp: one product), R temp
+  // buf(bR), P4..P6 in `ext`.  The last node stays in registers; the epilogue forms z,
+  // scales by `mult` (= -2^s), reverts the balancing (matcore.py:175-177) when `unbal` is
+  // set, stages through R and writes row-major to Lg (ld).
+  __device__ __noinline__ void degopt(int k, int bX, int b3, bool have_fp, int bR, double* ext, int ext_ld,
+                                      int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
                                       int& products) {
-    Node nodes[8];
-    nodes[0] = nodes[1] = nodes[7] = Node{buf(bX), C::LDM};
-    nodes[2] = Node{buf(bX), C::LDM};
-    nodes[3] = Node{buf(b3), C::LDM};
-    for (int t = 0; t < 3; ++t) nodes[4 + t] = Node{extra[t], extra_ld};
+    Ctx s = *this;
+    s.degopt_impl(k, bX, b3, have_fp, bR, ext, ext_ld, ext_stride, mult, unbal, Lg, ldg, products);
+  }
+  __device__ __forceinline__ void degopt_impl(int k, int bX, int b3, bool have_fp, int bR, double* ext, int ext_ld,
+                                              int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
+                                              int& products) {
+    Nodes nd{buf(bX), buf(b3), ext, ext_ld, ext_stride};
     double* R = buf(bR);
     double acc[NMAX / 2];
-    double c[MAXT], c0;
-    Node nd[MAXT];
     if (!have_fp) {  // P3 = P2 * P2
-      c[0] = 1.0;
-      for (int q = 1; q < MAXT; ++q) c[q] = 0.0;
-      for (int q = 0; q < MAXT; ++q) nd[q] = nodes[2];
-      gemm_comb(1, c, nd, 0.0, buf(bX), acc);
+      const double one[2] = {0.0, 1.0};
+      gemm_comb(nd, 2, one, buf(bX), acc);
       products++;
       __syncthreads();
       store_half_rows(buf(b3), C::LDM, acc);
@@ -733,18 +762,14 @@ struct Ctx {
     int nn = 3;  // nodes P1..P3 available
     bool last_in_regs = false;
     for (int j = 1; j < k; ++j) {
-      const double* lrow = lgm_lhs(*P, k, j);
-      const double* rrow = lgm_rhs(*P, k, j);
-      int nt = gather_terms(rrow, nn, nodes, c, nd, c0);
-      combine_into(R, nt, c, nd, c0);
+      combine_into(R, nd, nn, lgm_rhs(*P, k, j));
       __syncthreads();
-      nt = gather_terms(lrow, nn, nodes, c, nd, c0);
-      gemm_comb(nt, c, nd, c0, R, acc);
+      gemm_comb(nd, nn, lgm_lhs(*P, k, j), R, acc);
       products++;
       nn++;
       __syncthreads();
       if (j < k - 1) {
-        store_half_rows(const_cast<double*>(nodes[nn].p), nodes[nn].ld, acc);
+        store_half_rows(const_cast<double*>(nd.ptr(nn)), nd.ld(nn), acc);
         __syncthreads();
       } else {
         last_in_regs = true;
@@ -755,16 +780,19 @@ struct Ctx {
     const double* sc = scale();
     if (row < n) {
       const int col0 = team * (NMAX / 2);
+      double cf[TMAX - 1];
+#pragma unroll
+      for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? orow[t - 1] : 0.0;
 #pragma unroll
       for (int jj = 0; jj < NMAX / 2; ++jj) {
         const int col = col0 + jj;
         if (col < n) {
           double v = 0.0;
-          for (int t = 2; t <= nn; ++t) {
-            double ct = orow[t - 1];
-            if (ct != 0.0) {
-              double pv = (t == nn && last_in_regs) ? acc[jj] : nodes[t].p[row * nodes[t].ld + col];
-              v = __dadd_rn(v, __dmul_rn(ct, pv));
+#pragma unroll
+          for (int t = 2; t <= TMAX; ++t) {
+            if (cf[t - 2] != 0.0) {
+              const double pv = (t == nn && last_in_regs) ? acc[jj] : nd.ptr(t)[row * nd.ld(t) + col];
+              v = __dadd_rn(v, __dmul_rn(cf[t - 2], pv));
             }
           }
           if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
@@ -993,11 +1021,10 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   c.minus_identity(BUF_Y, BUF_B);  // A - I: estimator operand in select, GEMM operand below
   __syncthreads();
   if (!have_ai2) {  // s = 0: A_I2 = (B - I)(B - I), one product
-    double cc[Ctx<NMAX>::MAXT] = {1.0};
-    typename Ctx<NMAX>::Node bb[Ctx<NMAX>::MAXT];
-    for (int q = 0; q < Ctx<NMAX>::MAXT; ++q) bb[q] = {c.buf(BUF_Y), Cfg<NMAX>::LDM};
+    typename Ctx<NMAX>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), nullptr, 0, 0};  // P2 := A - I
+    const double one[2] = {0.0, 1.0};
     double acc[NMAX / 2];
-    c.gemm_comb(1, cc, bb, 0.0, c.buf(BUF_Y), acc);
+    c.gemm_comb(nd, 2, one, c.buf(BUF_Y), acc);
     products++;
     if (c.row < n) {
       double* D = c.buf(BUF_P) + c.row * Cfg<NMAX>::LDM + c.team * (NMAX / 2);
@@ -1023,10 +1050,10 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
     }
   }
   __syncthreads();
-  double* const extra[3] = {ws, ws + n * n, ws + 2 * n * n};  // P4..P6: this matrix's workspace slot
+  // P4..P6: this matrix's workspace slot (3 n^2 doubles, row stride n)
   {
     LGM_PHASE_BEGIN(c);
-    c.degopt(k, BUF_B, BUF_P, true, BUF_Y, extra, n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
+    c.degopt(k, BUF_B, BUF_P, true, BUF_Y, ws, n, n * n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
     LGM_PHASE_END(c, 4);
   }
   R.k = k;
