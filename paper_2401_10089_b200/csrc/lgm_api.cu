@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) est_kernel(const double* __rest
   int ps = 0;
   double e = 0.0;
   bool go = true;
+  c.init_ramp();
   if (zero_shortcut) go = c.any_nonzero(2, 0.0);  // matcore.py:309-310
   if (go) e = c.estimate(2, p1, M2 != nullptr, 0, itmax, ps);
   if (c.tid == 0) { est[b] = e; passes[b] = ps; }

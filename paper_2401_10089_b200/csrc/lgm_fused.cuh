@@ -43,7 +43,7 @@ struct Cfg {
   static constexpr int OFF_PROW = NBUF * MAT;                // [2 teams][2][NMAX+2]
   static constexpr int PROW = NMAX + 2;
   static constexpr int OFF_VEC = OFF_PROW + 2 * 2 * PROW;    // [8][NMAX]
-  static constexpr int OFF_SCALE = OFF_VEC + 8 * NMAX;       // [NMAX] balancing scales
+  static constexpr int OFF_SCALE = OFF_VEC + 9 * NMAX;       // [NMAX] balancing scales
   static constexpr int OFF_RED = OFF_SCALE + NMAX;           // [64] reduction scratch
   static constexpr int OFF_INT = OFF_RED + 64;               // ints: piv[2][NMAX], misc[64]
   static constexpr int SMEM_DOUBLES = OFF_INT + (2 * NMAX + 64 + 1) / 2 + 1;
@@ -105,6 +105,20 @@ struct Ctx {
   __device__ __forceinline__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
 
   // ---- elementwise helpers ------------------------------------------------------------
+  // Estimator restart column (matcore.py:265-271): v_i = (-1)^i (1 + i/max(1, n-1)),
+  // normalised by numpy's pairwise sum of |v|; built once per matrix into vec(8).
+  __device__ void init_ramp() {
+    if (tid == 0) {
+      red()[RD_EST] = lgm_pairwise_sum(
+          [&](int i) { return fabs(((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))); }, n);
+    }
+    __syncthreads();
+    const double rsum = red()[RD_EST];
+    for (int i = tid; i < n; i += C::NT)
+      vec(8)[i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
+    __syncthreads();
+  }
+
   __device__ void zero_all() {
     // matrices, pivot rows, estimator vectors and scales (padding must read as 0)
     static_assert(C::OFF_RED % 2 == 0, "double2 zeroing");
@@ -556,11 +570,10 @@ struct Ctx {
     int* order = misc() + MI_ORDER;
     // initial block X (matcore.py:265-271)
     {
-      double rsum = lgm_pairwise_sum(
-          [&](int i) { return fabs(((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))); }, n);
+      const double inv_n = 1.0 / n;
       for (int i = tid; i < n; i += C::NT) {
-        vec(0)[i] = 1.0 / n;
-        if (t > 1) vec(2)[i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
+        vec(0)[i] = inv_n;
+        if (t > 1) vec(2)[i] = vec(8)[i];  // normalised ramp, built once per matrix (init_ramp)
       }
     }
     __syncthreads();
@@ -941,6 +954,7 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   int n = c.n;
   c.zero_all();
   __syncthreads();
+  c.init_ramp();
   if (c.load(BUF_B, Ag, ld)) {
     R.status = LGM_NONFINITE;
     if (c.tid == 0) *rep = R;
