@@ -203,26 +203,61 @@ struct Ctx {
     for (int sw = 0; sw < max_sweeps; ++sw) {
       sweeps++;
       bool moved = false;
+      const int m8 = n - (n % 8);
       for (int i = 0; i < n; ++i) {
-        // every thread evaluates the (pairwise-ordered) sums redundantly: uniform decisions
-        double dg = fabs(B[i * C::LDM + i]);
-        double c = pw_abs_sum(B + i, C::LDM) - dg;
-        double r = pw_abs_sum(B + i * C::LDM, 1) - dg;
-        if (c == 0.0 || r == 0.0) continue;
-        double tot = c + r, f = 1.0;
-        while (true) {
-          note(c, r / 2.0);
-          if (!(c < r / 2.0)) break;
-          c *= 2.0; r /= 2.0; f *= 2.0;
+        // numpy pairwise sums of |B[:, i]| (lanes 0-7) and |B[i, :]| (lanes 8-15) of warp 0:
+        // the 8 interleaved accumulators, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by
+        // xor-shuffles (commutative adds), tail added in order by lane 0.  Lane 0 decides;
+        // only its margin record is reported.
+        if (warp == 0) {
+          const int q = lane & 7;
+          const bool colside = lane < 8;
+          const double* base = colside ? B + i : B + i * C::LDM;
+          const int stride = colside ? C::LDM : 1;
+          double acc = 0.0;
+          if (n >= 8 && lane < 16) {
+            acc = fabs(base[q * stride]);
+            for (int k = 8 + q; k < m8; k += 8) acc += fabs(base[k * stride]);
+          }
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+          double csum = __shfl_sync(0xffffffffu, acc, 0);
+          double rsum = __shfl_sync(0xffffffffu, acc, 8);
+          if (lane == 0) {
+            if (n < 8) {
+              csum = 0.0;
+              rsum = 0.0;
+              for (int k = 0; k < n; ++k) csum += fabs(B[k * C::LDM + i]);
+              for (int k = 0; k < n; ++k) rsum += fabs(B[i * C::LDM + k]);
+            } else {
+              for (int k = m8; k < n; ++k) csum += fabs(B[k * C::LDM + i]);
+              for (int k = m8; k < n; ++k) rsum += fabs(B[i * C::LDM + k]);
+            }
+            const double dg = fabs(B[i * C::LDM + i]);
+            double c = csum - dg, r = rsum - dg, f = 0.0;
+            if (!(c == 0.0 || r == 0.0)) {
+              double tot = c + r;
+              f = 1.0;
+              while (true) {
+                note(c, r / 2.0);
+                if (!(c < r / 2.0)) break;
+                c *= 2.0; r /= 2.0; f *= 2.0;
+              }
+              while (true) {
+                note(c, r * 2.0);
+                if (!(c >= r * 2.0)) break;
+                c /= 2.0; r *= 2.0; f /= 2.0;
+              }
+              note(c + r, 0.95 * tot);
+              if (!(c + r < 0.95 * tot && 1e-300 < f && f < 1e300)) f = 0.0;
+            }
+            red()[RD_MARGIN + (i & 1)] = f;  // 0: leave row/column i alone (double-buffered)
+          }
         }
-        while (true) {
-          note(c, r * 2.0);
-          if (!(c >= r * 2.0)) break;
-          c /= 2.0; r *= 2.0; f /= 2.0;
-        }
-        note(c + r, 0.95 * tot);
-        if (c + r < 0.95 * tot && 1e-300 < f && f < 1e300) {
-          __syncthreads();  // all threads finished reading column/row i
+        __syncthreads();
+        const double f = red()[RD_MARGIN + (i & 1)];
+        if (f != 0.0) {
           double inv = 1.0 / f;  // exact: f is a power of two in (1e-300, 1e300)
           for (int q = tid; q < n; q += C::NT) B[q * C::LDM + i] *= f;
           __syncthreads();
