@@ -18,14 +18,14 @@ int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed);
 // ------------------------------------------------------------------------------ kernels
 
 template <int NMAX>
-__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 7 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
+__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 8 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
                                                                   lgm_report* rep, long long ld, int n, double* ws,
                                                                   const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];
   Ctx<NMAX> c;
   c.init(smem, n, &P);
   const long long b = blockIdx.x;
-  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 3 * n * n);
+  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 4 * n * n);
 }
 
 template <int NMAX>
@@ -57,14 +57,15 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) est_kernel(const double* __rest
   const long long b = blockIdx.x;
   c.zero_all();
   __syncthreads();
-  c.load(2, M1 + b * n * ld, ld);
-  if (M2) c.load(0, M2 + b * n * ld, ld);
+  typedef typename Ctx<NMAX>::MRef MR;
+  const MR m1{const_cast<double*>(M1) + b * n * ld, (int)ld};
+  const MR m2{M2 ? const_cast<double*>(M2) + b * n * ld : nullptr, (int)ld};
   int ps = 0;
   double e = 0.0;
   bool go = true;
   c.init_ramp();
-  if (zero_shortcut) go = c.any_nonzero(2, 0.0);  // matcore.py:309-310
-  if (go) e = c.estimate(2, p1, M2 != nullptr, 0, itmax, ps);
+  if (zero_shortcut) go = c.any_nonzero_ref(m1);  // matcore.py:309-310
+  if (go) e = c.estimate(m1, p1, M2 != nullptr, m2, itmax, ps);
   if (c.tid == 0) { est[b] = e; passes[b] = ps; }
 }
 
@@ -96,11 +97,17 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT) degopt_kernel(const double* __r
   c.zero_all();
   __syncthreads();
   c.load(BUF_B, X + b * n * ld, ld);
-  if (FP) c.load(BUF_P, FP + b * n * ld, ld);
+  // P3 (the first product) and P4..P6 in the extra shared buffers of this kernel
+  typedef typename Ctx<NMAX>::MRef MR;
+  const MR p3{c.sm() + Cfg<NMAX>::SMEM_DOUBLES, Cfg<NMAX>::LDM};
+  if (FP) {
+    for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+      for (int j = c.lane; j < n; j += 32) p3.p[i * Cfg<NMAX>::LDM + j] = FP[b * n * ld + (long long)i * ld + j];
+  }
   for (int i = c.tid; i < n; i += Cfg<NMAX>::NT) c.scale()[i] = 1.0;
   __syncthreads();
   int prods = 0;
-  c.degopt(k, BUF_B, BUF_P, FP != nullptr, BUF_Y, c.sm() + Cfg<NMAX>::SMEM_DOUBLES, Cfg<NMAX>::LDM, Cfg<NMAX>::MAT, 1.0,
+  c.degopt(k, BUF_B, p3, FP != nullptr, BUF_Y, c.sm() + Cfg<NMAX>::SMEM_DOUBLES + Cfg<NMAX>::MAT, Cfg<NMAX>::LDM, Cfg<NMAX>::MAT, 1.0,
            false, Z + b * n * ld, ld, prods);
   if (c.tid == 0) products[b] = prods;
 }
@@ -165,8 +172,8 @@ long long lgm_launch_count(void) { return g_lgm_launches.load(std::memory_order_
 
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
-  // n <= 64: one 3 n^2 slot per matrix for the polynomial nodes P4..P6 (L2 resident)
-  *bytes = n <= 64 ? (size_t)batch * 3 * n * n * sizeof(double) : lgm_grid_workspace_bytes(n, batch);
+  // n <= 64: one 4 n^2 slot per matrix: polynomial nodes P4..P6 and A_prev / A_I2 (L2 resident)
+  *bytes = n <= 64 ? (size_t)batch * 4 * n * n * sizeof(double) : lgm_grid_workspace_bytes(n, batch);
   return 0;
 }
 

@@ -38,7 +38,7 @@ struct Cfg {
   static constexpr int NT = 64 * T;       // threads per CTA
   static constexpr int LDM = NMAX + 1;    // padded row stride (doubles)
   static constexpr int MAT = NMAX * LDM;  // doubles per matrix buffer
-  static constexpr int NBUF = 3;          // B (X), Y, A_prev / A_I2
+  static constexpr int NBUF = 2;          // B (X) and Y; A_prev / A_I2 and P4..P6 live in L2
   // shared-memory carve-up (in doubles)
   static constexpr int OFF_PROW = NBUF * MAT;                // [2 teams][2][NMAX+2]
   static constexpr int PROW = NMAX + 2;
@@ -49,7 +49,7 @@ struct Cfg {
   static constexpr int SMEM_DOUBLES = OFF_INT + (2 * NMAX + 64 + 1) / 2 + 1;
   static constexpr size_t SMEM_BYTES = (size_t)SMEM_DOUBLES * sizeof(double);
   // kernels that keep the polynomial nodes P4..P6 in shared memory too (building blocks)
-  static constexpr size_t SMEM_BYTES_X = SMEM_BYTES + 3 * MAT * sizeof(double);
+  static constexpr size_t SMEM_BYTES_X = SMEM_BYTES + 4 * MAT * sizeof(double);
 };
 
 // misc int slots
@@ -70,6 +70,12 @@ struct Ctx {
   int plateau;     // DB stop tests in the noise band [tol/10, 10 tol] (uniform)
 
   __device__ __forceinline__ static double* sm() { return lgm_smem; }
+  // a matrix operand: shared buffer (row stride LDM) or global workspace slot (row stride n)
+  struct MRef {
+    double* p;
+    int ld;
+  };
+  __device__ MRef bref(int b) const { return MRef{buf(b), C::LDM}; }
   __device__ double* buf(int b) const { return sm() + b * C::MAT; }
   __device__ double* prow(int tm, int parity) const { return sm() + C::OFF_PROW + (tm * 2 + parity) * C::PROW; }
   __device__ double* vec(int v) const { return sm() + C::OFF_VEC + v * NMAX; }
@@ -139,6 +145,24 @@ struct Ctx {
       for (int j = lane; j < n; j += 32) {
       d[i * C::LDM + j] = (i == j) ? 1.0 : 0.0;
     }
+  }
+
+  // onenorm of a referenced matrix (numpy order: column sums over rows in order)
+  __device__ double onenorm_ref(MRef M) {
+    double cs = 0.0;
+    for (int j = tid; j < n; j += C::NT) {
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc = (i == 0) ? fabs(M.p[i * M.ld + j]) : acc + fabs(M.p[i * M.ld + j]);
+      cs = fmax(cs, acc);
+    }
+    cs = lgm_warp_max(cs);
+    __syncthreads();
+    if (lane == 0) red()[RD_NORM + warp] = cs;
+    __syncthreads();
+    double r = red()[RD_NORM];
+    for (int w = 1; w < C::NT / 32; ++w) r = fmax(r, red()[RD_NORM + w]);
+    __syncthreads();
+    return r;
   }
 
   // onenorm(M - shift*I) exactly as numpy: column sums accumulated over rows in order.
@@ -529,15 +553,14 @@ struct Ctx {
   // accesses stay LDS/STS)
   // (static: the context values come in as arguments, so callers working on a register copy
   // of the context never have its address taken)
-  __device__ __noinline__ static void apply_pow_off(int mb, int p, bool trans, int oa, int ob, int n, int row,
-                                                    int team) {
-    const double* M = sm() + mb * C::MAT;
+  __device__ __noinline__ static void apply_pow_off(const double* M, int ldM, int p, bool trans, int oa, int ob, int n,
+                                                    int row, int team) {
     double* xa = sm() + oa;
     double* xb = sm() + ob;
     double m[NMAX];
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
-      m[j] = (row < n && j < n) ? (trans ? M[j * C::LDM + row] : M[row * C::LDM + j]) : 0.0;
+      m[j] = (row < n && j < n) ? (trans ? M[j * ldM + row] : M[row * ldM + j]) : 0.0;
     for (int q = 0; q < p; ++q) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
@@ -557,8 +580,8 @@ struct Ctx {
       xb = tt;
     }
   }
-  __device__ __forceinline__ void apply_pow(int mb, int p, bool trans, double*& xa, double*& xb) {
-    apply_pow_off(mb, p, trans, (int)(xa - sm()), (int)(xb - sm()), n, row, team);
+  __device__ __forceinline__ void apply_pow(MRef M, int p, bool trans, double*& xa, double*& xb) {
+    apply_pow_off(M.p, M.ld, p, trans, (int)(xa - sm()), (int)(xb - sm()), n, row, team);
     if (p & 1) {
       double* tt = xa;
       xa = xb;
@@ -577,6 +600,13 @@ struct Ctx {
       }
   }
 
+  __device__ bool any_nonzero_ref(MRef M) {
+    bool nz = false;
+    for (int i = warp; i < n; i += C::NT / 32)
+      for (int j = lane; j < n; j += 32) nz |= M.p[i * M.ld + j] != 0.0;
+    return __syncthreads_or(nz);
+  }
+
   __device__ bool any_nonzero(int b, double sh) {
     bool nz = false;
     const double* M = buf(b);
@@ -589,7 +619,7 @@ struct Ctx {
 
   // Operator = M1^p1 [* MA] with M1 = buf(b1), MA = buf(bA) (matrices stored explicitly,
   // e.g. A - I materialised like numpy's B - I).
-  __device__ __noinline__ double estimate(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
+  __device__ __noinline__ double estimate(MRef b1, int p1, bool has2, MRef bA, int itmax, int& passes) {
     Ctx s = *this;
     int ps = passes;
     const double e = s.estimate_impl(b1, p1, has2, bA, itmax, ps);
@@ -597,7 +627,7 @@ struct Ctx {
     mm = s.mm;
     return e;
   }
-  __device__ __forceinline__ double estimate_impl(int b1, int p1, bool has2, int bA, int itmax, int& passes) {
+  __device__ __forceinline__ double estimate_impl(MRef b1, int p1, bool has2, MRef bA, int itmax, int& passes) {
     const int t = n < 2 ? n : 2;
     const int total = p1 + (has2 ? 1 : 0);
     // vec layout: col c uses vec(2c) / vec(2c+1) ping-pong; vec(4), vec(5) = Z cols; vec(7) = h
@@ -719,12 +749,13 @@ struct Ctx {
   struct Nodes {
     const double* p2;
     const double* p3;
+    int p3_ld;
     double* ext;
     int ext_ld, ext_stride;
     __device__ __forceinline__ const double* ptr(int t) const {
       return t == 2 ? p2 : (t == 3 ? p3 : ext + (t - 4) * ext_stride);
     }
-    __device__ __forceinline__ int ld(int t) const { return t <= 3 ? C::LDM : ext_ld; }
+    __device__ __forceinline__ int ld(int t) const { return t == 2 ? C::LDM : (t == 3 ? p3_ld : ext_ld); }
   };
   static constexpr int TMAX = 7;  // nodes P2..P7
 
@@ -787,16 +818,16 @@ struct Ctx {
   // buf(bR), P4..P6 in `ext`.  The last node stays in registers; the epilogue forms z,
   // scales by `mult` (= -2^s), reverts the balancing (matcore.py:175-177) when `unbal` is
   // set, stages through R and writes row-major to Lg (ld).
-  __device__ __noinline__ void degopt(int k, int bX, int b3, bool have_fp, int bR, double* ext, int ext_ld,
+  __device__ __noinline__ void degopt(int k, int bX, MRef b3, bool have_fp, int bR, double* ext, int ext_ld,
                                       int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
                                       int& products) {
     Ctx s = *this;
     s.degopt_impl(k, bX, b3, have_fp, bR, ext, ext_ld, ext_stride, mult, unbal, Lg, ldg, products);
   }
-  __device__ __forceinline__ void degopt_impl(int k, int bX, int b3, bool have_fp, int bR, double* ext, int ext_ld,
+  __device__ __forceinline__ void degopt_impl(int k, int bX, MRef b3, bool have_fp, int bR, double* ext, int ext_ld,
                                               int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
                                               int& products) {
-    Nodes nd{buf(bX), buf(b3), ext, ext_ld, ext_stride};
+    Nodes nd{buf(bX), b3.p, b3.ld, ext, ext_ld, ext_stride};
     double* R = buf(bR);
     double acc[NMAX / 2];
     if (!have_fp) {  // P3 = P2 * P2
@@ -804,7 +835,7 @@ struct Ctx {
       gemm_comb(nd, 2, one, buf(bX), acc);
       products++;
       __syncthreads();
-      store_half_rows(buf(b3), C::LDM, acc);
+      store_half_rows(b3.p, b3.ld, acc);
       __syncthreads();
     }
     int nn = 3;  // nodes P1..P3 available
@@ -876,12 +907,12 @@ struct Ctx {
   }
 
   // ---- Algorithm 1 (oracle/driver.py logm_status) ----------------------------------------
-  __device__ __noinline__ double alpha(int bB, bool have_ai2, int bAI2, double nA, int m, double theta,
+  // bB: A - I (shared), bAI2: A_I2 (global workspace slot), nI2 = ||A_I2||_1 (cached per root)
+  __device__ __noinline__ double alpha(MRef bB, bool have_ai2, MRef bAI2, double nA, double nI2, int m, double theta,
                           double (&cache)[16], unsigned& cvalid, int& nest, int& passes) {
     const int itmax = P->est_itmax;
     double t1, Pm;
     if (have_ai2) {
-      double nI2 = onenorm(bAI2, 0.0);
       double r2 = sqrt(nI2);
       if (le(r2, theta)) {  // Eq. 27
         t1 = r2;
@@ -890,7 +921,7 @@ struct Ctx {
         if (!((cvalid >> m) & 1u)) {
           nest++;
           double e = 0.0;
-          if (any_nonzero(bAI2, 0.0)) e = estimate(bAI2, m / 2, false, bB, itmax, passes);
+          if (any_nonzero_ref(bAI2)) e = estimate(bAI2, m / 2, false, bB, itmax, passes);
           cache[m] = e; cvalid |= 1u << m;
         }
         Pm = cache[m];
@@ -900,7 +931,7 @@ struct Ctx {
       if (!((cvalid >> m) & 1u)) {
         nest++;
         double e = 0.0;
-        if (any_nonzero(bB, 0.0)) e = estimate(bB, m, false, bB, itmax, passes);
+        if (any_nonzero_ref(bB)) e = estimate(bB, m, false, bB, itmax, passes);
         cache[m] = e; cvalid |= 1u << m;
       }
       Pm = cache[m];
@@ -920,7 +951,7 @@ struct Ctx {
           e = estimate(bAI2, m / 2, true, bB, itmax, passes);
         } else {
           e = 0.0;
-          if (any_nonzero(bB, 0.0)) e = estimate(bB, m + 1, false, bB, itmax, passes);
+          if (any_nonzero_ref(bB)) e = estimate(bB, m + 1, false, bB, itmax, passes);
         }
         cache[m + 1] = e; cvalid |= 1u << (m + 1);
       }
@@ -936,12 +967,11 @@ struct Ctx {
   }
 
   // returns k; cert = alpha certifying k
-  __device__ __noinline__ int select(int bB, int bAI2, double nA, double alpha_loop, double (&cache)[16], unsigned& cvalid,
-                        int& nest, int& passes, double& cert) {
+  __device__ __noinline__ int select(MRef bB, MRef bAI2, double nA, double nI2, double alpha_loop, double (&cache)[16],
+                        unsigned& cvalid, int& nest, int& passes, double& cert) {
     const int K = P->max_k;
     const double* th = P->theta;
     const int* mk = P->order;
-    double nI2 = onenorm(bAI2, 0.0);
     double r2 = sqrt(nI2);
     int mK = mk[K - 1];
     int min_im;
@@ -969,7 +999,7 @@ struct Ctx {
     double cert_max = found ? max_bound : alpha_loop;
     if (min_im >= max_in) { cert = cert_max; return max_in; }
     for (int j = min_im; j < max_in; ++j) {
-      double a = alpha(bB, true, bAI2, nA, mk[j - 1], th[j - 1], cache, cvalid, nest, passes);
+      double a = alpha(bB, true, bAI2, nA, nI2, mk[j - 1], th[j - 1], cache, cvalid, nest, passes);
       if (le(a, th[j - 1])) { cert = a; return j; }
       if (le(a, th[j])) { cert = a; return j + 1; }
     }
@@ -979,7 +1009,7 @@ struct Ctx {
 };
 
 // Buffer roles in the fused logm kernel
-enum { BUF_B = 0, BUF_Y = 1, BUF_P = 2 };
+enum { BUF_B = 0, BUF_Y = 1 };
 
 template <int NMAX>
 __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep, double* ws) {
@@ -1011,6 +1041,9 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   unsigned cvalid = 0u;
   int nest = 0, passes = 0, s = 0, db_iters = 0, products = 0;
   bool have_ai2 = false;
+  // A_prev / A_I2 in this matrix's workspace slot 3 (row stride n)
+  const typename Ctx<NMAX>::MRef AI2{ws + 3 * n * n, n};
+  double nI2 = 0.0;
   double alpha_loop = c.onenorm(BUF_B, 1.0);
   bool finish = c.le(alpha_loop, thK);
   int status = 0;
@@ -1021,13 +1054,17 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
       LGM_PHASE_BEGIN(c);
       c.minus_identity(BUF_Y, BUF_B);  // A - I materialised as numpy does (estimator operand)
       __syncthreads();
-      a = c.alpha(BUF_Y, have_ai2, BUF_P, nA, mK, thK, cache, cvalid, nest, passes);
+      a = c.alpha(c.bref(BUF_Y), have_ai2, AI2, nA, nI2, mK, thK, cache, cvalid, nest, passes);
       LGM_PHASE_END(c, 1);
     }
     alpha_loop = a;
     finish = c.le(a, thK);
     if (!finish) {
-      c.copy_buf(BUF_P, BUF_B);
+      {  // A_prev = B
+        const double* Bm = c.buf(BUF_B);
+        for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+          for (int j = c.lane; j < n; j += 32) AI2.p[i * n + j] = Bm[i * Cfg<NMAX>::LDM + j];
+      }
       __syncthreads();
       int its = 0;
       {
@@ -1038,16 +1075,27 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
       db_iters += its;
       if (status) break;
       s++;
-      // A_I2 = A_prev - 2 B + I, in place over A_prev
+      // A_I2 = A_prev - 2 B + I, in place over A_prev; its 1-norm (numpy
+      // order: column sums over rows in order) is cached for the next alpha / select
       {
-        double* Pm = c.buf(BUF_P);
         const double* Bm = c.buf(BUF_B);
-        for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
-          for (int j = c.lane; j < n; j += 32) {
-          double v = Pm[i * Cfg<NMAX>::LDM + j] - 2.0 * Bm[i * Cfg<NMAX>::LDM + j];
-          if (i == j) v = v + 1.0;
-          Pm[i * Cfg<NMAX>::LDM + j] = v;
+        double cs = 0.0;
+        for (int j = c.tid; j < n; j += Cfg<NMAX>::NT) {
+          double acc = 0.0;
+          for (int i = 0; i < n; ++i) {
+            double v = AI2.p[i * n + j] - 2.0 * Bm[i * Cfg<NMAX>::LDM + j];
+            if (i == j) v = v + 1.0;
+            AI2.p[i * n + j] = v;
+            acc = (i == 0) ? fabs(v) : acc + fabs(v);
+          }
+          cs = fmax(cs, acc);
         }
+        cs = lgm_warp_max(cs);
+        __syncthreads();
+        if (c.lane == 0) c.red()[RD_NORM + c.warp] = cs;
+        __syncthreads();
+        nI2 = c.red()[RD_NORM];
+        for (int w = 1; w < Cfg<NMAX>::NT / 32; ++w) nI2 = fmax(nI2, c.red()[RD_NORM + w]);
       }
       have_ai2 = true;
       cvalid = 0u;
@@ -1070,23 +1118,20 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   c.minus_identity(BUF_Y, BUF_B);  // A - I: estimator operand in select, GEMM operand below
   __syncthreads();
   if (!have_ai2) {  // s = 0: A_I2 = (B - I)(B - I), one product
-    typename Ctx<NMAX>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), nullptr, 0, 0};  // P2 := A - I
+    typename Ctx<NMAX>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), Cfg<NMAX>::LDM, nullptr, 0, 0};  // P2 := A - I
     const double one[2] = {0.0, 1.0};
     double acc[NMAX / 2];
     c.gemm_comb(nd, 2, one, c.buf(BUF_Y), acc);
     products++;
-    if (c.row < n) {
-      double* D = c.buf(BUF_P) + c.row * Cfg<NMAX>::LDM + c.team * (NMAX / 2);
-#pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj) if (c.team * (NMAX / 2) + jj < n) D[jj] = acc[jj];
-    }
+    c.store_half_rows(AI2.p, AI2.ld, acc);
     __syncthreads();
+    nI2 = c.onenorm_ref(AI2);
   }
   double cert = 0.0;
   int k;
   {
     LGM_PHASE_BEGIN(c);
-    k = c.select(BUF_Y, BUF_P, nA, alpha_loop, cache, cvalid, nest, passes, cert);
+    k = c.select(c.bref(BUF_Y), AI2, nA, nI2, alpha_loop, cache, cvalid, nest, passes, cert);
     LGM_PHASE_END(c, 3);
   }
   // P2 = I - B (the schemes approximate -log(I - X), schemes.py:129-131); B is dead now.
@@ -1102,7 +1147,7 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   // P4..P6: this matrix's workspace slot (3 n^2 doubles, row stride n)
   {
     LGM_PHASE_BEGIN(c);
-    c.degopt(k, BUF_B, BUF_P, true, BUF_Y, ws, n, n * n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
+    c.degopt(k, BUF_B, AI2, true, BUF_Y, ws, n, n * n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
     LGM_PHASE_END(c, 4);
   }
   R.k = k;
