@@ -192,16 +192,28 @@ def logm_batched(A, opts=None, devices=None):
                 Ad = Ab[lo:hi].to(device=dev, dtype=torch.float64).contiguous()
             L, rep, ws = run_device(Ad, opts)
             outs.append((lo, hi, dev, L, rep, Ad, ws))
-    Ls, reps = [], []
+    # gather: reports always to (pinned) host memory; L to host (pinned, one async copy per
+    # shard) for numpy / CPU-tensor input, else to the input's device (no copy when a single
+    # shard already lives there)
+    n = Ab.shape[-1]
+    rep_host = torch.empty(max(B, 1) * _lib.REPORT_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+    to_host = was_numpy or not Ab.is_cuda
+    if to_host:
+        Lh = torch.empty((B, n, n), dtype=torch.float64, pin_memory=True)
     for lo, hi, dev, L, rep, Ad, ws in outs:
-        reps.append(rep.cpu().numpy().view(_lib.REPORT_DTYPE)[: hi - lo])
-        Ls.append(L)
-    reports = np.concatenate(reps) if reps else np.zeros(0, dtype=_lib.REPORT_DTYPE)
-    if was_numpy:
-        Lout = np.concatenate([L.cpu().numpy() for L in Ls]) if Ls else np.zeros((0,) + Ab.shape[1:])
+        isz = _lib.REPORT_DTYPE.itemsize
+        rep_host[lo * isz:hi * isz].copy_(rep[: (hi - lo) * isz], non_blocking=True)
+        if to_host:
+            Lh[lo:hi].copy_(L, non_blocking=True)
+    for dev in {o[2] for o in outs}:
+        torch.cuda.synchronize(dev)
+    reports = rep_host.numpy().view(_lib.REPORT_DTYPE)[:B]
+    if to_host:
+        Lout = Lh.numpy() if was_numpy else Lh
+    elif len(outs) == 1 and outs[0][2] == Ab.device:
+        Lout = outs[0][3]
     else:
-        target = Ab.device
-        Lout = torch.cat([L.to(target) for L in Ls]) if Ls else torch.empty_like(Ab)
+        Lout = torch.cat([o[3].to(Ab.device) for o in outs]) if outs else torch.empty_like(Ab)
     if opts.raise_on_error:
         bad = np.nonzero(reports["status"] != 0)[0]
         if bad.size:
