@@ -598,39 +598,73 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
   // skip tiles whose columns all lie in the panel
   if (col0 >= k0 && col0 + TN <= k0 + nb) return;
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < TM * TK; idx += 128) {
-    int r = idx / TK, c = idx - r * TK;
-    int i = row0 + r;
-    As[r * LDA_S + c] = (i < n && c < nb) ? J.M[(size_t)i * n + k0 + c] : 0.0;
-  }
-  for (int idx = tid; idx < TK * TN; idx += 128) {
-    int c = idx / TN, jj = idx - c * TN;
-    int j = col0 + jj;
-    Bs[c * LDB_S + jj] = (c < nb && j < n) ? J.W[(size_t)c * n + j] : 0.0;
-  }
-  __syncthreads();
-  double acc[4][4][2];
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-  tile_mma(As, Bs, acc);
   const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
+  const bool vec = (n & 1) == 0;
+  // C fragments first (their latency overlaps the A / W staging below); pivot rows of this
+  // panel start from zero, panel columns are left alone
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+    const int rs = (i < n) ? J.rowstep[i] : -1;
+    const bool live = i < n && !(rs >= k0 && rs < k0 + nb);
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = c0 + ni * 8 + 2 * t;
+      if (vec && live && j + 1 < n) {
+        const double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)i * n + j]);
+        acc[mi][ni][0] = v.x;
+        acc[mi][ni][1] = v.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[mi][ni][e] = (live && j + e < n) ? J.M[(size_t)i * n + j + e] : 0.0;
+      }
+    }
+  }
+  for (int idx = tid; idx < TM * (TK / 2); idx += 128) {
+    const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
+    const int i = row0 + r;
+    double2 v = make_double2(0.0, 0.0);
+    if (i < n) {
+      if (vec && c + 1 < nb) v = *reinterpret_cast<const double2*>(&J.M[(size_t)i * n + k0 + c]);
+      else {
+        v.x = (c < nb) ? J.M[(size_t)i * n + k0 + c] : 0.0;
+        v.y = (c + 1 < nb) ? J.M[(size_t)i * n + k0 + c + 1] : 0.0;
+      }
+    }
+    As[r * LDA_S + c] = v.x;
+    As[r * LDA_S + c + 1] = v.y;
+  }
+  for (int idx = tid; idx < TK * (TN / 2); idx += 128) {
+    const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
+    const int j = col0 + jj;
+    double2 v = make_double2(0.0, 0.0);
+    if (c < nb) {
+      if (vec && j + 1 < n) v = *reinterpret_cast<const double2*>(&J.W[(size_t)c * n + j]);
+      else {
+        v.x = (j < n) ? J.W[(size_t)c * n + j] : 0.0;
+        v.y = (j + 1 < n) ? J.W[(size_t)c * n + j + 1] : 0.0;
+      }
+    }
+    *reinterpret_cast<double2*>(&Bs[c * LDB_S + jj]) = v;
+  }
+  __syncthreads();
+  tile_mma(As, Bs, acc);
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
     const int i = r0 + mi * 8 + g;
     if (i >= n) continue;
-    const int rs = J.rowstep[i];
-    const bool zero_row = (rs >= k0 && rs < k0 + nb);
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = c0 + ni * 8 + 2 * t + e;
-        if (j >= n || (j >= k0 && j < k0 + nb)) continue;
-        double* cp = &J.M[(size_t)i * n + j];
-        *cp = (zero_row ? 0.0 : *cp) + acc[mi][ni][e];
+      const int j = c0 + ni * 8 + 2 * t;
+      const bool in0 = j < n && !(j >= k0 && j < k0 + nb);
+      const bool in1 = j + 1 < n && !(j + 1 >= k0 && j + 1 < k0 + nb);
+      if (vec && in0 && in1) {
+        *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      } else {
+        if (in0) J.M[(size_t)i * n + j] = acc[mi][ni][0];
+        if (in1) J.M[(size_t)i * n + j + 1] = acc[mi][ni][1];
       }
     }
   }
@@ -1374,6 +1408,7 @@ struct Grid {
     for (int k0 = 0; k0 < n; k0 += NB) {
       const int nb = std::min(NB, n - k0);
       if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
+        PhaseTimer pt(PH_OTHER, st);  // (profiling only: panel share of the G2 inversion)
         lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, st>>>(d_jobs, n, k0, nb);
       } else {
         lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, st>>>(d_jobs, n, k0, nb, 0);
