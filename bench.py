@@ -145,9 +145,39 @@ def _cpu_worker(chunk):
     return ok
 
 
+def _cpu_serial(As, cores):
+    """Mode 1 of BASELINE.md section 2: serial over matrices, BLAS on all cores (a spawned
+    child so OPENBLAS_NUM_THREADS takes effect)."""
+    ctx = mp.get_context("spawn")
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    with ctx.Pool(1, initializer=_cpu_serial_init, initargs=(cores,)) as pool:
+        pool.map(_cpu_worker, [As[:1]])
+        t0 = time.perf_counter()
+        pool.map(_cpu_worker, [As])
+        return time.perf_counter() - t0
+
+
+def _cpu_serial_init(cores):
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+
+
+def cpu_mode(n):
+    """The faster of BASELINE.md's two modes for this size (probe: the pool wins for
+    n <= 128, where the path is Python-overhead bound; all-core BLAS beyond)."""
+    return "pool" if n <= 128 else "serial"
+
+
+def mode_text(n, cores):
+    return (f"process pool x{cores}, OPENBLAS_NUM_THREADS=1" if cpu_mode(n) == "pool"
+            else f"serial over matrices, OPENBLAS_NUM_THREADS={cores}")
+
+
 def cpu_time(As, cores):
-    """Time the oracle port over matrices As with a pool of `cores` single-BLAS-thread
-    workers (mode 2 of BASELINE.md section 2).  Returns wall seconds."""
+    """Time the oracle port over matrices As on `cores` host cores.  Returns wall seconds."""
+    if cpu_mode(As.shape[-1]) == "serial":
+        return _cpu_serial(As, cores)
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
     chunks = [c for c in np.array_split(As, max(1, min(len(As), cores * 4))) if len(c)]
@@ -279,12 +309,12 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
-        sample = args.cpu_sample or (B if n <= 64 else max(4, min(B, 8)))
+        sample = args.cpu_sample or (B if n <= 64 else (max(4, min(B, 8)) if n <= 1024 else 1))
         secs = cpu_time(A_np[:sample], cores)
         cpu = {"value": sample / secs, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"first {sample} of the {B} config-{args.config} matrices, oracle port "
-                         f"(oracle/driver.py over numpy/scipy/OpenBLAS), process pool x{cores}, "
-                         f"OPENBLAS_NUM_THREADS=1, {secs:.2f} s wall"}
+                         f"(oracle/driver.py over numpy/scipy/OpenBLAS), {mode_text(n, cores)}, "
+                         f"{secs:.2f} s wall"}
 
     status_counts = {int(s): int(c) for s, c in zip(*np.unique(reps["status"], return_counts=True))}
     line = {
@@ -326,10 +356,11 @@ def run_reference(args, cfg, rank, world):
     A_np, name = workload(cfg, batch=args.batch)
     B, n, _ = A_np.shape
     cores = host_cores()
-    sample = args.cpu_sample or (256 if n <= 64 else max(2, min(B, cores)))
+    sample = args.cpu_sample or (256 if n <= 64 else (max(2, min(B, cores)) if n <= 256 else
+                                                      (2 if n <= 1024 else 1)))
     sample = min(sample, B)
     for _ in range(min(args.warmup, 1)):
-        cpu_time(A_np[:min(sample, cores)], cores)
+        cpu_time(A_np[:min(sample, cores if cpu_mode(n) == "pool" else 1)], cores)
     secs = []
     for s in range(args.steps):
         lo = (s * sample) % B
@@ -346,7 +377,7 @@ def run_reference(args, cfg, rank, world):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{sample} matrices of config {args.config} per step, oracle port "
                                    f"(oracle/driver.py: restated driver over the numpy/scipy restatement of the "
-                                   f"reference primitives), process pool x{cores}, OPENBLAS_NUM_THREADS=1"},
+                                   f"reference primitives), {mode_text(n, cores)}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
