@@ -158,12 +158,48 @@ def run_device(A_dev, opts, stream=None):
     return L, rep, ws
 
 
-def logm_batched(A, opts=None, devices=None):
+_STREAMS = {}
+
+
+def _host_chunks(B, n):
+    """Chunking of a host-resident batch for the copy/compute pipeline: Engine F launches
+    (n <= lgm_max_fused_n) of >= 1300 matrices (about one resident wave at n = 32) so the
+    H2D of chunk i+1 and the D2H of chunk i-1 overlap chunk i's kernel (measured at config
+    2: 1 chunk 4.79 ms, 2: 4.19, 3: 3.97, 4: 4.07, 8: 4.19).  Engine G is host-orchestrated
+    per launch, so it keeps one chunk."""
+    if n > int(_lib.load().lgm_max_fused_n()):
+        return 1
+    return max(1, min(6, B // 1300))
+
+
+def _streams(dev, count):
+    key = (dev.index, count)
+    if key not in _STREAMS:
+        _STREAMS[key] = [_torch().cuda.Stream(dev) for _ in range(count)]
+    return _STREAMS[key]
+
+
+_REP_STAGING = {}
+
+
+def _rep_staging(nbytes):
+    """Pinned staging for the per-matrix reports (reused: pinned allocation costs ~1 ms)."""
+    buf = _REP_STAGING.get("buf")
+    if buf is None or buf.numel() < nbytes:
+        buf = _torch().empty(max(nbytes, 1 << 16), dtype=_torch().uint8, pin_memory=True)
+        _REP_STAGING["buf"] = buf
+    return buf
+
+
+def logm_batched(A, opts=None, devices=None, out=None):
     """Batched principal logarithm of (B, n, n) (or (n, n)) float64 matrices.
 
     Returns (L, reports) where ``reports`` is a numpy structured array (REPORT_DTYPE), one
     record per matrix.  With ``opts.raise_on_error`` (default) the first failing matrix
-    raises the reference's exception type.
+    raises the reference's exception type.  ``out``: optional host buffer for L when the
+    input is on the host (numpy array or CPU tensor of the input's shape, float64,
+    contiguous; pinned memory lets the copies overlap the kernels) -- repeated callers
+    pass one to avoid a pinned allocation per call.
     """
     torch = _torch()
     opts = opts or LogmOptions()
@@ -178,38 +214,56 @@ def logm_batched(A, opts=None, devices=None):
     devices = [torch.device(d) for d in devices]
     B = Ab.shape[0]
     G = len(devices)
+    n = Ab.shape[-1]
     bounds = [(g * B) // G for g in range(G + 1)]
+    isz = _lib.REPORT_DTYPE.itemsize
+    # reports always go to (pinned) host memory; L to pinned host memory for numpy / CPU
+    # tensor input (chunked H2D -> kernel -> D2H pipeline, one stream per chunk), else it
+    # stays on the device (no copy when a single shard already lives there)
+    rep_host = _rep_staging(max(B, 1) * isz)
+    to_host = was_numpy or not Ab.is_cuda
+    if to_host:
+        if out is None:
+            Lh = torch.empty((B, n, n), dtype=torch.float64, pin_memory=True)
+        else:
+            Lh = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
+            if (tuple(Lh.shape[-3:] if Lh.dim() == 3 else (1,) + tuple(Lh.shape)) != (B, n, n)
+                    or Lh.dtype != torch.float64 or Lh.is_cuda or not Lh.is_contiguous()):
+                raise ValueError("out must be a contiguous float64 host buffer of the input's shape")
+            Lh = Lh.view(B, n, n)
+        host = (torch.from_numpy(Ab) if was_numpy else Ab.to(torch.float64)).contiguous()
     outs = []
     for g, dev in enumerate(devices):
         lo, hi = bounds[g], bounds[g + 1]
         if hi == lo:
             continue
         with torch.cuda.device(dev):
-            if was_numpy:
-                host = torch.from_numpy(Ab[lo:hi])
-                Ad = host.pin_memory().to(dev, non_blocking=True) if G > 1 else host.to(dev)
+            if to_host:
+                nc = _host_chunks(hi - lo, n)
+                cb = [lo + ((hi - lo) * c) // nc for c in range(nc + 1)]
+                cur = torch.cuda.current_stream(dev)
+                for c, s in enumerate(_streams(dev, nc)):
+                    a, b = cb[c], cb[c + 1]
+                    s.wait_stream(cur)
+                    with torch.cuda.stream(s):
+                        Ad = host[a:b].to(dev, non_blocking=True)
+                        L, rep, ws = run_device(Ad, opts, s)
+                        Lh[a:b].copy_(L, non_blocking=True)
+                        rep_host[a * isz:b * isz].copy_(rep[:(b - a) * isz], non_blocking=True)
+                    outs.append((a, b, dev, L, rep, Ad, ws))
             else:
                 Ad = Ab[lo:hi].to(device=dev, dtype=torch.float64).contiguous()
-            L, rep, ws = run_device(Ad, opts)
-            outs.append((lo, hi, dev, L, rep, Ad, ws))
-    # gather: reports always to (pinned) host memory; L to host (pinned, one async copy per
-    # shard) for numpy / CPU-tensor input, else to the input's device (no copy when a single
-    # shard already lives there)
-    n = Ab.shape[-1]
-    rep_host = torch.empty(max(B, 1) * _lib.REPORT_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
-    to_host = was_numpy or not Ab.is_cuda
-    if to_host:
-        Lh = torch.empty((B, n, n), dtype=torch.float64, pin_memory=True)
-    for lo, hi, dev, L, rep, Ad, ws in outs:
-        isz = _lib.REPORT_DTYPE.itemsize
-        rep_host[lo * isz:hi * isz].copy_(rep[: (hi - lo) * isz], non_blocking=True)
-        if to_host:
-            Lh[lo:hi].copy_(L, non_blocking=True)
+                L, rep, ws = run_device(Ad, opts)
+                rep_host[lo * isz:hi * isz].copy_(rep[:(hi - lo) * isz], non_blocking=True)
+                outs.append((lo, hi, dev, L, rep, Ad, ws))
     for dev in {o[2] for o in outs}:
         torch.cuda.synchronize(dev)
-    reports = rep_host.numpy().view(_lib.REPORT_DTYPE)[:B]
+    reports = rep_host[:B * isz].numpy().copy().view(_lib.REPORT_DTYPE)
     if to_host:
-        Lout = Lh.numpy() if was_numpy else Lh
+        if out is not None:
+            Lout = out.reshape(B, n, n) if isinstance(out, np.ndarray) else Lh
+        else:
+            Lout = Lh.numpy() if was_numpy else Lh
     elif len(outs) == 1 and outs[0][2] == Ab.device:
         Lout = outs[0][3]
     else:
