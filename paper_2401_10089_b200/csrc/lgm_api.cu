@@ -17,15 +17,15 @@ int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed);
 
 // ------------------------------------------------------------------------------ kernels
 
-template <int NMAX>
+template <int NMAX, bool FULL>
 __global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 8 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
                                                                   lgm_report* rep, long long ld, int n, double* ws,
                                                                   const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];
-  Ctx<NMAX> c;
+  Ctx<NMAX, FULL> c;
   c.init(smem, n, &P);
   const long long b = blockIdx.x;
-  logm_one<NMAX>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 4 * n * n);
+  logm_one<NMAX, FULL>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 4 * n * n);
 }
 
 template <int NMAX>
@@ -152,6 +152,15 @@ static bool args_ok(const void* p, int64_t n, int64_t batch, int64_t ld) {
   return p && n >= 1 && batch >= 0 && ld >= n && batch <= (int64_t)0x7fffffff;
 }
 
+template <int NMAX, bool FULL>
+static int launch_fused(const double* A, double* L, lgm_report* rep, int64_t ld, int64_t n, int64_t batch, void* ws,
+                        const LgmParams& P, cudaStream_t s) {
+  if (prep<NMAX>(logm_fused_kernel<NMAX, FULL>)) return LGM_ERR_CUDA;
+  lgm_count_launch(), logm_fused_kernel<NMAX, FULL><<<(unsigned)batch, Cfg<NMAX>::NT, Cfg<NMAX>::SMEM_BYTES, s>>>(
+                          A, L, rep, ld, (int)n, (double*)ws, P);
+  return check_launch();
+}
+
 extern "C" {
 
 void lgm_default_opts(lgm_opts* o) {
@@ -205,17 +214,14 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   size_t need = 0;
   lgm_workspace_bytes(n, batch, &need);
   if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
-  if (n <= 32) {
-    if (prep<32>(logm_fused_kernel<32>)) return LGM_ERR_CUDA;
-    lgm_count_launch(), logm_fused_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
-                                                                                    (double*)ws, P);
-    return check_launch();
-  }
   if (n <= 64) {
-    if (prep<64>(logm_fused_kernel<64>)) return LGM_ERR_CUDA;
-    lgm_count_launch(), logm_fused_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES, s>>>(A, L, rep, ld, (int)n,
-                                                                                    (double*)ws, P);
-    return check_launch();
+    // FULL instantiations (n == NMAX) carry n as a compile-time constant
+    const bool full = (n == 32 || n == 64);
+    if (n <= 32)
+      return full ? launch_fused<32, true>(A, L, rep, ld, n, batch, ws, P, s)
+                  : launch_fused<32, false>(A, L, rep, ld, n, batch, ws, P, s);
+    return full ? launch_fused<64, true>(A, L, rep, ld, n, batch, ws, P, s)
+                : launch_fused<64, false>(A, L, rep, ld, n, batch, ws, P, s);
   }
   return lgm_grid_logm(A, L, n, batch, ld, P, rep, ws, s);
 }

@@ -56,6 +56,28 @@ __device__ __forceinline__ uint64_t lgm_warp_argmax(uint64_t key, int& lane_win)
   return kmax;
 }
 
+// 1/x from the MUFU approximation refined by two Newton steps (<= 1 ulp; the Gauss-Jordan
+// pivot reciprocal -- not bit-identical to the IEEE quotient, which the parity bar does not
+// require of the inverse).  Zero, subnormal and non-finite x take the IEEE division.
+__device__ __forceinline__ double lgm_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  const double ax = fabs(x);
+  if (!(ax >= 2.2250738585072014e-308 && ax <= 1.0e300)) y = 1.0 / x;
+  return y;
+}
+
+// Cheap reciprocal for margin bookkeeping (relative error ~1e-7 is irrelevant there).
+__device__ __forceinline__ double lgm_rcp_rough(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
 __device__ __forceinline__ double lgm_warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

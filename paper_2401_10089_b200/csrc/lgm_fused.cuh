@@ -60,10 +60,20 @@ enum { RD_LOGDET = 0 /* 2 */, RD_KEY = 4 /* [2 teams][4 slots] */, RD_CN = 12 /*
        RD_CHANGE = 16, RD_SCALE = 20 /* [2 warps] */, RD_MARGIN = 24, RD_EST = 28,
        RD_NORM = 32 /* [4] */, RD_H = 40 /* 9 sorted h values */ };
 
-template <int NMAX>
+// The matrix order as seen by the kernel code: a runtime int, or the compile-time NMAX when
+// the kernel is instantiated for n == NMAX (FULL), which folds every `row < n` / `j < n`
+// guard and trip count away.
+template <int NMAX, bool FULL>
+struct NVal {
+  int v;
+  __device__ __forceinline__ operator int() const { return FULL ? NMAX : v; }
+  __device__ __forceinline__ NVal& operator=(int x) { v = x; return *this; }
+};
+
+template <int NMAX, bool FULL = false>
 struct Ctx {
   using C = Cfg<NMAX>;
-  int n;
+  NVal<NMAX, FULL> n;
   int tid, warp, lane, team, wit, row;  // wit = warp index in team, row = wit*32 + lane
   const LgmParams* P;
   double mm;       // running min margin (uniform)
@@ -101,12 +111,12 @@ struct Ctx {
   // ---- margins (uniform) -------------------------------------------------------------
   __device__ __forceinline__ void note(double x, double thr) {
     double den = fabs(thr);
-    double m = den > 0.0 ? fabs(x - thr) / den : fabs(x - thr);
+    double m = den > 0.0 ? fabs(x - thr) * lgm_rcp_rough(den) : fabs(x - thr);
     mm = fmin(mm, m);
   }
   __device__ __forceinline__ void gap(double a, double b) {
     double den = fmax(fabs(a), fabs(b));
-    mm = fmin(mm, den > 0.0 ? fabs(a - b) / den : 0.0);
+    mm = fmin(mm, den > 0.0 ? fabs(a - b) * lgm_rcp_rough(den) : 0.0);
   }
   __device__ __forceinline__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
 
@@ -348,7 +358,7 @@ struct Ctx {
           used = true;
           my_step = k;
           mylog = r0;  // log|p| taken once after the loop (one pivot per row)
-          rowscale = 1.0 / r0;
+          rowscale = lgm_rcp(r0);
 #pragma unroll
           for (int j = 0; j < NMAX; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(r[j], r[j + 1]);
           pw[NMAX] = rowscale;
@@ -1011,8 +1021,8 @@ struct Ctx {
 // Buffer roles in the fused logm kernel
 enum { BUF_B = 0, BUF_Y = 1 };
 
-template <int NMAX>
-__device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep, double* ws) {
+template <int NMAX, bool FULL>
+__device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long long ld, lgm_report* rep, double* ws) {
   const LgmParams& P = *c.P;
   lgm_report R = {};
   R.balanced = P.balance;
@@ -1042,7 +1052,7 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   int nest = 0, passes = 0, s = 0, db_iters = 0, products = 0;
   bool have_ai2 = false;
   // A_prev / A_I2 in this matrix's workspace slot 3 (row stride n)
-  const typename Ctx<NMAX>::MRef AI2{ws + 3 * n * n, n};
+  const typename Ctx<NMAX, FULL>::MRef AI2{ws + 3 * n * n, n};
   double nI2 = 0.0;
   double alpha_loop = c.onenorm(BUF_B, 1.0);
   bool finish = c.le(alpha_loop, thK);
@@ -1118,7 +1128,7 @@ __device__ void logm_one(Ctx<NMAX>& c, const double* Ag, double* Lg, long long l
   c.minus_identity(BUF_Y, BUF_B);  // A - I: estimator operand in select, GEMM operand below
   __syncthreads();
   if (!have_ai2) {  // s = 0: A_I2 = (B - I)(B - I), one product
-    typename Ctx<NMAX>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), Cfg<NMAX>::LDM, nullptr, 0, 0};  // P2 := A - I
+    typename Ctx<NMAX, FULL>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), Cfg<NMAX>::LDM, nullptr, 0, 0};  // P2 := A - I
     const double one[2] = {0.0, 1.0};
     double acc[NMAX / 2];
     c.gemm_comb(nd, 2, one, c.buf(BUF_Y), acc);
