@@ -31,3 +31,10 @@ $(PROF): $(SRC)/lgm_api.cu $(SRC)/lgm_grid.cu $(wildcard $(SRC)/*.cuh $(SRC)/*.h
 	$(NVCC) $(NVFLAGS) -DLGM_PHASE_PROF -c $(SRC)/lgm_grid.cu -o $(OUT)/lgm_grid_prof.o
 	$(NVCC) $(ARCH) -shared -o $@ $(OUT)/lgm_api_prof.o $(OUT)/lgm_grid_prof.o
 .PHONY: prof
+
+# A/B variants: make variant V=mb10 VFLAGS=-DLGM_F32_MINB=10  (tools/time_lib.py with LGM_LIB)
+variant:
+	@mkdir -p $(OUT)/var
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/lgm_api.cu -o $(OUT)/var/lgm_api_$(V).o
+	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/var/lgm_api_$(V).o $(OUT)/lgm_grid.o
+.PHONY: variant

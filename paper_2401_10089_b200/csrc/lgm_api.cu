@@ -17,8 +17,11 @@ int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed);
 
 // ------------------------------------------------------------------------------ kernels
 
+#ifndef LGM_F32_MINB
+#define LGM_F32_MINB 8
+#endif
 template <int NMAX, bool FULL>
-__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? 8 : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
+__global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? LGM_F32_MINB : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
                                                                   lgm_report* rep, long long ld, int n, double* ws,
                                                                   const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];

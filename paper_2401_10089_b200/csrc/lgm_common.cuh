@@ -56,6 +56,8 @@ __device__ __forceinline__ uint64_t lgm_warp_argmax(uint64_t key, int& lane_win)
   return kmax;
 }
 
+static __device__ __noinline__ double lgm_div_slow(double x) { return 1.0 / x; }
+
 // 1/x from the MUFU approximation refined by two Newton steps (<= 1 ulp; the Gauss-Jordan
 // pivot reciprocal -- not bit-identical to the IEEE quotient, which the parity bar does not
 // require of the inverse).  Zero, subnormal and non-finite x take the IEEE division.
@@ -66,8 +68,10 @@ __device__ __forceinline__ double lgm_rcp(double x) {
   y = fma(y, e, y);
   e = fma(-x, y, 1.0);
   y = fma(y, e, y);
-  const double ax = fabs(x);
-  if (!(ax >= 2.2250738585072014e-308 && ax <= 1.0e300)) y = 1.0 / x;
+  // |x| < 2^-1022 (zero / subnormal, flushed by .ftz) or |x| >= 2^1021 (reciprocal near the
+  // subnormal range) or inf / nan: IEEE division
+  const unsigned hx = (unsigned)__double2hiint(x) & 0x7fffffffu;
+  if (hx - 0x00100000u >= 0x7fc00000u - 0x00100000u) y = lgm_div_slow(x);
   return y;
 }
 

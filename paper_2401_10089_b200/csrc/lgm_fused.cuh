@@ -352,20 +352,22 @@ struct Ctx {
           if (k1 > k0) { kmax = k1; prow_idx = i1; } else { kmax = k0; prow_idx = i0; }
         }
         if (kmax <= 1ull) { status = 1; break; }  // all remaining candidates exactly zero
+        // 1/|pivot| on every lane from the argmax key (exact |pivot|), the sign from the
+        // published row's column-k entry: no divergent division on the owner
+        const double rabs = lgm_rcp(lgm_unkey(kmax));
         double* pw = prow(team, k & 1);
         const bool own = (row == prow_idx);
-        if (own) {  // one lane publishes its raw row (current frame) and 1/pivot
+        if (own) {  // one lane publishes its raw row (current frame)
           used = true;
           my_step = k;
           mylog = r0;  // log|p| taken once after the loop (one pivot per row)
-          rowscale = lgm_rcp(r0);
+          rowscale = r0 < 0.0 ? -rabs : rabs;
 #pragma unroll
           for (int j = 0; j < NMAX; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(r[j], r[j + 1]);
-          pw[NMAX] = rowscale;
-          pv[k] = prow_idx;
         }
+        if (lane == 0 && wit == 0) pv[k] = prow_idx;
         team_sync();
-        g = own ? 0.0 : r0 * pr[NMAX];  // branch-free: the owner keeps its raw row
+        g = own ? 0.0 : r0 * (pr[0] < 0.0 ? -rabs : rabs);  // branch-free: the owner keeps its raw row
         last = own ? 1.0 : -g;
       }
       // shifted elimination: r[j] <- r[j+1] - g * prow[j+1]; g == 0 -> exact rotation
@@ -558,19 +560,18 @@ struct Ctx {
   // p successive thin products x <- M x (row-per-thread; M^T x: column-per-thread) for the
   // team's estimator column.  The thread's row (column) of M is held in registers across
   // the p products; x ping-pongs between xa and xb (smem, zero beyond n); on return xa
-  // holds the result.
-  // (not inlined: called from four sites; shared-memory operands passed as offsets so the
-  // accesses stay LDS/STS)
-  // (static: the context values come in as arguments, so callers working on a register copy
-  // of the context never have its address taken)
-  __device__ __noinline__ static void apply_pow_off(const double* M, int ldM, int p, bool trans, int oa, int ob, int n,
-                                                    int row, int team) {
-    double* xa = sm() + oa;
-    double* xb = sm() + ob;
+  // holds the result.  Inlined at a single call site in estimate_impl (a non-inlined callee
+  // gets a reduced register budget under the ABI and serialises the x loads).
+  __device__ __forceinline__ void apply_pow(MRef M, int p, bool trans, double*& xa, double*& xb) {
     double m[NMAX];
+    const bool ok = row < n;
+    if (trans) {
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j)
-      m[j] = (row < n && j < n) ? (trans ? M[j * ldM + row] : M[row * ldM + j]) : 0.0;
+      for (int j = 0; j < NMAX; ++j) m[j] = (ok && j < n) ? M.p[j * M.ld + row] : 0.0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NMAX; ++j) m[j] = (ok && j < n) ? M.p[row * M.ld + j] : 0.0;
+    }
     for (int q = 0; q < p; ++q) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
@@ -582,21 +583,28 @@ struct Ctx {
         a2 = fma(m[j + 2], x23.x, a2);
         a3 = fma(m[j + 3], x23.y, a3);
       }
-      if (row < n) xb[row] = (a0 + a1) + (a2 + a3);
-      if (C::T == 1) __syncwarp();
-      else asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(C::T * 32) : "memory");
+      if (ok) xb[row] = (a0 + a1) + (a2 + a3);
+      team_sync();
       double* tt = xa;
       xa = xb;
       xb = tt;
     }
   }
-  __device__ __forceinline__ void apply_pow(MRef M, int p, bool trans, double*& xa, double*& xb) {
-    apply_pow_off(M.p, M.ld, p, trans, (int)(xa - sm()), (int)(xb - sm()), n, row, team);
-    if (p & 1) {
-      double* tt = xa;
-      xa = xb;
-      xb = tt;
+
+  // op = M1^p1 [* MA]: forward applies MA (if has2) then M1^p1; the adjoint applies
+  // (M1^T)^p1 then MA^T.  One loop over the two stages so apply_pow is inlined once.
+  __device__ __noinline__ void apply_seq(MRef b1, int p1, bool has2, MRef bA, bool trans, double*& xa_, double*& xb_) {
+    Ctx s = *this;
+    double* xa = xa_;
+    double* xb = xb_;
+#pragma unroll 1
+    for (int st = 0; st < 2; ++st) {
+      const bool use_a = trans ? (st == 1) : (st == 0);
+      if (use_a && !has2) continue;
+      s.apply_pow(use_a ? bA : b1, use_a ? 1 : p1, trans, xa, xb);
     }
+    xa_ = xa;
+    xb_ = xb;
   }
 
   // buf(dst) = buf(src) - I, element-exact like numpy's B - I
@@ -661,9 +669,12 @@ struct Ctx {
       if (team < ncols) {
         double* xa = vec(2 * team);
         double* xb = vec(2 * team + 1);
-        if (has2) { apply_pow(bA, 1, false, xa, xb); cur ^= 1; }
-        apply_pow(b1, p1, false, xa, xb);
-        cur ^= (p1 & 1);
+        {
+          LGM_PHASE_BEGIN(*this);
+          apply_seq(b1, p1, has2, bA, false, xa, xb);
+          LGM_PHASE_END(*this, 5);
+        }
+        cur = (p1 + (has2 ? 1 : 0)) & 1;
         // column 1-norm (axis-0 sum); team reduction
         double v = (row < n) ? fabs(xa[row]) : 0.0;
         v = lgm_warp_sum(v);
@@ -691,8 +702,11 @@ struct Ctx {
         team_sync();
         double* xa = ya;
         double* xb = yb2;
-        apply_pow(b1, p1, true, xa, xb);
-        if (has2) apply_pow(bA, 1, true, xa, xb);
+        {
+          LGM_PHASE_BEGIN(*this);
+          apply_seq(b1, p1, has2, bA, true, xa, xb);
+          LGM_PHASE_END(*this, 5);
+        }
         if (row < n) vec(4 + team)[row] = xa[row];
       }
       passes += total;
@@ -705,6 +719,7 @@ struct Ctx {
       }
       __syncthreads();
       const int ntop = n < 4 * t + 1 ? n : 4 * t + 1;
+      LGM_PHASE_BEGIN(*this);
       if (warp == 0) {
         uint64_t taken = 0ull;
         for (int q = 0; q < ntop; ++q) {
@@ -730,6 +745,7 @@ struct Ctx {
         }
       }
       __syncthreads();
+      LGM_PHASE_END(*this, 6);
       for (int a = 0; a + 1 < ntop && a < 4 * t; ++a) gap(red()[RD_H + a], red()[RD_H + a + 1]);
       int picks[2], npick = 0;
       for (int q = 0; q < (ntop < 4 * t ? ntop : 4 * t) && npick < t; ++q) {

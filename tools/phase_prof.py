@@ -38,7 +38,8 @@ driver.run_device(A, opts)
 e1.record()
 torch.cuda.synchronize()
 lib.lgm_debug_phase_cycles(buf, 1)
-names = ["balance", "alpha(scaling loop)", "sqrt_db", "select", "poly+epilogue"]
+names = ["balance", "alpha(scaling loop)", "sqrt_db", "select", "poly+epilogue",
+         "  of which estimator applies (alpha+select)", "  of which estimator top-9 (alpha+select)"]
 tot = sum(buf[i] for i in range(5))
 out = {"config": args.config, "batch": int(A.shape[0]), "kernel_ms": e0.elapsed_time(e1),
        "cycles_per_matrix": {nm: buf[i] / A.shape[0] for i, nm in enumerate(names)},
