@@ -479,7 +479,11 @@ struct Ctx {
       if (st) { iters = it - 1; return LGM_NONFINITE; }  // as_square inside lu_factor (matcore.py:122)
       double logdet = 0.0;
       int my_step = -1, sing = 0;
-      if (active) sing = gj_invert(r, logdet, my_step);
+      {
+        LGM_PHASE_BEGIN(*this);
+        if (active) sing = gj_invert(r, logdet, my_step);
+        LGM_PHASE_END(*this, 7);
+      }
       if (tid == 0) { misc()[MI_STATUS] = 0; }
       __syncthreads();
       if (active && row == 0 && wit == 0) {
@@ -525,18 +529,28 @@ struct Ctx {
           }
           r[j] = dj;
         }
-        double change = colsum_max(r);
-#pragma unroll
-        for (int j = 0; j < NMAX; ++j) {
-          double aj = 0.0;
-          if (row < n && j < n) aj = fabs(X[q * C::LDM + ((it == 1) ? j : pv[j])]);
-          r[j] = aj;
+      }
+      __syncthreads();  // X' and Y' complete
+      // ||X' - X||_1 (team 1, butterfly over the registers) and ||X'||_1 (team 0: column per
+      // thread, rows in order -- numpy's axis-0 reduction order) in parallel
+      if (team == 1) {
+        const double change = colsum_max(r);
+        if (wit == 0 && lane == 0) red()[RD_CHANGE] = change;
+      } else {
+        double acc = 0.0;
+        if (row < n) {
+          for (int i = 0; i < n; ++i) acc += fabs(X[i * C::LDM + row]);
         }
-        double size = colsum_max(r);
-        if (wit == 0 && lane == 0) { red()[RD_CHANGE] = change; red()[RD_SCALE] = size; }
+        double m = lgm_warp_max(acc);
+        if (C::T > 1) {
+          if (lane == 0) red()[RD_SCALE + wit] = m;
+          team_sync();
+          m = fmax(red()[RD_SCALE], red()[RD_SCALE + 1]);
+        }
+        if (wit == 0 && lane == 0) red()[RD_SCALE + 2] = m;
       }
       __syncthreads();
-      const double change = red()[RD_CHANGE], size = red()[RD_SCALE];
+      const double change = red()[RD_CHANGE], size = red()[RD_SCALE + 2];
       __syncthreads();
       if (size == 0.0) return LGM_DB_NOCONV;  // sqrtm.py:69-70
       const double rel = change / size;
