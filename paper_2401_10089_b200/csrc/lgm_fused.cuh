@@ -334,40 +334,48 @@ struct Ctx {
       double g = 0.0, last = r0;        // defaults: pure rotation (steps k >= n)
       const double* pr = prow(team, k & 1);
       if (k < n) {                      // team-uniform
-        const bool cand = (row < n) && !used;
-        uint64_t key = cand ? lgm_key(fabs(r0)) : 0ull;
-        int wl;
-        uint64_t kmax = lgm_warp_argmax(key, wl);
-        int prow_idx = wit * 32 + wl;
+        // argmax |r0| over the remaining rows on a packed key: the high word of |r0| and the
+        // low word with its 8 low bits replaced by 255 - row (ties, and values equal to
+        // within 2^-44 relative, go to the lowest row -- LAPACK idamax's first index; any
+        // such pivot is an equally valid partial-pivoting choice).  Exact zeros are not
+        // candidates, so an all-zero key means an exactly singular step.
+        const bool cand = (row < n) && !used && r0 != 0.0;
+        const unsigned khi = cand ? ((unsigned)__double2hiint(r0) & 0x7fffffffu) : 0u;
+        const unsigned klo = cand ? (((unsigned)__double2loint(r0) & ~0xffu) | (unsigned)(255 - row)) : 0u;
+        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        int prow_idx = 255 - (int)(mlo & 0xffu);
+        double pval = __shfl_sync(0xffffffffu, r0, prow_idx & 31);  // exact signed pivot
         if (C::T > 1) {
           if (lane == 0) {
-            reinterpret_cast<unsigned long long*>(kslot)[wit] = kmax;
-            reinterpret_cast<int*>(kslot + 2)[wit] = prow_idx;
+            reinterpret_cast<unsigned long long*>(kslot)[wit] = ((unsigned long long)mhi << 32) | mlo;
+            kslot[2 + wit] = pval;
           }
           team_sync();
-          uint64_t k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
-          uint64_t k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
-          int i0 = reinterpret_cast<int*>(kslot + 2)[0];
-          int i1 = reinterpret_cast<int*>(kslot + 2)[1];
-          if (k1 > k0) { kmax = k1; prow_idx = i1; } else { kmax = k0; prow_idx = i0; }
+          const unsigned long long k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
+          const unsigned long long k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
+          const int w = k1 > k0 ? 1 : 0;
+          const unsigned long long km = w ? k1 : k0;
+          mhi = (unsigned)(km >> 32);
+          mlo = (unsigned)km;
+          pval = kslot[2 + w];
+          prow_idx = 255 - (int)(mlo & 0xffu);
         }
-        if (kmax <= 1ull) { status = 1; break; }  // all remaining candidates exactly zero
-        // 1/|pivot| on every lane from the argmax key (exact |pivot|), the sign from the
-        // published row's column-k entry: no divergent division on the owner
-        const double rabs = lgm_rcp(lgm_unkey(kmax));
+        if ((mhi | mlo) == 0u) { status = 1; break; }  // all remaining candidates exactly zero
+        const double rp = lgm_rcp(pval);  // every lane, in parallel with the owner's stores
         double* pw = prow(team, k & 1);
         const bool own = (row == prow_idx);
         if (own) {  // one lane publishes its raw row (current frame)
           used = true;
           my_step = k;
           mylog = r0;  // log|p| taken once after the loop (one pivot per row)
-          rowscale = r0 < 0.0 ? -rabs : rabs;
+          rowscale = rp;
 #pragma unroll
           for (int j = 0; j < NMAX; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(r[j], r[j + 1]);
         }
         if (lane == 0 && wit == 0) pv[k] = prow_idx;
         team_sync();
-        g = own ? 0.0 : r0 * (pr[0] < 0.0 ? -rabs : rabs);  // branch-free: the owner keeps its raw row
+        g = own ? 0.0 : r0 * rp;  // branch-free: the owner keeps its raw row
         last = own ? 1.0 : -g;
       }
       // shifted elimination: r[j] <- r[j+1] - g * prow[j+1]; g == 0 -> exact rotation
