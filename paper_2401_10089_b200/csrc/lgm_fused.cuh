@@ -662,7 +662,9 @@ struct Ctx {
   __device__ __noinline__ double estimate(MRef b1, int p1, bool has2, MRef bA, int itmax, int& passes) {
     Ctx s = *this;
     int ps = passes;
+    LGM_PHASE_BEGIN(*this);
     const double e = s.estimate_impl(b1, p1, has2, bA, itmax, ps);
+    LGM_PHASE_END(*this, 6);
     passes = ps;
     mm = s.mm;
     return e;
@@ -741,7 +743,6 @@ struct Ctx {
       }
       __syncthreads();
       const int ntop = n < 4 * t + 1 ? n : 4 * t + 1;
-      LGM_PHASE_BEGIN(*this);
       if (warp == 0) {
         uint64_t taken = 0ull;
         for (int q = 0; q < ntop; ++q) {
@@ -767,7 +768,6 @@ struct Ctx {
         }
       }
       __syncthreads();
-      LGM_PHASE_END(*this, 6);
       for (int a = 0; a + 1 < ntop && a < 4 * t; ++a) gap(red()[RD_H + a], red()[RD_H + a + 1]);
       int picks[2], npick = 0;
       for (int q = 0; q < (ntop < 4 * t ? ntop : 4 * t) && npick < t; ++q) {

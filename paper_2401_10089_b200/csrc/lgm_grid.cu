@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   int* rstep = reinterpret_cast<int*>(prow + G1Smem<NT>::PR);  // [NT] rowstep
   int* piv = rstep + NT;                                   // [NT]
   unsigned long long* wkey = reinterpret_cast<unsigned long long*>(piv + NT);  // [2][16]
-  int* widx = reinterpret_cast<int*>(wkey + 32);           // [2][16]
+  double* wval = reinterpret_cast<double*>(wkey + 32);     // [2][16] exact signed pivot per warp
 
   const InvJob J = jobs[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   for (int i = tid; i < NT; i += NT) rstep[i] = -1;
   if (tid < 80) prow[tid] = 0.0;  // pure-rotation steps read it with g = 0
   int my_step = -1;
-  double logsum = 0.0;  // sum of log|pivot| of this thread's pivot (at most one)
+  double mypiv = 1.0;   // this thread's pivot value (at most one); log|.| taken at the end
   int status = 0;
   __syncthreads();
   for (int k0 = 0; k0 < n && status == 0; k0 += 32) {
@@ -208,38 +208,40 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       const double r0 = r[0];
       double g = 0.0, last = r0;       // kk >= nb: pure rotation
       if (kk < nb) {
-        const bool cand = (tid < n) && (my_step < 0);
-        uint64_t key = cand ? dkey(fabs(r0)) : 0ull;
-        // warp argmax (ties -> lowest lane = lowest row)
-        unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(key >> 32));
-        unsigned lo = __reduce_max_sync(0xffffffffu, ((unsigned)(key >> 32) == hi) ? (unsigned)key : 0u);
-        const uint64_t wmax = ((uint64_t)hi << 32) | lo;
-        const int wl = __ffs(__ballot_sync(0xffffffffu, key == wmax)) - 1;
-        if (lane == 0) { wkey[par * 16 + warp] = wmax; widx[par * 16 + warp] = warp * 32 + wl; }
-        __syncthreads();
-        uint64_t kb = wkey[par * 16];
-        int p = widx[par * 16];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) {
-          const uint64_t kw = wkey[par * 16 + w];
-          if (kw > kb) { kb = kw; p = widx[par * 16 + w]; }
+        // packed-key argmax (see Engine F's gj_invert): high word of |r0|, low word with its
+        // 9 low bits replaced by 511 - row (ties -> lowest row); exact zeros excluded
+        const bool cand = (tid < n) && (my_step < 0) && r0 != 0.0;
+        const unsigned khi = cand ? ((unsigned)__double2hiint(r0) & 0x7fffffffu) : 0u;
+        const unsigned klo = cand ? (((unsigned)__double2loint(r0) & ~0x1ffu) | (unsigned)(511 - tid)) : 0u;
+        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const double wv = __shfl_sync(0xffffffffu, r0, (511 - (int)(mlo & 0x1ffu)) & 31);
+        if (lane == 0) {
+          wkey[par * 16 + warp] = ((unsigned long long)mhi << 32) | mlo;
+          wval[par * 16 + warp] = wv;
         }
-        if (kb <= 1ull) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
+        __syncthreads();
+        // block max: lane w < NW holds warp w's key, two more redux
+        const unsigned long long kw = lane < NW ? wkey[par * 16 + lane] : 0ull;
+        mhi = __reduce_max_sync(0xffffffffu, (unsigned)(kw >> 32));
+        mlo = __reduce_max_sync(0xffffffffu, (unsigned)(kw >> 32) == mhi ? (unsigned)kw : 0u);
+        if ((mhi | mlo) == 0u) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
+        const int p = 511 - (int)(mlo & 0x1ffu);
+        const double rp = lgm_rcp(wval[par * 16 + (p >> 5)]);
         double* pw = prow + par * 40;
         const bool own = (tid == p);
         if (own) {
           my_step = k0 + kk;
           piv_here = true;
-          logsum = log(fabs(r0));
-          rowscale = 1.0 / r0;
+          mypiv = r0;
+          rowscale = rp;
 #pragma unroll
           for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
-          pw[32] = rowscale;
           rstep[tid] = k0 + kk;
           piv[k0 + kk] = tid;
         }
         __syncthreads();
-        g = own ? 0.0 : r0 * pr[32];
+        g = own ? 0.0 : r0 * rp;
         last = own ? 1.0 : -g;
       }
 #pragma unroll
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   }
   // publish pivots, log|det|, status
   for (int i = tid; i < n; i += NT) { J.piv[i] = piv[i]; J.rowstep[i] = rstep[i]; }
-  double s = logsum;
+  double s = my_step >= 0 ? log(fabs(mypiv)) : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   __syncthreads();

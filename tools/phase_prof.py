@@ -39,7 +39,7 @@ e1.record()
 torch.cuda.synchronize()
 lib.lgm_debug_phase_cycles(buf, 1)
 names = ["balance", "alpha(scaling loop)", "sqrt_db", "select", "poly+epilogue",
-         "  of which estimator applies (alpha+select)", "  of which estimator top-9 (alpha+select)", "  of which GJ inversion (sqrt_db, team 0)"]
+         "  of which estimator applies (alpha+select)", "  of which estimate() total (alpha+select)", "  of which GJ inversion (sqrt_db, team 0)"]
 tot = sum(buf[i] for i in range(5))
 out = {"config": args.config, "batch": int(A.shape[0]), "kernel_ms": e0.elapsed_time(e1),
        "cycles_per_matrix": {nm: buf[i] / A.shape[0] for i, nm in enumerate(names)},
