@@ -137,7 +137,8 @@ struct InvJob {
   double* M;        // n x n row-major, inverted in place (storage permuted, see below)
   int* piv;         // piv[k] = row chosen at step k
   int* rowstep;     // rowstep[i] = step at which row i became pivot (-1 = not yet)
-  double* W;        // NB x n snapshot of this panel's pivot rows
+  double* W;        // NB x n snapshot of this panel's pivot rows (even panels)
+  double* W2;       // the same for odd panels (G2 look-ahead: two panels in flight)
   double* logdet;   // sum log|pivot|
   int* status;      // 0 ok, 1 exact zero pivot
 };
@@ -579,26 +580,32 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n
 
 // Snapshot the pivot rows of panel k0 (their values outside the panel are the B operand of
 // the trailing update and get overwritten by it).
-__global__ void gj_snapshot_kernel(const InvJob* jobs, int n, int k0, int nb) {
+__global__ void gj_snapshot_kernel(const InvJob* jobs, int n, int k0, int nb, int wpar) {
   const InvJob J = jobs[blockIdx.y];
   if (*J.status) return;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb * n; idx += gridDim.x * blockDim.x) {
     int c = idx / n, j = idx - c * n;
-    J.W[idx] = J.M[(size_t)J.piv[k0 + c] * n + j];
+    (wpar ? J.W2 : J.W)[idx] = J.M[(size_t)J.piv[k0 + c] * n + j];
   }
 }
 
 // Trailing update for every column j outside the panel:
 //   M[i][j] <- (i pivot of this panel ? 0 : M[i][j]) + sum_c M[i][k0+c] * W[c][j].
 // grid: (ceil(n/64) col tiles, ceil(n/64) row tiles, jobs); 128 threads; DMMA core.
-__global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int n, int k0, int nb) {
+// Columns written: [col_lo, col_hi) minus the panel minus [ex_lo, ex_hi); tile x covers
+// [col_base + x*TN, +TN).  W parity `wpar` selects the snapshot buffer.
+__global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int n, int k0, int nb, int col_base,
+                                                        int col_lo, int col_hi, int ex_lo, int ex_hi, int wpar) {
   __shared__ __align__(16) double As[TM * LDA_S];
   __shared__ __align__(16) double Bs[TK * LDB_S];
   const InvJob J = jobs[blockIdx.z];
   if (*J.status) return;
-  const int col0 = blockIdx.x * TN, row0 = blockIdx.y * TM;
-  // skip tiles whose columns all lie in the panel
+  const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * TM;
+  // skip tiles with no writable column
+  if (col0 >= col_hi || col0 + TN <= col_lo) return;
   if (col0 >= k0 && col0 + TN <= k0 + nb) return;
+  if (col0 >= ex_lo && col0 + TN <= ex_hi) return;
+  const double* Wp = wpar ? J.W2 : J.W;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
@@ -643,10 +650,10 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
     const int j = col0 + jj;
     double2 v = make_double2(0.0, 0.0);
     if (c < nb) {
-      if (vec && j + 1 < n) v = *reinterpret_cast<const double2*>(&J.W[(size_t)c * n + j]);
+      if (vec && j + 1 < n) v = *reinterpret_cast<const double2*>(&Wp[(size_t)c * n + j]);
       else {
-        v.x = (j < n) ? J.W[(size_t)c * n + j] : 0.0;
-        v.y = (j + 1 < n) ? J.W[(size_t)c * n + j + 1] : 0.0;
+        v.x = (j < n) ? Wp[(size_t)c * n + j] : 0.0;
+        v.y = (j + 1 < n) ? Wp[(size_t)c * n + j + 1] : 0.0;
       }
     }
     *reinterpret_cast<double2*>(&Bs[c * LDB_S + jj]) = v;
@@ -660,8 +667,9 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       const int j = c0 + ni * 8 + 2 * t;
-      const bool in0 = j < n && !(j >= k0 && j < k0 + nb);
-      const bool in1 = j + 1 < n && !(j + 1 >= k0 && j + 1 < k0 + nb);
+      const bool in0 = j >= col_lo && j < col_hi && !(j >= k0 && j < k0 + nb) && !(j >= ex_lo && j < ex_hi);
+      const bool in1 = j + 1 >= col_lo && j + 1 < col_hi && !(j + 1 >= k0 && j + 1 < k0 + nb) &&
+                       !(j + 1 >= ex_lo && j + 1 < ex_hi);
       if (vec && in0 && in1) {
         *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
       } else {
@@ -775,7 +783,7 @@ __device__ double pw_block(const double* p, size_t stride, int n) {
 }
 
 // Osborne radix-2 balancing (matcore.py:180-215), one CTA per matrix, bit-identical to numpy.
-__global__ void __launch_bounds__(256) balance_kernel_g(Slots S, const int* ids, double* scale, int* sweeps_out,
+__global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids, double* scale, int* sweeps_out,
                                                         int max_sweeps, double* margin) {
   const int b = ids[blockIdx.x];
   const int n = S.n;
@@ -783,6 +791,7 @@ __global__ void __launch_bounds__(256) balance_kernel_g(Slots S, const int* ids,
   double* sc = scale + (size_t)b * n;
   __shared__ int loff[128], llen[128];
   __shared__ double lsum[2][128];
+  __shared__ double lacc[2][128 * 8];
   __shared__ int s_nleaf, s_do;
   __shared__ double s_f, s_mm;
   if (threadIdx.x == 0) { s_nleaf = pw_leaves(n, 0, loff, llen, 0); s_mm = margin[b]; }
@@ -794,10 +803,36 @@ __global__ void __launch_bounds__(256) balance_kernel_g(Slots S, const int* ids,
     sweeps++;
     bool moved = false;
     for (int i = 0; i < n; ++i) {
+      // leaf sums in numpy's order, split over (leaf, accumulator) so all loads are in
+      // flight at once: accumulator a of a leaf sums elements a, a+8, ... (pairwise_sum's
+      // 8-way unrolled block), then one thread per leaf combines them and adds the tail
+      for (int t = threadIdx.x; t < 2 * nleaf * 8; t += blockDim.x) {
+        const int which = t / (nleaf * 8), rem = t - which * nleaf * 8, q = rem >> 3, a = rem & 7;
+        const int len = llen[q];
+        if (len < 8) continue;
+        const double* p = which == 0 ? B + (size_t)loff[q] * n + i : B + (size_t)i * n + loff[q];
+        const size_t stride = which == 0 ? (size_t)n : 1;
+        const int m8 = len - len % 8;
+        double r = fabs(p[a * stride]);
+        for (int k = 8 + a; k < m8; k += 8) r += fabs(p[k * stride]);
+        lacc[which][rem] = r;
+      }
+      __syncthreads();
       for (int l = threadIdx.x; l < 2 * nleaf; l += blockDim.x) {
-        int which = l / nleaf, q = l - which * nleaf;
-        if (which == 0) lsum[0][q] = pw_block(B + (size_t)loff[q] * n + i, n, llen[q]);   // column i
-        else lsum[1][q] = pw_block(B + (size_t)i * n + loff[q], 1, llen[q]);              // row i
+        const int which = l / nleaf, q = l - which * nleaf;
+        const int len = llen[q];
+        const double* p = which == 0 ? B + (size_t)loff[q] * n + i : B + (size_t)i * n + loff[q];
+        const size_t stride = which == 0 ? (size_t)n : 1;
+        double res;
+        if (len < 8) {
+          res = 0.0;
+          for (int k = 0; k < len; ++k) res += fabs(p[k * stride]);
+        } else {
+          const double* r = &lacc[which][q * 8];
+          res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+          for (int k = len - len % 8; k < len; ++k) res += fabs(p[k * stride]);
+        }
+        lsum[which][q] = res;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -1293,7 +1328,14 @@ struct Grid {
   int* d_ids = nullptr;       // [batch] scratch id list
   int* d_piv = nullptr;       // [2][batch][n]
   int* d_step = nullptr;      // [2][batch][n]
-  double* d_W = nullptr;      // [2][batch][NB*n]
+  double* d_W = nullptr;      // [2 parities][2][batch][NB*n]
+  cudaStream_t sB = nullptr;  // G2 look-ahead: panel stream (higher priority)
+  cudaEvent_t evN = nullptr, evP = nullptr;
+  ~Grid() {
+    if (sB) cudaStreamDestroy(sB);
+    if (evN) cudaEventDestroy(evN);
+    if (evP) cudaEventDestroy(evP);
+  }
   double* d_logdet = nullptr; // [2][batch]
   int* d_istat = nullptr;     // [2][batch]
   InvJob* d_jobs = nullptr;   // [2*batch]
@@ -1318,7 +1360,7 @@ struct Grid {
     add(batch * 4);
     add(2 * batch * n * 4);
     add(2 * batch * n * 4);
-    add(2 * batch * NB * n * 8);
+    add(4 * batch * NB * n * 8);
     add(2 * batch * 8);
     add(2 * batch * 4);
     add(2 * batch * sizeof(InvJob));
@@ -1347,7 +1389,7 @@ struct Grid {
     d_ids = (int*)take(batch * 4);
     d_piv = (int*)take(2 * (size_t)batch * n * 4);
     d_step = (int*)take(2 * (size_t)batch * n * 4);
-    d_W = (double*)take(2 * (size_t)batch * NB * n * 8);
+    d_W = (double*)take(4 * (size_t)batch * NB * n * 8);
     d_logdet = (double*)take(2 * batch * 8);
     d_istat = (int*)take(2 * batch * 4);
     d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
@@ -1396,6 +1438,7 @@ struct Grid {
       J.piv = d_piv + ((size_t)w * batch + b) * n;
       J.rowstep = d_step + ((size_t)w * batch + b) * n;
       J.W = d_W + ((size_t)w * batch + b) * NB * n;
+      J.W2 = J.W + (size_t)2 * batch * NB * n;
       J.logdet = d_logdet + w * batch + b;
       J.status = d_istat + w * batch + b;
     }
@@ -1407,16 +1450,48 @@ struct Grid {
     }
     lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
     const int tiles = (n + TM - 1) / TM;
-    for (int k0 = 0; k0 < n; k0 += NB) {
+    auto panel = [&](int k0, cudaStream_t s) {
       const int nb = std::min(NB, n - k0);
       if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
-        PhaseTimer pt(PH_OTHER, st);  // (profiling only: panel share of the G2 inversion)
-        lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, st>>>(d_jobs, n, k0, nb);
+        lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, s>>>(d_jobs, n, k0, nb);
       } else {
-        lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, st>>>(d_jobs, n, k0, nb, 0);
+        lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, s>>>(d_jobs, n, k0, nb, 0);
       }
-      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb);
-      lgm_count_launch(), gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb);
+    };
+    auto snapshot = [&](int k0, int par) {
+      const int nb = std::min(NB, n - k0);
+      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb, par);
+    };
+    // Look-ahead: panel k+1 is factored on a second (higher-priority) stream while the
+    // trailing update of panel k runs on `st`.  Per panel k: the next panel's columns are
+    // updated first (narrow launch), then its factorisation is released to sB, then the
+    // full update skips both panels; the snapshot of panel k+1's pivot rows waits for both.
+    if (!sB) {
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, hi));
+      CK(cudaEventCreateWithFlags(&evN, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
+    }
+    panel(0, st);
+    snapshot(0, 0);
+    for (int k0 = 0, par = 0; k0 < n; k0 += NB, par ^= 1) {
+      const int nb = std::min(NB, n - k0);
+      const int kn = k0 + NB, nbn = kn < n ? std::min(NB, n - kn) : 0;
+      if (kn < n) {
+        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, kn, kn, kn + nbn, 0, 0,
+                                                                                par);
+        CK(cudaEventRecord(evN, st));
+        CK(cudaStreamWaitEvent(sB, evN, 0));
+        panel(kn, sB);
+        CK(cudaEventRecord(evP, sB));
+      }
+      lgm_count_launch(), gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, 0, 0, n, kn,
+                                                                                   kn + nbn, par);
+      if (kn < n) {
+        CK(cudaStreamWaitEvent(st, evP, 0));
+        snapshot(kn, par ^ 1);
+      }
     }
     CK(cudaGetLastError());
     return 0;
@@ -1747,7 +1822,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     if (P.balance && !live.empty()) {
       if (G.upload_ids(live)) return LGM_ERR_CUDA;
       PhaseTimer pt(PH_BALANCE, st);
-      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
+      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), n >= 2048 ? 1024 : 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
       CK(cudaGetLastError());
       std::vector<int> sw(batch);
       CK(cudaMemcpyAsync(sw.data(), G.d_sweeps, batch * 4, cudaMemcpyDeviceToHost, st));
@@ -2061,7 +2136,7 @@ int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n64, int
   lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
   std::vector<double> mm0(batch, INFINITY);
   CK(cudaMemcpyAsync(G.d_margin, mm0.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  lgm_count_launch(), balance_kernel_g<<<batch, 256, 0, st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
+  lgm_count_launch(), balance_kernel_g<<<batch, n >= 2048 ? 1024 : 256, 0, st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
   lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, B, ld);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
