@@ -906,7 +906,33 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   if (a.scaling[b]) mu = fmin(fmax(exp(-(a.xlog[b] + a.ylog[b]) / (2.0 * n)), LGM_MU_MIN), LGM_MU_MAX);
   const double inv_mu = 1.0 / mu;
   double dsum = 0.0, ssum = 0.0;
-  for (int r = 0; r < n; ++r) {
+  // rows in chunks of 8 with every load of the chunk issued before the (row-ordered) sums:
+  // the permuted-storage gathers are scattered, so their latency needs overlapping when
+  // few columns (threads) are in flight (small batches at large n)
+  constexpr int U = 8;
+  int r = 0;
+  for (; r + U <= n; r += U) {
+    double xi[U], yi[U], xo[U], yo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t e = (size_t)(r + u) * n + c;
+      xi[u] = RX[(size_t)xp[r + u] * n + qxc];
+      yi[u] = a.first ? ((r + u == c) ? 1.0 : 0.0) : RY[(size_t)yp[r + u] * n + qyc];
+      xo[u] = X[e];
+      yo[u] = Y[e];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t e = (size_t)(r + u) * n + c;
+      const double xn = 0.5 * (mu * xo[u] + yi[u] * inv_mu);
+      const double yn = 0.5 * (mu * yo[u] + xi[u] * inv_mu);
+      X[e] = xn;
+      Y[e] = yn;
+      dsum = (r + u == 0) ? fabs(xn - xo[u]) : dsum + fabs(xn - xo[u]);
+      ssum = (r + u == 0) ? fabs(xn) : ssum + fabs(xn);
+    }
+  }
+  for (; r < n; ++r) {
     const size_t e = (size_t)r * n + c;
     const double xinv = RX[(size_t)xp[r] * n + qxc];
     const double yinv = a.first ? ((r == c) ? 1.0 : 0.0) : RY[(size_t)yp[r] * n + qyc];
