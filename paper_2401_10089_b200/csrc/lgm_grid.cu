@@ -589,6 +589,11 @@ __global__ void gj_snapshot_kernel(const InvJob* jobs, int n, int k0, int nb, in
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
 // Trailing update for every column j outside the panel:
 //   M[i][j] <- (i pivot of this panel ? 0 : M[i][j]) + sum_c M[i][k0+c] * W[c][j].
 // grid: (ceil(n/64) col tiles, ceil(n/64) row tiles, jobs); 128 threads; DMMA core.
@@ -631,33 +636,31 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
       }
     }
   }
+  // A (panel multipliers) and W (pivot-row snapshot) tiles: cp.async straight into shared
+  // memory (no staging registers while the C fragments are held), scalar fallback at the
+  // edges / odd n
   for (int idx = tid; idx < TM * (TK / 2); idx += 128) {
     const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
     const int i = row0 + r;
-    double2 v = make_double2(0.0, 0.0);
-    if (i < n) {
-      if (vec && c + 1 < nb) v = *reinterpret_cast<const double2*>(&J.M[(size_t)i * n + k0 + c]);
-      else {
-        v.x = (c < nb) ? J.M[(size_t)i * n + k0 + c] : 0.0;
-        v.y = (c + 1 < nb) ? J.M[(size_t)i * n + k0 + c + 1] : 0.0;
-      }
+    if (i < n && vec && c + 1 < nb) {
+      cp_async16(&As[r * LDA_S + c], &J.M[(size_t)i * n + k0 + c]);
+    } else {
+      As[r * LDA_S + c] = (i < n && c < nb) ? J.M[(size_t)i * n + k0 + c] : 0.0;
+      As[r * LDA_S + c + 1] = (i < n && c + 1 < nb) ? J.M[(size_t)i * n + k0 + c + 1] : 0.0;
     }
-    As[r * LDA_S + c] = v.x;
-    As[r * LDA_S + c + 1] = v.y;
   }
   for (int idx = tid; idx < TK * (TN / 2); idx += 128) {
     const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
     const int j = col0 + jj;
-    double2 v = make_double2(0.0, 0.0);
-    if (c < nb) {
-      if (vec && j + 1 < n) v = *reinterpret_cast<const double2*>(&Wp[(size_t)c * n + j]);
-      else {
-        v.x = (j < n) ? Wp[(size_t)c * n + j] : 0.0;
-        v.y = (j + 1 < n) ? Wp[(size_t)c * n + j + 1] : 0.0;
-      }
+    if (c < nb && vec && j + 1 < n) {
+      cp_async16(&Bs[c * LDB_S + jj], &Wp[(size_t)c * n + j]);
+    } else {
+      Bs[c * LDB_S + jj] = (c < nb && j < n) ? Wp[(size_t)c * n + j] : 0.0;
+      Bs[c * LDB_S + jj + 1] = (c < nb && j + 1 < n) ? Wp[(size_t)c * n + j + 1] : 0.0;
     }
-    *reinterpret_cast<double2*>(&Bs[c * LDB_S + jj]) = v;
   }
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   tile_mma(As, Bs, acc);
 #pragma unroll
@@ -1180,10 +1183,6 @@ struct CombSpec {
 // once both combinations are materialised (combine_kernel): measured 2.2x faster at n = 512
 // than building the left combination inside the A-tile load (gemm_comb_kernel).
 constexpr int GP_A = TM * LDA_S, GP_B = TK * LDB_S;
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
 __global__ void __launch_bounds__(128) gemm_plain_kernel(Slots S, const int* ids, int ak, int bk, int ck) {
   extern __shared__ __align__(16) double gsm[];
   const int b = ids[blockIdx.z];
