@@ -400,12 +400,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     gj_panel_cluster_kernel(const InvJob* jobs, int n, int k0, int nb) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ unsigned long long s_key[2];
-  __shared__ double s_cand[2][34];  // candidate row (32) + its pivot value
-  __shared__ double s_prow[2][34];  // winner row, local copy
-  __shared__ int s_win[2];
-  __shared__ uint64_t wkey[16];
-  __shared__ int widx[16];
+  __shared__ unsigned long long s_key[2];   // this CTA's best packed key per step parity
+  __shared__ double s_cand[2][34];          // its candidate row (32) + exact pivot value
+  __shared__ double s_prow[2][34];          // the cluster winner's row, local copy
+  __shared__ unsigned long long s_wkey[2][16];
+  __shared__ double s_red[16];
+  __shared__ double s_tot;
   const int part = (int)cl.block_rank();
   const InvJob J = jobs[blockIdx.x / CL];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -421,8 +421,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
   for (int c = 0; c < 32; ++c) r[c] = (valid && c < nb) ? J.M[(size_t)row * n + k0 + c] : 0.0;
   bool used = valid ? (J.rowstep[row] >= 0) : true;
   bool piv_here = false;
-  double rowscale = 1.0;
+  double rowscale = 1.0, mypiv = 1.0;
   int status = 0;
+  // packed pivot key: high word of |r0|; low word with its 12 low bits replaced by 4095 - row
+  // (ties and values equal to within 2^-40 go to the lowest row); exact zeros excluded
+  auto pack = [&](double v, bool cand) -> unsigned long long {
+    if (!cand || v == 0.0) return 0ull;
+    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
+    const unsigned lo = ((unsigned)__double2loint(v) & ~0xfffu) | (unsigned)(4095 - row);
+    return ((unsigned long long)hi << 32) | lo;
+  };
+  auto warp_max = [&](unsigned long long k) -> unsigned long long {
+    const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+  };
 #pragma unroll 1
   for (int kk = 0; kk < 32; ++kk) {
     const double r0 = r[0];
@@ -430,52 +443,35 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     const int par = kk & 1;
     const double* pr = s_prow[par];
     if (kk < nb) {
-      uint64_t key = (valid && !used) ? dkey(fabs(r0)) : 0ull;
-      int idx = (valid && !used) ? row : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        uint64_t k2 = __shfl_xor_sync(0xffffffffu, key, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-        if (k2 > key || (k2 == key && i2 < idx)) { key = k2; idx = i2; }
-      }
-      if (lane == 0) { wkey[warp] = key; widx[warp] = idx; }
+      // block argmax: warp redux, then every warp reduces the 16 warp keys itself
+      const unsigned long long wk = warp_max(pack(r0, valid && !used));
+      if (lane == 0) s_wkey[par][warp] = wk;
       __syncthreads();
-      if (tid == 0) {
-        uint64_t kb = wkey[0];
-        int ib = widx[0];
-        for (int w = 1; w < 16; ++w)
-          if (wkey[w] > kb || (wkey[w] == kb && widx[w] < ib)) { kb = wkey[w]; ib = widx[w]; }
-        s_key[par] = kb;
-        s_win[par] = ib;
-      }
-      __syncthreads();
-      if (row == s_win[par] && s_key[par] > 0ull) {  // publish this CTA's candidate row
+      const unsigned long long bk = warp_max(lane < 16 ? s_wkey[par][lane] : 0ull);
+      const int brow = 4095 - (int)(bk & 0xfffu);
+      if (tid == 0) s_key[par] = bk;
+      if (bk != 0ull && valid && row == brow) {  // publish this CTA's candidate row
 #pragma unroll
         for (int c = 0; c < 32; ++c) s_cand[par][c] = r[c];
       }
       cl.sync();
-      // winner over the cluster (ties -> lowest row: CTAs own increasing row ranges)
-      uint64_t kb = 0ull;
-      int qb = 0;
-      for (int q = 0; q < CL; ++q) {
-        const uint64_t kq = *cl.map_shared_rank(&s_key[par], q);
-        if (kq > kb) { kb = kq; qb = q; }
-      }
-      if (kb <= 1ull) { status = 1; break; }
-      const int p = *cl.map_shared_rank(&s_win[par], qb);
-      if (tid < 32) s_prow[par][tid] = cl.map_shared_rank(&s_cand[par][0], qb)[tid];
+      // cluster winner: lanes q < CL of every warp read CTA q's key over DSMEM
+      const unsigned long long ck = warp_max(lane < CL ? *cl.map_shared_rank(&s_key[par], lane) : 0ull);
+      if (ck == 0ull) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
+      const int p = 4095 - (int)(ck & 0xfffu);
+      if (tid < 32) s_prow[par][tid] = cl.map_shared_rank(&s_cand[par][0], p / rpc)[tid];
       __syncthreads();
+      const double rp = lgm_rcp(pr[0]);  // the winner's exact pivot (its row in its frame)
       const bool own = valid && (row == p);  // (idle threads' row ids alias other CTAs' rows)
-      const double inv = 1.0 / pr[0];
       if (own) {
         used = true;
         piv_here = true;
-        rowscale = inv;
+        rowscale = rp;
+        mypiv = r0;
         J.rowstep[row] = k0 + kk;
         J.piv[k0 + kk] = row;
-        *J.logdet += log(fabs(r0));
       }
-      g = own ? 0.0 : r0 * inv;
+      g = own ? 0.0 : r0 * rp;
       last = own ? 1.0 : -g;
     }
 #pragma unroll
@@ -491,6 +487,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     cl.sync();
     return;
   }
+  // log|det| contribution of this panel's pivots: one log per pivot row, CTA sum, one atomic
+  double lg = piv_here ? log(fabs(mypiv)) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+  if (lane == 0) s_red[warp] = lg;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 16; ++w) t += s_red[w];
+    s_tot = t;
+  }
   if (piv_here) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) r[c] *= rowscale;
@@ -500,7 +507,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     for (int c = 0; c < 32; ++c)
       if (c < nb) J.M[(size_t)row * n + k0 + c] = r[c];
   }
-  cl.sync();  // keep peers' shared memory alive until every DSMEM read is done
+  cl.sync();  // partial sums visible; peers' shared memory alive for the DSMEM reads
+  if (part == 0 && tid == 0) {  // deterministic: CTA order
+    double t = 0.0;
+    for (int q = 0; q < CL; ++q) t += *cl.map_shared_rank(&s_tot, q);
+    *J.logdet += t;
+  }
+  cl.sync();
 }
 
 __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n, int k0, int nb, int in_smem) {
