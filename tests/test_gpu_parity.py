@@ -267,3 +267,22 @@ def test_logm_multi_device_sharding_bitwise():
     L1, r1 = lp.logm_batched(A)
     L2, r2 = lp.logm_batched(A, devices=["cuda:0", "cuda:0", "cuda:0"])
     assert np.array_equal(L1, L2) and r1.tobytes() == r2.tobytes()
+
+
+def test_logm_host_pipeline_chunks_and_out_buffer():
+    """The host-buffer path (pinned input, chunked H2D/kernel/D2H on per-chunk streams,
+    caller-provided `out`) returns exactly the device-resident result and reports."""
+    A = synth.config(2)                                        # 4096 x 32^2: 3 chunks
+    Ad = torch.from_numpy(A).cuda()
+    Ldev, rdev = lp.logm_batched(Ad)
+    Ah = torch.from_numpy(A).pin_memory()
+    out = torch.empty_like(Ah).pin_memory()
+    Lh, rh = lp.logm_batched(Ah, out=out)
+    assert Lh.data_ptr() == out.data_ptr()
+    assert torch.equal(Lh, Ldev.cpu()) and rh.tobytes() == rdev.tobytes()
+    outn = np.empty_like(A)
+    Ln, rn = lp.logm_batched(A, out=outn)                      # numpy in, numpy out buffer
+    assert Ln is outn or np.shares_memory(Ln, outn)
+    assert np.array_equal(Ln, Ldev.cpu().numpy()) and rn.tobytes() == rdev.tobytes()
+    with pytest.raises(ValueError):
+        lp.logm_batched(A, out=np.empty((3, 32, 32)))
