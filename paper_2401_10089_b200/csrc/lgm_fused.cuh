@@ -924,7 +924,9 @@ struct Ctx {
           }
           if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
           v = mult * v;
-          if (unbal) v = v * (sc[row] / sc[col]);
+          // sc[] are powers of two within (1e-300, 1e300) (radix-2 balancing), so
+          // sc[row] / sc[col] == sc[row] * 2^-e(col) exactly: the reciprocal is an exponent flip
+          if (unbal) v = v * (sc[row] * __hiloint2double(0x7fe00000 - __double2hiint(sc[col]), 0));
           R[row * C::LDM + col] = v;
         }
       }
