@@ -11,7 +11,9 @@ fallback.  ``logm_batched`` takes (B, n, n) and shards by matrix across devices.
 from . import constants
 from .driver import (LogmOptions, LogmReport, OpCounter, UNIT_ROUNDOFF, logm, logm_batched,
                      unbalance_postprocess)
-from .exceptions import ConvergenceError, ExtensionMissingError, SingularMatrixError, SpectrumError
+from .exceptions import (ConvergenceError, ExtensionMissingError, SchemeFormatError, SingularMatrixError,
+                         SpectrumError)
+from .matio import format_matrix, parse_matrix, read_matrix, write_matrix
 from .primitives import (BalanceTransform, balance, balance_batched, est_power_norm, est_product_norm,
                          eval_degopt, sqrt_db, sqrt_db_batched)
 
@@ -22,4 +24,5 @@ __all__ = [
     "unbalance_postprocess", "ConvergenceError", "ExtensionMissingError", "SingularMatrixError",
     "SpectrumError", "BalanceTransform", "balance", "balance_batched", "est_power_norm",
     "est_product_norm", "eval_degopt", "sqrt_db", "sqrt_db_batched", "constants",
+    "SchemeFormatError", "format_matrix", "parse_matrix", "read_matrix", "write_matrix",
 ]

@@ -21,3 +21,7 @@ class SpectrumError(ValueError):
 
 class ExtensionMissingError(RuntimeError):
     """The CUDA shared library is not built / not loadable.  There is no CPU fallback."""
+
+
+class SchemeFormatError(ValueError):
+    """A matrix (or coefficient) text file could not be parsed (exceptions.py:22)."""

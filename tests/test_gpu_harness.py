@@ -1,0 +1,74 @@
+"""Harness / CLI on the GPU (SPEC.md:515-562 examples): logm command, bench records, Er."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2401_10089_b200 as lp  # noqa: E402
+from paper_2401_10089_b200 import cli, constants as C, harness, matio  # noqa: E402
+
+
+def test_cmd_logm_identity_known_log_and_singular(tmp_path, capsys):
+    p = tmp_path / "I.txt"
+    matio.write_matrix(str(p), np.eye(6))
+    out = tmp_path / "L.txt"
+    assert cli.main(["logm", str(p), "-o", str(out)]) == 0
+    assert np.array_equal(matio.read_matrix(str(out)), np.zeros((6, 6)))
+    err = capsys.readouterr().err
+    assert "s: 0" in err and "k: 1" in err
+    A, L = harness.gen_test_matrices("b", 11, 24)
+    matio.write_matrix(str(tmp_path / "A.txt"), A[0])
+    matio.write_matrix(str(tmp_path / "Lref.txt"), L[0])
+    assert cli.main(["logm", str(tmp_path / "A.txt"), "-o", str(out), "--ref", str(tmp_path / "Lref.txt")]) == 0
+    er = float([ln for ln in capsys.readouterr().err.splitlines() if ln.startswith("Er:")][0].split()[1])
+    assert er <= 1e-12
+    Z = np.eye(4)
+    Z[2, :] = 0.0
+    matio.write_matrix(str(tmp_path / "Z.txt"), Z)
+    assert cli.main(["logm", str(tmp_path / "Z.txt")]) == 3
+    assert "singular" in capsys.readouterr().err
+
+
+def test_cmd_bench_family_b_records(tmp_path):
+    """bench on family (b), n = 32, 20 matrices -> all Er <= 1e-10."""
+    out = tmp_path / "recs.csv"
+    assert cli.main(["bench", "--family", "b", "--n", "32", "--count", "20", "--seed", "1", "-o", str(out)]) == 0
+    recs = harness.records_from_csv(out.read_text())
+    assert len(recs) == 20 and all(r.status == 0 and r.er <= 1e-10 for r in recs)
+    assert all(r.equivalent_m == r.products + 4.0 * r.divisions / 3.0 for r in recs)
+    # performance profile over two copies of the same method set: p = 1 everywhere
+    prof = harness.performance_profile({r.matrix_id: {"gpu": r.er, "gpu2": r.er} for r in recs})
+    assert all(p == 1.0 for pts in prof.values() for _, p in pts)
+
+
+def test_family_c_bidiagonal_and_selection_invariant():
+    """family (c), superdiagonal 5, n = 8: logm succeeds, alpha <= Theta_k;
+    SPEC.md:594 (#7): when s >= 1 the evaluation uses exactly k - 1 products."""
+    A, _ = harness.gen_test_matrices("c", 0, 8, superdiag=5.0)
+    L, reps = lp.logm_batched(A)
+    r = reps[0]
+    assert r["status"] == 0 and r["alpha_used"] <= C.THETA[r["k"] - 1]
+    if r["s"] >= 1:
+        assert r["products"] == r["k"] - 1
+    E = torch.linalg.matrix_exp(torch.from_numpy(np.asarray(L)[0]).cuda()).cpu().numpy()
+    assert np.linalg.norm(E - A[0]) <= 1e-12 * np.linalg.norm(A[0])
+
+
+@pytest.mark.parametrize("n", [32, 96])
+def test_relative_error_batched_matches_host(n):
+    A, L = harness.gen_test_matrices("b", 5, n, count=4)
+    Lg, _ = lp.logm_batched(A)
+    Lg = np.asarray(Lg)
+    dev = harness.relative_error_batched(torch.from_numpy(Lg).cuda(), torch.from_numpy(L).cuda())
+    host = np.array([harness.relative_error(Lg[q], L[q]) for q in range(4)])
+    assert np.allclose(dev, host, rtol=1e-6, atol=0) and (host <= 1e-11).all()
