@@ -42,7 +42,7 @@ enum {
   LGM_DB_NOCONV = 2,       /* DB maxiter / collapse     -> ConvergenceError   (sqrtm.py:69-78)    */
   LGM_SCALING_MAXITER = 3, /* s reached opts.maxiter_s  -> ConvergenceError       */
   LGM_NONFINITE = 4,       /* NaN/Inf input or iterate  -> ValueError         (matcore.py:64-65)  */
-  LGM_SPECTRUM = 5         /* reserved (spectrum pre-check, off)                                  */
+  LGM_SPECTRUM = 5         /* set by the host-side eig_small pre-check when enabled  */
 };
 
 /* call-level errors (return values) */

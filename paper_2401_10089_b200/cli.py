@@ -23,7 +23,7 @@ import numpy as np
 
 from . import constants as C
 from . import harness, matio
-from .exceptions import ConvergenceError, SchemeFormatError, SingularMatrixError
+from .exceptions import ConvergenceError, SchemeFormatError, SingularMatrixError, SpectrumError
 
 EXIT_OK, EXIT_INPUT, EXIT_NUMERIC = 0, 2, 3
 
@@ -41,7 +41,7 @@ def cmd_logm(args):
     A = matio.read_matrix(args.input)
     if np.iscomplexobj(A):
         raise ValueError("complex input is not supported by the FP64 GPU path")
-    opts = driver.LogmOptions(max_k=args.max_k, balance=not args.no_balance)
+    opts = driver.LogmOptions(max_k=args.max_k, balance=not args.no_balance, check_spectrum=args.check_spectrum)
     L, rep = driver.logm(A, opts)
     if args.output:
         matio.write_matrix(args.output, L)
@@ -119,6 +119,7 @@ def build_parser():
     p.add_argument("--ref", help="reference logarithm file: print Er")
     p.add_argument("--no-balance", action="store_true")
     p.add_argument("--max-k", type=int, default=C.K_MAX)
+    p.add_argument("--check-spectrum", action="store_true", help="eig_small pre-check (n <= 512)")
     p.set_defaults(fn=cmd_logm)
     p = sub.add_parser("gen", help="write a synthetic matrix family")
     p.add_argument("family", choices=["a", "b", "c", "d"])
@@ -152,8 +153,10 @@ def main(argv=None):
     args = build_parser().parse_args(argv)
     try:
         return args.fn(args)
-    except (SingularMatrixError, ConvergenceError) as exc:
-        sys.stderr.write(f"error: {'singular' if isinstance(exc, SingularMatrixError) else 'no convergence'}: {exc}\n")
+    except (SingularMatrixError, ConvergenceError, SpectrumError) as exc:
+        kind = {SingularMatrixError: "singular", ConvergenceError: "no convergence",
+                SpectrumError: "spectrum"}[type(exc)]
+        sys.stderr.write(f"error: {kind}: {exc}\n")
         return EXIT_NUMERIC
     except (OSError, SchemeFormatError, ValueError) as exc:
         sys.stderr.write(f"error: input: {exc}\n")

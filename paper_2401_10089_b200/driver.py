@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from . import constants as C
-from .exceptions import ConvergenceError, SingularMatrixError
+from .exceptions import ConvergenceError, SingularMatrixError, SpectrumError
 
 UNIT_ROUNDOFF = 2.0 ** -53
 
@@ -53,6 +53,11 @@ class LogmOptions:
     db_maxiter: int = 50
     est_itmax: int = 5
     raise_on_error: bool = True
+    # eig_small pre-check: off by default (caller contract);
+    # when on, matrices with n <= spectrum_cap and an eigenvalue on the closed negative real
+    # axis get status SPECTRUM (-> SpectrumError)
+    check_spectrum: bool = False
+    spectrum_cap: int = 512
 
     def theta(self):
         return tuple(self.theta_table) if self.theta_table is not None else C.THETA
@@ -133,6 +138,8 @@ def _raise_for(rep, idx):
         raise ConvergenceError(msg + where, report)
     if st == _lib.NONFINITE:
         raise ValueError(msg + where)
+    if st == _lib.SPECTRUM:
+        raise SpectrumError(msg + where)
     raise RuntimeError(msg + where)
 
 
@@ -259,6 +266,10 @@ def logm_batched(A, opts=None, devices=None, out=None):
     for dev in {o[2] for o in outs}:
         torch.cuda.synchronize(dev)
     reports = rep_host[:B * isz].numpy().copy().view(_lib.REPORT_DTYPE)
+    if opts.check_spectrum and B and n <= opts.spectrum_cap:
+        from .validate import spectrum_violations
+        bad = spectrum_violations(Ab if not was_numpy else torch.from_numpy(Ab), opts.spectrum_cap)
+        reports["status"][bad] = _lib.SPECTRUM
     if to_host:
         if out is not None:
             Lout = out.reshape(B, n, n) if isinstance(out, np.ndarray) else Lh

@@ -72,3 +72,36 @@ def test_relative_error_batched_matches_host(n):
     dev = harness.relative_error_batched(torch.from_numpy(Lg).cuda(), torch.from_numpy(L).cuda())
     host = np.array([harness.relative_error(Lg[q], L[q]) for q in range(4)])
     assert np.allclose(dev, host, rtol=1e-6, atol=0) and (host <= 1e-11).all()
+
+
+def test_expm_ref_batched_and_round_trip():
+    """SPEC.md:592 (#5): n = 128, ||A|| = 0.5: ||expm_ref(logm(I + A)) - (I + A)|| <= 1e-13."""
+    from paper_2401_10089_b200.validate import expm_ref_batched
+    A, _ = harness.gen_test_matrices("a", 3, 128, count=3)
+    Ad = torch.from_numpy(A).cuda()
+    L, reps = lp.logm_batched(Ad)
+    E = expm_ref_batched(L)
+    res = torch.linalg.matrix_norm(E - Ad, ord=2) / torch.linalg.matrix_norm(Ad, ord=2)
+    assert (reps["status"] == 0).all() and float(res.max()) <= 1e-13
+    X = torch.from_numpy(np.random.default_rng(0).standard_normal((4, 20, 20)) * 3.0).cuda()
+    ref = torch.linalg.matrix_exp(X)
+    got = expm_ref_batched(X)
+    assert float((torch.linalg.matrix_norm(got - ref) / torch.linalg.matrix_norm(ref)).max()) <= 1e-12
+
+
+def test_spectrum_precheck(tmp_path, capsys):
+    from paper_2401_10089_b200.validate import spectrum_violations
+    rng = np.random.default_rng(2)
+    from paper_2401_10089_b200 import synth
+    S = synth.spd(rng, 10, -1, 1)
+    N = np.diag([-1.0, 2.0, 3.0])
+    Z = np.diag([0.0, 1.0, 2.0])
+    assert list(spectrum_violations(np.stack([np.eye(3), N, Z]))) == [False, True, True]
+    assert not spectrum_violations(torch.from_numpy(S).cuda())[0]
+    with pytest.raises(lp.SpectrumError):
+        lp.logm(N, lp.LogmOptions(check_spectrum=True))
+    _, reps = lp.logm_batched(np.stack([np.eye(3), N]), lp.LogmOptions(check_spectrum=True, raise_on_error=False))
+    assert list(reps["status"]) == [0, 5]
+    matio.write_matrix(str(tmp_path / "N.txt"), N)
+    assert cli.main(["logm", str(tmp_path / "N.txt"), "--check-spectrum"]) == 3
+    assert "spectrum" in capsys.readouterr().err
