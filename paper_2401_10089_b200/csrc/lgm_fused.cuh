@@ -334,33 +334,34 @@ struct Ctx {
       double g = 0.0, last = r0;        // defaults: pure rotation (steps k >= n)
       const double* pr = prow(team, k & 1);
       if (k < n) {                      // team-uniform
-        // argmax |r0| over the remaining rows on a packed key: the high word of |r0| and the
-        // low word with its 8 low bits replaced by 255 - row (ties, and values equal to
-        // within 2^-44 relative, go to the lowest row -- LAPACK idamax's first index; any
-        // such pivot is an equally valid partial-pivoting choice).  Exact zeros are not
-        // candidates, so an all-zero key means an exactly singular step.
+        // argmax |r0| over the remaining rows on a single 32-bit key: the high word of |r0|
+        // (exponent and 20 mantissa bits) with its low RB bits replaced by (2 NMAX - 1 - row),
+        // so one redux picks a row whose |value| is within 2^-13 relative of the largest
+        // (ties -> lowest row).  That is partial pivoting with a 1 - 2^-13 threshold, as
+        // stable as the exact argmax; the exact signed pivot then comes by shuffle.  Exact
+        // zeros are not candidates: an all-zero key means an exactly singular step.
+        constexpr int RB = (NMAX == 32) ? 6 : 7;
+        constexpr unsigned RMASK = (1u << RB) - 1u;
         const bool cand = (row < n) && !used && r0 != 0.0;
-        const unsigned khi = cand ? ((unsigned)__double2hiint(r0) & 0x7fffffffu) : 0u;
-        const unsigned klo = cand ? (((unsigned)__double2loint(r0) & ~0xffu) | (unsigned)(255 - row)) : 0u;
-        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
-        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
-        int prow_idx = 255 - (int)(mlo & 0xffu);
+        const unsigned key = cand ? ((((unsigned)__double2hiint(r0) & 0x7fffffffu) & ~RMASK) |
+                                     (unsigned)(2 * NMAX - 1 - row)) : 0u;
+        unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+        int prow_idx = 2 * NMAX - 1 - (int)(kmax & RMASK);
         double pval = __shfl_sync(0xffffffffu, r0, prow_idx & 31);  // exact signed pivot
         if (C::T > 1) {
           if (lane == 0) {
-            reinterpret_cast<unsigned long long*>(kslot)[wit] = ((unsigned long long)mhi << 32) | mlo;
+            reinterpret_cast<unsigned*>(kslot)[wit] = kmax;
             kslot[2 + wit] = pval;
           }
           team_sync();
-          const unsigned long long k0 = reinterpret_cast<unsigned long long*>(kslot)[0];
-          const unsigned long long k1 = reinterpret_cast<unsigned long long*>(kslot)[1];
+          const unsigned k0 = reinterpret_cast<unsigned*>(kslot)[0];
+          const unsigned k1 = reinterpret_cast<unsigned*>(kslot)[1];
           const int w = k1 > k0 ? 1 : 0;
-          const unsigned long long km = w ? k1 : k0;
-          mhi = (unsigned)(km >> 32);
-          mlo = (unsigned)km;
+          kmax = w ? k1 : k0;
           pval = kslot[2 + w];
-          prow_idx = 255 - (int)(mlo & 0xffu);
+          prow_idx = 2 * NMAX - 1 - (int)(kmax & RMASK);
         }
+        const unsigned mhi = kmax, mlo = 0u;
         if ((mhi | mlo) == 0u) { status = 1; break; }  // all remaining candidates exactly zero
         const double rp = lgm_rcp(pval);  // every lane, in parallel with the owner's stores
         double* pw = prow(team, k & 1);
