@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   int* piv = rstep + NT;                                   // [NT]
   unsigned long long* wkey = reinterpret_cast<unsigned long long*>(piv + NT);  // [2][16]
   double* wval = reinterpret_cast<double*>(wkey + 32);     // [2][16] exact signed pivot per warp
+  unsigned* wkey32 = reinterpret_cast<unsigned*>(wkey);     // [2][16] per-warp best key
 
   const InvJob J = jobs[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -209,25 +210,23 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       const double r0 = r[0];
       double g = 0.0, last = r0;       // kk >= nb: pure rotation
       if (kk < nb) {
-        // packed-key argmax (see Engine F's gj_invert): high word of |r0|, low word with its
-        // 9 low bits replaced by 511 - row (ties -> lowest row); exact zeros excluded
+        // single 32-bit key per level (see Engine F's gj_invert): high word of |r0| with its
+        // 10 low bits replaced by 1023 - row -> threshold pivoting at 1 - 2^-10 (ties -> lowest
+        // row); exact zeros excluded, so an all-zero key means a singular step
         const bool cand = (tid < n) && (my_step < 0) && r0 != 0.0;
-        const unsigned khi = cand ? ((unsigned)__double2hiint(r0) & 0x7fffffffu) : 0u;
-        const unsigned klo = cand ? (((unsigned)__double2loint(r0) & ~0x1ffu) | (unsigned)(511 - tid)) : 0u;
-        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
-        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
-        const double wv = __shfl_sync(0xffffffffu, r0, (511 - (int)(mlo & 0x1ffu)) & 31);
+        const unsigned key = cand ? ((((unsigned)__double2hiint(r0) & 0x7fffffffu) & ~0x3ffu) |
+                                     (unsigned)(1023 - tid)) : 0u;
+        const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+        const double wv = __shfl_sync(0xffffffffu, r0, (1023 - (int)(wk & 0x3ffu)) & 31);
         if (lane == 0) {
-          wkey[par * 16 + warp] = ((unsigned long long)mhi << 32) | mlo;
+          wkey32[par * 16 + warp] = wk;
           wval[par * 16 + warp] = wv;
         }
         __syncthreads();
-        // block max: lane w < NW holds warp w's key, two more redux
-        const unsigned long long kw = lane < NW ? wkey[par * 16 + lane] : 0ull;
-        mhi = __reduce_max_sync(0xffffffffu, (unsigned)(kw >> 32));
-        mlo = __reduce_max_sync(0xffffffffu, (unsigned)(kw >> 32) == mhi ? (unsigned)kw : 0u);
-        if ((mhi | mlo) == 0u) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
-        const int p = 511 - (int)(mlo & 0x1ffu);
+        // block max: lane w < NW holds warp w's key, one more redux
+        const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par * 16 + lane] : 0u);
+        if (bk == 0u) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
+        const int p = 1023 - (int)(bk & 0x3ffu);
         const double rp = lgm_rcp(wval[par * 16 + (p >> 5)]);
         double* pw = prow + par * 40;
         const bool own = (tid == p);
