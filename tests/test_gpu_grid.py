@@ -88,7 +88,7 @@ def test_est_zero_and_diag_grid():
     assert est[0] == pytest.approx(8.0, rel=1e-14)
 
 
-@pytest.mark.parametrize("n", [65, 128, 200, 520, 545, 1000])
+@pytest.mark.parametrize("n", [65, 128, 200, 520, 545, 1000, 1024])
 def test_sqrt_db_grid(n):
     rng = np.random.default_rng(n)
     G = rng.standard_normal((2, n, n))
