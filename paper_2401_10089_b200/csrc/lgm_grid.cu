@@ -139,6 +139,7 @@ struct InvJob {
   int* rowstep;     // rowstep[i] = step at which row i became pivot (-1 = not yet)
   double* W;        // NB x n snapshot of this panel's pivot rows (even panels)
   double* W2;       // the same for odd panels (G2 look-ahead: two panels in flight)
+  double* A1;       // n x NB copy of the first panel's multipliers (G2 rank-64 delayed update)
   double* logdet;   // sum log|pivot|
   int* status;      // 0 ok, 1 exact zero pivot
 };
@@ -691,6 +692,158 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
         if (in0) J.M[(size_t)i * n + j] = acc[mi][ni][0];
         if (in1) J.M[(size_t)i * n + j + 1] = acc[mi][ni][1];
       }
+    }
+  }
+}
+
+// ---- rank-64 delayed update (G2, n % 64 == 0) ---------------------------------------------
+// Two consecutive 32-column panels P1 = [k0, k0+32), P2 = [k0+32, k0+64) are applied to the
+// rest of the matrix in ONE pass (half the HBM traffic of two rank-32 passes).  With z1/z2 = 0
+// on the pivot rows of P1/P2, A1 = P1's multipliers (copied before the pass overwrites P1),
+// W1 = P1's pivot rows before any update, A2 = P2's multipliers and W2 = P2's pivot rows
+// after P1's update, the two Gauss-Jordan stages compose to
+//   j in P1:          M[i][j] <- z2 M[i][j] + sum_c A2[i][c] W2[c][j]           (M holds A1)
+//   j outside P1, P2: M[i][j] <- z1 z2 M[i][j] + sum_c z2 A1[i][c] W1[c][j] + sum_c A2[i][c] W2[c][j]
+// where W2[c][j] = M[p2_c][j] + sum_c' A1[p2_c][c'] W1[c'][j] (P2's pivot rows are not P1
+// pivots) and W2[c][j in P1] = A1[p2_c][j - k0].  P2's columns are left alone.
+
+__global__ void gj_copy_a1_kernel(const InvJob* jobs, int n, int k0) {
+  const InvJob J = jobs[blockIdx.y];
+  if (*J.status) return;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * NB; idx += gridDim.x * blockDim.x) {
+    const int i = idx / NB, c = idx - i * NB;
+    J.A1[idx] = J.M[(size_t)i * n + k0 + c];
+  }
+}
+
+// W2 (into J.W2) from the unmodified pivot rows of P2, A1 and W1 (= J.W); then W1's P1 columns
+// are zeroed for the combined pass.  One thread per column j, the 32 x 32 block A1[p2_c][:] in
+// shared memory.
+__global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, int k0) {
+  __shared__ double a1s[NB][NB + 1];
+  __shared__ int p2s[NB];
+  const InvJob J = jobs[blockIdx.y];
+  if (*J.status) return;
+  const int tid = threadIdx.x;
+  if (tid < NB) p2s[tid] = J.piv[k0 + NB + tid];
+  __syncthreads();
+  for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
+    const int c = idx / NB, cc = idx - c * NB;
+    a1s[c][cc] = J.A1[(size_t)p2s[c] * NB + cc];
+  }
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + tid;
+  if (j >= n) return;
+  if (j >= k0 && j < k0 + NB) {
+#pragma unroll 4
+    for (int c = 0; c < NB; ++c) J.W2[(size_t)c * n + j] = a1s[c][j - k0];
+#pragma unroll 4
+    for (int c = 0; c < NB; ++c) J.W[(size_t)c * n + j] = 0.0;
+    return;
+  }
+  if (j >= k0 + NB && j < k0 + 2 * NB) {
+#pragma unroll 4
+    for (int c = 0; c < NB; ++c) J.W2[(size_t)c * n + j] = 0.0;
+    return;
+  }
+  double w[NB];
+#pragma unroll
+  for (int cc = 0; cc < NB; ++cc) w[cc] = J.W[(size_t)cc * n + j];
+#pragma unroll 2
+  for (int c = 0; c < NB; ++c) {
+    double acc = J.M[(size_t)p2s[c] * n + j];
+#pragma unroll
+    for (int cc = 0; cc < NB; ++cc) acc = fma(a1s[c][cc], w[cc], acc);
+    J.W2[(size_t)c * n + j] = acc;
+  }
+}
+
+constexpr size_t UP2_SMEM = (size_t)(2 * TM * LDA_S + 2 * TK * LDB_S) * 8;
+
+// Combined pass (see above).  Tile x covers [col_base + x*TN, +TN); columns written:
+// [col_lo, col_hi) minus P2 minus [ex_lo, ex_hi).
+__global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int n, int k0, int col_base,
+                                                         int col_lo, int col_hi, int ex_lo, int ex_hi) {
+  extern __shared__ __align__(16) double u2sm[];
+  double* As1 = u2sm;
+  double* As2 = As1 + TM * LDA_S;
+  double* Bs1 = As2 + TM * LDA_S;
+  double* Bs2 = Bs1 + TK * LDB_S;
+  const InvJob J = jobs[blockIdx.z];
+  if (*J.status) return;
+  const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * TM;
+  const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
+  if (col0 >= col_hi || col0 + TN <= col_lo) return;
+  if (col0 >= p2lo && col0 + TN <= p2hi) return;
+  if (col0 >= ex_lo && col0 + TN <= ex_hi) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
+  // stage A1 / A2 / W1 / W2 (cp.async; n % 64 == 0 so every 16-byte chunk is in range)
+  for (int idx = tid; idx < TM * (TK / 2); idx += 128) {
+    const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
+    cp_async16(&As1[r * LDA_S + c], &J.A1[(size_t)(row0 + r) * NB + c]);
+    cp_async16(&As2[r * LDA_S + c], &J.M[(size_t)(row0 + r) * n + p2lo + c]);
+  }
+  for (int idx = tid; idx < TK * (TN / 2); idx += 128) {
+    const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
+    cp_async16(&Bs1[c * LDB_S + jj], &J.W[(size_t)c * n + col0 + jj]);
+    cp_async16(&Bs2[c * LDB_S + jj], &J.W2[(size_t)c * n + col0 + jj]);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  // C fragments while the tiles land; z1 / z2 masks per row
+  double acc[4][4][2];
+  bool z2r[4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+    const int rs = J.rowstep[i];
+    const bool z1 = !(rs >= p1lo && rs < p2lo), z2 = !(rs >= p2lo && rs < p2hi);
+    z2r[mi] = z2;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = c0 + ni * 8 + 2 * t;  // j, j+1 on the same side of every 32-aligned boundary
+      const bool keep = (j >= p1lo && j < p2lo) ? z2 : (z1 && z2);
+      const double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)i * n + j]);
+      acc[mi][ni][0] = keep ? v.x : 0.0;
+      acc[mi][ni][1] = keep ? v.y : 0.0;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int lr0 = (warp >> 1) * 32, lc0 = (warp & 1) * 32;
+#pragma unroll
+  for (int k = 0; k < TK; k += 4) {  // + z2 A1 W1
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = z2r[mi] ? As1[(lr0 + mi * 8 + g) * LDA_S + k + t] : 0.0;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs1[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int k = 0; k < TK; k += 4) {  // + A2 W2
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = As2[(lr0 + mi * 8 + g) * LDA_S + k + t];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs2[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = c0 + ni * 8 + 2 * t;
+      const bool in = j >= col_lo && j < col_hi && !(j >= p2lo && j < p2hi) && !(j >= ex_lo && j < ex_hi);
+      if (in) *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
   }
 }
@@ -1365,7 +1518,7 @@ struct Grid {
   int* d_ids = nullptr;       // [batch] scratch id list
   int* d_piv = nullptr;       // [2][batch][n]
   int* d_step = nullptr;      // [2][batch][n]
-  double* d_W = nullptr;      // [2 parities][2][batch][NB*n]
+  double* d_W = nullptr;      // [2 parities + A1 copy][2][batch][NB*n]
   cudaStream_t sB = nullptr;  // G2 look-ahead: panel stream (higher priority)
   cudaEvent_t evN = nullptr, evP = nullptr;
   ~Grid() {
@@ -1397,7 +1550,7 @@ struct Grid {
     add(batch * 4);
     add(2 * batch * n * 4);
     add(2 * batch * n * 4);
-    add(4 * batch * NB * n * 8);
+    add(6 * batch * NB * n * 8);
     add(2 * batch * 8);
     add(2 * batch * 4);
     add(2 * batch * sizeof(InvJob));
@@ -1426,7 +1579,7 @@ struct Grid {
     d_ids = (int*)take(batch * 4);
     d_piv = (int*)take(2 * (size_t)batch * n * 4);
     d_step = (int*)take(2 * (size_t)batch * n * 4);
-    d_W = (double*)take(4 * (size_t)batch * NB * n * 8);
+    d_W = (double*)take(6 * (size_t)batch * NB * n * 8);
     d_logdet = (double*)take(2 * batch * 8);
     d_istat = (int*)take(2 * batch * 4);
     d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
@@ -1476,6 +1629,7 @@ struct Grid {
       J.rowstep = d_step + ((size_t)w * batch + b) * n;
       J.W = d_W + ((size_t)w * batch + b) * NB * n;
       J.W2 = J.W + (size_t)2 * batch * NB * n;
+      J.A1 = J.W + (size_t)4 * batch * NB * n;
       J.logdet = d_logdet + w * batch + b;
       J.status = d_istat + w * batch + b;
     }
@@ -1512,6 +1666,40 @@ struct Grid {
     }
     panel(0, st);
     snapshot(0, 0);
+    static const bool rank64 = [] {  // LGM_G2_RANK64=0 falls back to rank-32 passes (A/B switch)
+      const char* e = std::getenv("LGM_G2_RANK64");
+      return !(e && e[0] == '0');
+    }();
+    if (rank64 && n % (2 * NB) == 0 && n > 512 && nj >= 4) {  // few jobs: the exposed P2 panel costs more
+      // rank-64 delayed update: P1 (factored, snapshot in W) -> A1 copy -> stage-1 update of
+      // P2's columns -> factor P2 -> W2 -> [next P1': combined update of its columns, factor it
+      // on sB] -> combined pass over everything else
+      CK(cudaFuncSetAttribute(gj_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UP2_SMEM));
+      for (int k0 = 0; k0 < n; k0 += 2 * NB) {
+        const int p2 = k0 + NB, kn = k0 + 2 * NB;
+        lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0);
+        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, NB, p2, p2, p2 + NB, 0, 0,
+                                                                                0);
+        panel(p2, st);
+        lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, k0);
+        if (kn < n) {
+          lgm_count_launch(), gj_update2_kernel<<<dim3(1, tiles, nj), 128, UP2_SMEM, st>>>(d_jobs, n, k0, kn, kn,
+                                                                                           kn + NB, 0, 0);
+          CK(cudaEventRecord(evN, st));
+          CK(cudaStreamWaitEvent(sB, evN, 0));
+          panel(kn, sB);
+          CK(cudaEventRecord(evP, sB));
+        }
+        lgm_count_launch(), gj_update2_kernel<<<dim3(tiles, tiles, nj), 128, UP2_SMEM, st>>>(
+                                d_jobs, n, k0, 0, 0, n, kn < n ? kn : 0, kn < n ? kn + NB : 0);
+        if (kn < n) {
+          CK(cudaStreamWaitEvent(st, evP, 0));
+          snapshot(kn, 0);
+        }
+      }
+      CK(cudaGetLastError());
+      return 0;
+    }
     for (int k0 = 0, par = 0; k0 < n; k0 += NB, par ^= 1) {
       const int nb = std::min(NB, n - k0);
       const int kn = k0 + NB, nbn = kn < n ? std::min(NB, n - kn) : 0;
