@@ -137,12 +137,13 @@ struct InvJob {
   double* M;        // n x n row-major, inverted in place (storage permuted, see below)
   int* piv;         // piv[k] = row chosen at step k
   int* rowstep;     // rowstep[i] = step at which row i became pivot (-1 = not yet)
-  double* W;        // NB x n snapshot of this panel's pivot rows (even panels)
-  double* W2;       // the same for odd panels (G2 look-ahead: two panels in flight)
-  double* A1;       // n x NB copy of the first panel's multipliers (G2 rank-64 delayed update)
+  double* Wb;       // 6 NB x n buffers ("kinds") at stride wst: pivot-row snapshots W (kinds
+  long long wst;    //  0/1: rank-32 look-ahead parities; rank-64 sets q: W1 = 3q, W2 = 3q+1)
+                    //  and the first panel's multiplier copy A1 (n x NB, kind 3q+2)
   double* logdet;   // sum log|pivot|
   int* status;      // 0 ok, 1 exact zero pivot
 };
+__device__ __forceinline__ double* wkind(const InvJob& J, int k) { return J.Wb + (long long)k * J.wst; }
 // After all panels, storage R satisfies R[piv[k]][j] = Minv[k][piv[j]], i.e.
 // Minv[a][c] = R[piv[a]][rowstep[c]].
 
@@ -593,12 +594,14 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n
 
 // Snapshot the pivot rows of panel k0 (their values outside the panel are the B operand of
 // the trailing update and get overwritten by it).
-__global__ void gj_snapshot_kernel(const InvJob* jobs, int n, int k0, int nb, int wpar) {
+__global__ void gj_snapshot_kernel(const InvJob* jobs, int n, int k0, int nb, int kind, int jlo, int jhi) {
   const InvJob J = jobs[blockIdx.y];
   if (*J.status) return;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb * n; idx += gridDim.x * blockDim.x) {
-    int c = idx / n, j = idx - c * n;
-    (wpar ? J.W2 : J.W)[idx] = J.M[(size_t)J.piv[k0 + c] * n + j];
+  double* W = wkind(J, kind);
+  const int w = jhi - jlo;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nb * w; idx += gridDim.x * blockDim.x) {
+    int c = idx / w, j = jlo + (idx - c * w);
+    W[(size_t)c * n + j] = J.M[(size_t)J.piv[k0 + c] * n + j];
   }
 }
 
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
   if (col0 >= col_hi || col0 + TN <= col_lo) return;
   if (col0 >= k0 && col0 + TN <= k0 + nb) return;
   if (col0 >= ex_lo && col0 + TN <= ex_hi) return;
-  const double* Wp = wpar ? J.W2 : J.W;
+  const double* Wp = wkind(J, wpar);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
@@ -707,54 +710,58 @@ __global__ void __launch_bounds__(128) gj_update_kernel(const InvJob* jobs, int 
 // where W2[c][j] = M[p2_c][j] + sum_c' A1[p2_c][c'] W1[c'][j] (P2's pivot rows are not P1
 // pivots) and W2[c][j in P1] = A1[p2_c][j - k0].  P2's columns are left alone.
 
-__global__ void gj_copy_a1_kernel(const InvJob* jobs, int n, int k0) {
+__global__ void gj_copy_a1_kernel(const InvJob* jobs, int n, int k0, int ka1) {
   const InvJob J = jobs[blockIdx.y];
   if (*J.status) return;
+  double* A1 = wkind(J, ka1);
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * NB; idx += gridDim.x * blockDim.x) {
     const int i = idx / NB, c = idx - i * NB;
-    J.A1[idx] = J.M[(size_t)i * n + k0 + c];
+    A1[idx] = J.M[(size_t)i * n + k0 + c];
   }
 }
 
 // W2 (into J.W2) from the unmodified pivot rows of P2, A1 and W1 (= J.W); then W1's P1 columns
 // are zeroed for the combined pass.  One thread per column j, the 32 x 32 block A1[p2_c][:] in
 // shared memory.
-__global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, int k0) {
+__global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, int k0, int q) {
   __shared__ double a1s[NB][NB + 1];
   __shared__ int p2s[NB];
   const InvJob J = jobs[blockIdx.y];
   if (*J.status) return;
+  double* W1 = wkind(J, 3 * q);
+  double* W2 = wkind(J, 3 * q + 1);
+  const double* A1 = wkind(J, 3 * q + 2);
   const int tid = threadIdx.x;
   if (tid < NB) p2s[tid] = J.piv[k0 + NB + tid];
   __syncthreads();
   for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
     const int c = idx / NB, cc = idx - c * NB;
-    a1s[c][cc] = J.A1[(size_t)p2s[c] * NB + cc];
+    a1s[c][cc] = A1[(size_t)p2s[c] * NB + cc];
   }
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + tid;
   if (j >= n) return;
   if (j >= k0 && j < k0 + NB) {
 #pragma unroll 4
-    for (int c = 0; c < NB; ++c) J.W2[(size_t)c * n + j] = a1s[c][j - k0];
+    for (int c = 0; c < NB; ++c) W2[(size_t)c * n + j] = a1s[c][j - k0];
 #pragma unroll 4
-    for (int c = 0; c < NB; ++c) J.W[(size_t)c * n + j] = 0.0;
+    for (int c = 0; c < NB; ++c) W1[(size_t)c * n + j] = 0.0;
     return;
   }
   if (j >= k0 + NB && j < k0 + 2 * NB) {
 #pragma unroll 4
-    for (int c = 0; c < NB; ++c) J.W2[(size_t)c * n + j] = 0.0;
+    for (int c = 0; c < NB; ++c) W2[(size_t)c * n + j] = 0.0;
     return;
   }
   double w[NB];
 #pragma unroll
-  for (int cc = 0; cc < NB; ++cc) w[cc] = J.W[(size_t)cc * n + j];
+  for (int cc = 0; cc < NB; ++cc) w[cc] = W1[(size_t)cc * n + j];
 #pragma unroll 2
   for (int c = 0; c < NB; ++c) {
     double acc = J.M[(size_t)p2s[c] * n + j];
 #pragma unroll
     for (int cc = 0; cc < NB; ++cc) acc = fma(a1s[c][cc], w[cc], acc);
-    J.W2[(size_t)c * n + j] = acc;
+    W2[(size_t)c * n + j] = acc;
   }
 }
 
@@ -763,7 +770,7 @@ constexpr size_t UP2_SMEM = (size_t)(2 * TM * LDA_S + 2 * TK * LDB_S) * 8;
 // Combined pass (see above).  Tile x covers [col_base + x*TN, +TN); columns written:
 // [col_lo, col_hi) minus P2 minus [ex_lo, ex_hi).
 __global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int n, int k0, int col_base,
-                                                         int col_lo, int col_hi, int ex_lo, int ex_hi) {
+                                                         int col_lo, int col_hi, int ex_lo, int ex_hi, int q) {
   extern __shared__ __align__(16) double u2sm[];
   double* As1 = u2sm;
   double* As2 = As1 + TM * LDA_S;
@@ -771,6 +778,9 @@ __global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int
   double* Bs2 = Bs1 + TK * LDB_S;
   const InvJob J = jobs[blockIdx.z];
   if (*J.status) return;
+  const double* W1 = wkind(J, 3 * q);
+  const double* W2 = wkind(J, 3 * q + 1);
+  const double* A1 = wkind(J, 3 * q + 2);
   const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * TM;
   const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
   if (col0 >= col_hi || col0 + TN <= col_lo) return;
@@ -782,13 +792,13 @@ __global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int
   // stage A1 / A2 / W1 / W2 (cp.async; n % 64 == 0 so every 16-byte chunk is in range)
   for (int idx = tid; idx < TM * (TK / 2); idx += 128) {
     const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
-    cp_async16(&As1[r * LDA_S + c], &J.A1[(size_t)(row0 + r) * NB + c]);
+    cp_async16(&As1[r * LDA_S + c], &A1[(size_t)(row0 + r) * NB + c]);
     cp_async16(&As2[r * LDA_S + c], &J.M[(size_t)(row0 + r) * n + p2lo + c]);
   }
   for (int idx = tid; idx < TK * (TN / 2); idx += 128) {
     const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
-    cp_async16(&Bs1[c * LDB_S + jj], &J.W[(size_t)c * n + col0 + jj]);
-    cp_async16(&Bs2[c * LDB_S + jj], &J.W2[(size_t)c * n + col0 + jj]);
+    cp_async16(&Bs1[c * LDB_S + jj], &W1[(size_t)c * n + col0 + jj]);
+    cp_async16(&Bs2[c * LDB_S + jj], &W2[(size_t)c * n + col0 + jj]);
   }
   asm volatile("cp.async.commit_group;\n" ::);
   // C fragments while the tiles land; z1 / z2 masks per row
@@ -1518,7 +1528,7 @@ struct Grid {
   int* d_ids = nullptr;       // [batch] scratch id list
   int* d_piv = nullptr;       // [2][batch][n]
   int* d_step = nullptr;      // [2][batch][n]
-  double* d_W = nullptr;      // [2 parities + A1 copy][2][batch][NB*n]
+  double* d_W = nullptr;      // [6 kinds][2][batch][NB*n]
   cudaStream_t sB = nullptr;  // G2 look-ahead: panel stream (higher priority)
   cudaEvent_t evN = nullptr, evP = nullptr;
   ~Grid() {
@@ -1550,7 +1560,7 @@ struct Grid {
     add(batch * 4);
     add(2 * batch * n * 4);
     add(2 * batch * n * 4);
-    add(6 * batch * NB * n * 8);
+    add(12 * batch * NB * n * 8);
     add(2 * batch * 8);
     add(2 * batch * 4);
     add(2 * batch * sizeof(InvJob));
@@ -1579,7 +1589,7 @@ struct Grid {
     d_ids = (int*)take(batch * 4);
     d_piv = (int*)take(2 * (size_t)batch * n * 4);
     d_step = (int*)take(2 * (size_t)batch * n * 4);
-    d_W = (double*)take(6 * (size_t)batch * NB * n * 8);
+    d_W = (double*)take(12 * (size_t)batch * NB * n * 8);
     d_logdet = (double*)take(2 * batch * 8);
     d_istat = (int*)take(2 * batch * 4);
     d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
@@ -1627,9 +1637,8 @@ struct Grid {
       J.M = S.buf(b, slot[q]);
       J.piv = d_piv + ((size_t)w * batch + b) * n;
       J.rowstep = d_step + ((size_t)w * batch + b) * n;
-      J.W = d_W + ((size_t)w * batch + b) * NB * n;
-      J.W2 = J.W + (size_t)2 * batch * NB * n;
-      J.A1 = J.W + (size_t)4 * batch * NB * n;
+      J.Wb = d_W + ((size_t)w * batch + b) * NB * n;
+      J.wst = (long long)2 * batch * NB * n;
       J.logdet = d_logdet + w * batch + b;
       J.status = d_istat + w * batch + b;
     }
@@ -1649,9 +1658,11 @@ struct Grid {
         lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, s>>>(d_jobs, n, k0, nb, 0);
       }
     };
-    auto snapshot = [&](int k0, int par) {
+    auto snapshot = [&](int k0, int kind, int jlo = 0, int jhi = -1, cudaStream_t s = nullptr) {
       const int nb = std::min(NB, n - k0);
-      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0, nb, par);
+      if (jhi < 0) jhi = n;
+      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * (jhi - jlo) + 255) / 256, nj), 256, 0, s ? s : st>>>(
+                              d_jobs, n, k0, nb, kind, jlo, jhi);
     };
     // Look-ahead: panel k+1 is factored on a second (higher-priority) stream while the
     // trailing update of panel k runs on `st`.  Per panel k: the next panel's columns are
@@ -1665,41 +1676,50 @@ struct Grid {
       CK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
     }
     panel(0, st);
-    snapshot(0, 0);
     static const bool rank64 = [] {  // LGM_G2_RANK64=0 falls back to rank-32 passes (A/B switch)
       const char* e = std::getenv("LGM_G2_RANK64");
       return !(e && e[0] == '0');
     }();
     if (rank64 && n % (2 * NB) == 0 && n > 512 && nj >= 4) {  // few jobs: the exposed P2 panel costs more
-      // rank-64 delayed update: P1 (factored, snapshot in W) -> A1 copy -> stage-1 update of
-      // P2's columns -> factor P2 -> W2 -> [next P1': combined update of its columns, factor it
-      // on sB] -> combined pass over everything else
+      // rank-64 delayed update with both panels of the next pair factored on sB during the
+      // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
+      // rows), A1 (copy of P1's multipliers), stage-1 update of P2's columns, factor P2, W2.
       CK(cudaFuncSetAttribute(gj_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UP2_SMEM));
-      for (int k0 = 0; k0 < n; k0 += 2 * NB) {
-        const int p2 = k0 + NB, kn = k0 + 2 * NB;
-        lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, st>>>(d_jobs, n, k0);
-        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, NB, p2, p2, p2 + NB, 0, 0,
-                                                                                0);
-        panel(p2, st);
-        lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, k0);
-        if (kn < n) {
+      auto prepare_pair = [&](int k0, int q, cudaStream_t s, bool full_snapshot) {
+        // P1 = [k0, k0+NB) already factored; everything except the full-width W1 / W2
+        if (full_snapshot) snapshot(k0, 3 * q, 0, n, s);
+        else snapshot(k0, 3 * q, k0 + NB, k0 + 2 * NB, s);  // P2's columns only (for stage 1)
+        lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, s>>>(d_jobs, n, k0, 3 * q + 2);
+        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, s>>>(d_jobs, n, k0, NB, k0 + NB, k0 + NB,
+                                                                               k0 + 2 * NB, 0, 0, 3 * q);
+        panel(k0 + NB, s);
+      };
+      prepare_pair(0, 0, st, true);
+      lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
+      for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
+        const int kn = k0 + 2 * NB;
+        const bool next = kn < n;
+        if (next) {  // finish the next pair's columns, then factor both of its panels on sB
           lgm_count_launch(), gj_update2_kernel<<<dim3(1, tiles, nj), 128, UP2_SMEM, st>>>(d_jobs, n, k0, kn, kn,
-                                                                                           kn + NB, 0, 0);
+                                                                                           kn + 2 * NB, 0, 0, q);
           CK(cudaEventRecord(evN, st));
           CK(cudaStreamWaitEvent(sB, evN, 0));
           panel(kn, sB);
+          prepare_pair(kn, q ^ 1, sB, false);
           CK(cudaEventRecord(evP, sB));
         }
         lgm_count_launch(), gj_update2_kernel<<<dim3(tiles, tiles, nj), 128, UP2_SMEM, st>>>(
-                                d_jobs, n, k0, 0, 0, n, kn < n ? kn : 0, kn < n ? kn + NB : 0);
-        if (kn < n) {
+                                d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
+        if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
           CK(cudaStreamWaitEvent(st, evP, 0));
-          snapshot(kn, 0);
+          snapshot(kn, 3 * (q ^ 1));
+          lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
         }
       }
       CK(cudaGetLastError());
       return 0;
     }
+    snapshot(0, 0);
     for (int k0 = 0, par = 0; k0 < n; k0 += NB, par ^= 1) {
       const int nb = std::min(NB, n - k0);
       const int kn = k0 + NB, nbn = kn < n ? std::min(NB, n - kn) : 0;
