@@ -616,18 +616,20 @@ struct Ctx {
 
   // op = M1^p1 [* MA]: forward applies MA (if has2) then M1^p1; the adjoint applies
   // (M1^T)^p1 then MA^T.  One loop over the two stages so apply_pow is inlined once.
-  __device__ __noinline__ void apply_seq(MRef b1, int p1, bool has2, MRef bA, bool trans, double*& xa_, double*& xb_) {
+  // (x vectors passed as shared-memory offsets so the accesses compile to LDS/STS, not
+  // generic loads through an address-taken pointer)
+  __device__ __noinline__ void apply_seq(MRef b1, int p1, bool has2, MRef bA, bool trans, int& oa, int& ob) {
     Ctx s = *this;
-    double* xa = xa_;
-    double* xb = xb_;
+    double* xa = sm() + oa;
+    double* xb = sm() + ob;
 #pragma unroll 1
     for (int st = 0; st < 2; ++st) {
       const bool use_a = trans ? (st == 1) : (st == 0);
       if (use_a && !has2) continue;
       s.apply_pow(use_a ? bA : b1, use_a ? 1 : p1, trans, xa, xb);
     }
-    xa_ = xa;
-    xb_ = xb;
+    oa = (int)(xa - sm());
+    ob = (int)(xb - sm());
   }
 
   // buf(dst) = buf(src) - I, element-exact like numpy's B - I
@@ -696,7 +698,10 @@ struct Ctx {
         double* xb = vec(2 * team + 1);
         {
           LGM_PHASE_BEGIN(*this);
-          apply_seq(b1, p1, has2, bA, false, xa, xb);
+          int oa = (int)(xa - sm()), ob = (int)(xb - sm());
+          apply_seq(b1, p1, has2, bA, false, oa, ob);
+          xa = sm() + oa;
+          xb = sm() + ob;
           LGM_PHASE_END(*this, 5);
         }
         cur = (p1 + (has2 ? 1 : 0)) & 1;
@@ -729,7 +734,10 @@ struct Ctx {
         double* xb = yb2;
         {
           LGM_PHASE_BEGIN(*this);
-          apply_seq(b1, p1, has2, bA, true, xa, xb);
+          int oa = (int)(xa - sm()), ob = (int)(xb - sm());
+          apply_seq(b1, p1, has2, bA, true, oa, ob);
+          xa = sm() + oa;
+          xb = sm() + ob;
           LGM_PHASE_END(*this, 5);
         }
         if (row < n) vec(4 + team)[row] = xa[row];
