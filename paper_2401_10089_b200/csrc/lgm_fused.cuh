@@ -919,18 +919,28 @@ struct Ctx {
       double cf[TMAX - 1];
 #pragma unroll
       for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? orow[t - 1] : 0.0;
+      // node-outer / column-inner: one node's 16 values of this row are loaded together (the
+      // per-element operation order over t is unchanged)
+      double z[NMAX / 2];
+#pragma unroll
+      for (int jj = 0; jj < NMAX / 2; ++jj) z[jj] = 0.0;
+#pragma unroll
+      for (int t = 2; t <= TMAX; ++t) {
+        if (cf[t - 2] != 0.0) {
+          const bool regs = (t == nn && last_in_regs);
+          const double* src = nd.ptr(t) + row * nd.ld(t) + col0;
+          double pv[NMAX / 2];
+#pragma unroll
+          for (int jj = 0; jj < NMAX / 2; ++jj) pv[jj] = regs ? acc[jj] : ((col0 + jj < n) ? src[jj] : 0.0);
+#pragma unroll
+          for (int jj = 0; jj < NMAX / 2; ++jj) z[jj] = __dadd_rn(z[jj], __dmul_rn(cf[t - 2], pv[jj]));
+        }
+      }
 #pragma unroll
       for (int jj = 0; jj < NMAX / 2; ++jj) {
         const int col = col0 + jj;
         if (col < n) {
-          double v = 0.0;
-#pragma unroll
-          for (int t = 2; t <= TMAX; ++t) {
-            if (cf[t - 2] != 0.0) {
-              const double pv = (t == nn && last_in_regs) ? acc[jj] : nd.ptr(t)[row * nd.ld(t) + col];
-              v = __dadd_rn(v, __dmul_rn(cf[t - 2], pv));
-            }
-          }
+          double v = z[jj];
           if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
           v = mult * v;
           // sc[] are powers of two within (1e-300, 1e300) (radix-2 balancing), so
