@@ -261,11 +261,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     }
     // factored panel -> global (K columns) and shared (A operand)
     if (tid < n) {
+      if (nb == 32 && (n & 1) == 0) {  // 16-byte stores (row segment of 256 B per thread)
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        if (c < nb) M[(size_t)tid * n + k0 + c] = r[c];
-        As[c * (NT + 4) + tid] = (c < nb) ? r[c] : 0.0;  // transposed: conflict-free row writes
+        for (int c = 0; c < 32; c += 2)
+          *reinterpret_cast<double2*>(&M[(size_t)tid * n + k0 + c]) = make_double2(r[c], r[c + 1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < nb) M[(size_t)tid * n + k0 + c] = r[c];
       }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) As[c * (NT + 4) + tid] = (c < nb) ? r[c] : 0.0;  // transposed: conflict-free
     } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) As[c * (NT + 4) + tid] = 0.0;
