@@ -1071,6 +1071,8 @@ struct DbArgs {
   int first;           // iteration 1: Y = I, Y^-1 = I
   double* change;      // [b] (max over columns, atomicMax; zeroed by host)
   double* size;
+  const int* istat;    // [2][b] singular flags of this iteration's X / Y inversions
+  int batch;
 };
 
 __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
@@ -1078,6 +1080,7 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   const int n = a.S.n;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
+  if (a.istat[b] || (!a.first && a.istat[a.batch + b])) return;  // singular iterate: X, Y kept
   double* X = a.S.buf(b, G_B);
   double* Y = a.S.buf(b, G_Y);
   const double* RX = a.S.buf(b, G_XI);
@@ -1859,18 +1862,7 @@ struct Grid {
         PhaseTimer pt(PH_INVERT, st);
         if (invert(mats2, which, slot)) return LGM_ERR_CUDA;
       }
-      std::vector<int> ist(2 * batch);
-      std::vector<double> lds(2 * batch);
-      CK(cudaMemcpyAsync(ist.data(), d_istat, 2 * batch * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      std::vector<int> next;
-      for (int b : act) {
-        iters[b] = it;
-        if (ist[b] || (it > 1 && ist[batch + b])) { status[b] = LGM_SINGULAR; iters[b] = it - 1; }
-        else next.push_back(b);
-      }
-      act = next;
-      if (act.empty()) break;
+      // (the singular flags are read back together with the norms below: one sync per iteration)
       // update + norms
       std::vector<int> hs(batch);
       for (int b = 0; b < batch; ++b) hs[b] = scaling[b];
@@ -1892,15 +1884,21 @@ struct Grid {
       a.first = it == 1;
       a.change = d_scal;
       a.size = d_scal2;
+      a.istat = d_istat;
+      a.batch = batch;
       PhaseTimer pt(PH_DBUPD, st);
       lgm_count_launch(), db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
       CK(cudaGetLastError());
       std::vector<double> ch(batch), sz(batch);
+      std::vector<int> ist(2 * batch);
       CK(cudaMemcpyAsync(ch.data(), d_scal, batch * 8, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(sz.data(), d_scal2, batch * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ist.data(), d_istat, 2 * batch * 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      next.clear();
+      std::vector<int> next;
       for (int b : act) {
+        iters[b] = it;
+        if (ist[b] || (it > 1 && ist[batch + b])) { status[b] = LGM_SINGULAR; iters[b] = it - 1; continue; }
         const double tol = tol_in > 0.0 ? tol_in : 10.0 * n * LGM_UNIT_ROUNDOFF;
         if (!std::isfinite(ch[b]) || !std::isfinite(sz[b])) { status[b] = LGM_NONFINITE; continue; }
         if (sz[b] == 0.0) { status[b] = LGM_DB_NOCONV; continue; }
