@@ -170,13 +170,13 @@ _STREAMS = {}
 
 def _host_chunks(B, n):
     """Chunking of a host-resident batch for the copy/compute pipeline: Engine F launches
-    (n <= lgm_max_fused_n) of >= 1300 matrices (about one resident wave at n = 32) so the
-    H2D of chunk i+1 and the D2H of chunk i-1 overlap chunk i's kernel (measured at config
-    2: 1 chunk 4.79 ms, 2: 4.19, 3: 3.97, 4: 4.07, 8: 4.19).  Engine G is host-orchestrated
-    per launch, so it keeps one chunk."""
+    (n <= lgm_max_fused_n) of >= ~680 matrices on their own streams (the chunk kernels
+    overlap each other on the device) so the H2D of chunk i+1 and the D2H of chunk i-1
+    overlap chunk i's kernel (config 2, 2.56 ms kernel: 1 chunk 3.91 ms, 3: 3.11, 4: 3.07,
+    6: 2.98, 8: 3.07).  Engine G is host-orchestrated per launch, so it keeps one chunk."""
     if n > int(_lib.load().lgm_max_fused_n()):
         return 1
-    return max(1, min(6, B // 1300))
+    return max(1, min(6, B // 680))
 
 
 def _streams(dev, count):
