@@ -38,3 +38,10 @@ variant:
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/lgm_api.cu -o $(OUT)/var/lgm_api_$(V).o
 	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/var/lgm_api_$(V).o $(OUT)/lgm_grid.o
 .PHONY: variant
+
+# A/B variants of the grid engine: make gvariant V=rt64 VFLAGS=-DG2_RT=64
+gvariant:
+	@mkdir -p $(OUT)/var
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/lgm_grid.cu -o $(OUT)/var/lgm_grid_$(V).o
+	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/lgm_api.o $(OUT)/var/lgm_grid_$(V).o
+.PHONY: gvariant

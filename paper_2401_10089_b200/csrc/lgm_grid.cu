@@ -51,6 +51,9 @@ struct PhaseTimer {
 };
 
 constexpr int NB = 32;      // Gauss-Jordan panel width
+#ifndef G2_RT
+#define G2_RT 64            // rows per tile of the rank-64 combined pass (64: 4 warps; 128 measured equal)
+#endif
 constexpr int NBUF = 8;     // n x n slots per matrix
 enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7 };
 
@@ -771,23 +774,25 @@ __global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, i
   }
 }
 
-constexpr size_t UP2_SMEM = (size_t)(2 * TM * LDA_S + 2 * TK * LDB_S) * 8;
+template <int RT>  // RT = output tile rows (64: 4 warps, 128: 8 warps); 64 columns
+constexpr size_t up2_smem() { return (size_t)(2 * RT * LDA_S + 2 * TK * LDB_S) * 8; }
 
 // Combined pass (see above).  Tile x covers [col_base + x*TN, +TN); columns written:
 // [col_lo, col_hi) minus P2 minus [ex_lo, ex_hi).
-__global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int n, int k0, int col_base,
+template <int RT>
+__global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, int n, int k0, int col_base,
                                                          int col_lo, int col_hi, int ex_lo, int ex_hi, int q) {
   extern __shared__ __align__(16) double u2sm[];
   double* As1 = u2sm;
-  double* As2 = As1 + TM * LDA_S;
-  double* Bs1 = As2 + TM * LDA_S;
+  double* As2 = As1 + RT * LDA_S;
+  double* Bs1 = As2 + RT * LDA_S;
   double* Bs2 = Bs1 + TK * LDB_S;
   const InvJob J = jobs[blockIdx.z];
   if (*J.status) return;
   const double* W1 = wkind(J, 3 * q);
   const double* W2 = wkind(J, 3 * q + 1);
   const double* A1 = wkind(J, 3 * q + 2);
-  const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * TM;
+  const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * RT;
   const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
   if (col0 >= col_hi || col0 + TN <= col_lo) return;
   if (col0 >= p2lo && col0 + TN <= p2hi) return;
@@ -796,12 +801,12 @@ __global__ void __launch_bounds__(128) gj_update2_kernel(const InvJob* jobs, int
   const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
   // stage A1 / A2 / W1 / W2 (cp.async; n % 64 == 0 so every 16-byte chunk is in range)
-  for (int idx = tid; idx < TM * (TK / 2); idx += 128) {
+  for (int idx = tid; idx < RT * (TK / 2); idx += 2 * RT) {
     const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
     cp_async16(&As1[r * LDA_S + c], &A1[(size_t)(row0 + r) * NB + c]);
     cp_async16(&As2[r * LDA_S + c], &J.M[(size_t)(row0 + r) * n + p2lo + c]);
   }
-  for (int idx = tid; idx < TK * (TN / 2); idx += 128) {
+  for (int idx = tid; idx < TK * (TN / 2); idx += 2 * RT) {
     const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
     cp_async16(&Bs1[c * LDB_S + jj], &W1[(size_t)c * n + col0 + jj]);
     cp_async16(&Bs2[c * LDB_S + jj], &W2[(size_t)c * n + col0 + jj]);
@@ -1693,7 +1698,9 @@ struct Grid {
       // rank-64 delayed update with both panels of the next pair factored on sB during the
       // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
       // rows), A1 (copy of P1's multipliers), stage-1 update of P2's columns, factor P2, W2.
-      CK(cudaFuncSetAttribute(gj_update2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UP2_SMEM));
+      CK(cudaFuncSetAttribute(gj_update2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up2_smem<64>()));
+      CK(cudaFuncSetAttribute(gj_update2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)up2_smem<128>()));
       auto prepare_pair = [&](int k0, int q, cudaStream_t s, bool full_snapshot) {
         // P1 = [k0, k0+NB) already factored; everything except the full-width W1 / W2
         if (full_snapshot) snapshot(k0, 3 * q, 0, n, s);
@@ -1709,7 +1716,7 @@ struct Grid {
         const int kn = k0 + 2 * NB;
         const bool next = kn < n;
         if (next) {  // finish the next pair's columns, then factor both of its panels on sB
-          lgm_count_launch(), gj_update2_kernel<<<dim3(1, tiles, nj), 128, UP2_SMEM, st>>>(d_jobs, n, k0, kn, kn,
+          lgm_count_launch(), gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0, kn, kn,
                                                                                            kn + 2 * NB, 0, 0, q);
           CK(cudaEventRecord(evN, st));
           CK(cudaStreamWaitEvent(sB, evN, 0));
@@ -1717,7 +1724,7 @@ struct Grid {
           prepare_pair(kn, q ^ 1, sB, false);
           CK(cudaEventRecord(evP, sB));
         }
-        lgm_count_launch(), gj_update2_kernel<<<dim3(tiles, tiles, nj), 128, UP2_SMEM, st>>>(
+        lgm_count_launch(), gj_update2_kernel<G2_RT><<<dim3(tiles, n / G2_RT, nj), 2 * G2_RT, up2_smem<G2_RT>(), st>>>(
                                 d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
         if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
           CK(cudaStreamWaitEvent(st, evP, 0));
