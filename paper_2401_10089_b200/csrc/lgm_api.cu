@@ -4,6 +4,7 @@
 // n  > 64: Engine G (lgm_grid.cu), host-orchestrated batched kernels over a caller-owned
 //          workspace (lgm_workspace_bytes).
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -182,10 +183,20 @@ int lgm_max_fused_n(void) { return 64; }
 
 long long lgm_launch_count(void) { return g_lgm_launches.load(std::memory_order_relaxed); }
 
+// Engine G launches index matrices (and their X / Y inversion jobs) in grid.y / grid.z, so a
+// larger batch runs as consecutive passes of at most this many matrices over one workspace.
+// LGM_GRID_CHUNK overrides it (tests exercise the pass loop with tiny chunks).
+static int64_t grid_chunk() {
+  const char* e = std::getenv("LGM_GRID_CHUNK");
+  const long long v = e ? std::atoll(e) : 0;
+  return v > 0 ? (int64_t)v : (int64_t)16384;
+}
+
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
   // n <= 64: one 4 n^2 slot per matrix: polynomial nodes P4..P6 and A_prev / A_I2 (L2 resident)
-  *bytes = n <= 64 ? (size_t)batch * 4 * n * n * sizeof(double) : lgm_grid_workspace_bytes(n, batch);
+  *bytes = n <= 64 ? (size_t)batch * 4 * n * n * sizeof(double)
+                   : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
 }
 
@@ -226,7 +237,13 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
     return full ? launch_fused<64, true>(A, L, rep, ld, n, batch, ws, P, s)
                 : launch_fused<64, false>(A, L, rep, ld, n, batch, ws, P, s);
   }
-  return lgm_grid_logm(A, L, n, batch, ld, P, rep, ws, s);
+  const int64_t ch = grid_chunk();
+  for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_logm(A + b0 * n * ld, L + b0 * n * ld, n, cnt, ld, P, rep + b0, ws, s);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 #define LGM_DISPATCH_SMALL(KERNEL, ...)                                                                  \
@@ -250,7 +267,13 @@ int lgm_sqrt_db_f64(const double* A, double* X, int64_t n, int64_t batch, int64_
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(sqrt_db_kernel, A, X, ld, (int)n, tol, maxiter, iters, status, P);
-  return lgm_grid_sqrt_db(A, X, n, batch, ld, tol, maxiter, iters, status, (cudaStream_t)stream);
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_sqrt_db(A + b0 * n * ld, X + b0 * n * ld, n, cnt, ld, tol, maxiter, iters + b0,
+                                    status + b0, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld, int32_t p, int32_t itmax,
@@ -260,7 +283,13 @@ int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(est_kernel, M, p, (const double*)nullptr, ld, (int)n, itmax, 1, est, passes, P);
-  return lgm_grid_est(M, p, nullptr, n, batch, ld, itmax, 1, est, passes, (cudaStream_t)stream);
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_est(M + b0 * n * ld, p, nullptr, n, cnt, ld, itmax, 1, est + b0, passes + b0,
+                                (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int64_t n, int64_t batch, int64_t ld,
@@ -270,7 +299,13 @@ int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(est_kernel, M1, p1, M2, ld, (int)n, itmax, 0, est, passes, P);
-  return lgm_grid_est(M1, p1, M2, n, batch, ld, itmax, 0, est, passes, (cudaStream_t)stream);
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_est(M1 + b0 * n * ld, p1, M2 ? M2 + b0 * n * ld : nullptr, n, cnt, ld, itmax, 0,
+                                est + b0, passes + b0, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_t batch, int64_t ld,
@@ -280,7 +315,13 @@ int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(balance_kernel, A, B, scale, ld, (int)n, max_sweeps, sweeps, P);
-  return lgm_grid_balance(A, B, scale, n, batch, ld, max_sweeps, sweeps, (cudaStream_t)stream);
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_balance(A + b0 * n * ld, B + b0 * n * ld, scale + b0 * n, n, cnt, ld, max_sweeps,
+                                    sweeps + b0, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
@@ -301,7 +342,13 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
                                                                                                   k, products, P);
     return check_launch();
   }
-  return lgm_grid_degopt(X, FP, Z, n, batch, ld, k, products, P, (cudaStream_t)stream);
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_degopt(X + b0 * n * ld, FP ? FP + b0 * n * ld : nullptr, Z + b0 * n * ld, n, cnt, ld, k,
+                                   products + b0, P, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 }  // extern "C"

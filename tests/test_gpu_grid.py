@@ -1,9 +1,13 @@
 """GPU parity for Engine G (n > 64): batched blocked Gauss-Jordan + DMMA GEMMs + batched
 estimator, host-orchestrated Algorithm 1.  Same tolerances as tests/test_gpu_parity.py."""
+import os
+
 import numpy as np
 import pytest
 
 from tests.parity import classify, rel_err, tolerance
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -159,3 +163,33 @@ def test_logm_grid_spd512_vs_oracle():
     A = synth.config(4, batch=2)
     L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
     _check(A, L, reps)
+
+
+def test_grid_batches_run_in_passes(tmp_path):
+    """Engine G indexes matrices in grid.y/z: batches beyond LGM_GRID_CHUNK (16384) run as
+    consecutive passes over one workspace.  A subprocess with LGM_GRID_CHUNK=3 must reproduce
+    the single-pass results bit for bit (logm, sqrt_db, balance building blocks)."""
+    import os
+    import subprocess
+    import sys
+    A = synth.config("3b", batch=7, n=80)
+    np.save(tmp_path / "A.npy", A)
+    L1, r1 = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    X1, it1, st1 = lp.sqrt_db_batched(A)
+    B1, sc1, sw1 = lp.balance_batched(A)
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {repr(ROOT)})
+import paper_2401_10089_b200 as lp
+A = np.load({repr(str(tmp_path / 'A.npy'))})
+L, r = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+X, it, st = lp.sqrt_db_batched(A)
+B, sc, sw = lp.balance_batched(A)
+np.savez({repr(str(tmp_path / 'out.npz'))}, L=L, r=r.view(np.uint8), X=X, it=it, st=st, B=B, sc=sc, sw=sw)
+"""
+    env = dict(os.environ, LGM_GRID_CHUNK="3")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    o = np.load(tmp_path / "out.npz")
+    assert np.array_equal(o["L"], L1) and o["r"].tobytes() == r1.view(np.uint8).tobytes()
+    assert np.array_equal(o["X"], X1) and np.array_equal(o["it"], it1) and np.array_equal(o["st"], st1)
+    assert np.array_equal(o["B"], B1) and np.array_equal(o["sc"], sc1) and np.array_equal(o["sw"], sw1)
