@@ -286,3 +286,30 @@ def test_logm_host_pipeline_chunks_and_out_buffer():
     assert np.array_equal(Ln, Ldev.cpu().numpy()) and rn.tobytes() == rdev.tobytes()
     with pytest.raises(ValueError):
         lp.logm_batched(A, out=np.empty((3, 32, 32)))
+
+
+@pytest.mark.parametrize("n", [32, 48, 80])
+def test_abi_row_stride_ld_greater_than_n(n):
+    """lgm_logm_f64 with padded rows (ld = n + 3): same bits as the contiguous call, the padding
+    of L untouched (include/logmpoly_b200.h: matrix b at A + b*n*ld, row stride ld)."""
+    import ctypes
+    from paper_2401_10089_b200 import _lib, driver
+    B, ld = 5, n + 3
+    A = synth.config(2 if n <= 32 else "3b", batch=B, n=n)
+    Lc, rc = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    Ap = torch.full((B, n, ld), 7.0, dtype=torch.float64, device="cuda")
+    Ap[:, :, :n] = torch.from_numpy(A).cuda()
+    Lp = torch.full((B, n, ld), -3.0, dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    rep = torch.empty(B * _lib.REPORT_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    need = ctypes.c_size_t(0)
+    assert lib.lgm_workspace_bytes(n, B, ctypes.byref(need)) == 0
+    ws = torch.empty(max(need.value, 1), dtype=torch.uint8, device="cuda")
+    o, keep = driver._c_opts(lp.LogmOptions())
+    rcode = lib.lgm_logm_f64(Ap.data_ptr(), Lp.data_ptr(), n, B, ld, ctypes.byref(o), rep.data_ptr(), ws.data_ptr(),
+                             need.value, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert rcode == 0
+    Lh = Lp.cpu().numpy()
+    assert np.array_equal(Lh[:, :, :n], Lc) and (Lh[:, :, n:] == -3.0).all()
+    assert rep.cpu().numpy().tobytes() == rc.tobytes()
