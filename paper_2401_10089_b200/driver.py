@@ -10,6 +10,7 @@ There is no CPU path: without a CUDA device or without the built library every c
 raises (ExtensionMissingError / RuntimeError).
 """
 import ctypes
+import threading
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -165,7 +166,9 @@ def run_device(A_dev, opts, stream=None):
     return L, rep, ws
 
 
-_STREAMS = {}
+# per-thread caches (streams, pinned report staging): concurrent callers on different threads
+# never share them, so logm_batched stays reentrant like the reference's pure functions
+_TLS = threading.local()
 
 
 def _host_chunks(B, n):
@@ -180,21 +183,22 @@ def _host_chunks(B, n):
 
 
 def _streams(dev, count):
+    cache = getattr(_TLS, "streams", None)
+    if cache is None:
+        cache = _TLS.streams = {}
     key = (dev.index, count)
-    if key not in _STREAMS:
-        _STREAMS[key] = [_torch().cuda.Stream(dev) for _ in range(count)]
-    return _STREAMS[key]
-
-
-_REP_STAGING = {}
+    if key not in cache:
+        cache[key] = [_torch().cuda.Stream(dev) for _ in range(count)]
+    return cache[key]
 
 
 def _rep_staging(nbytes):
-    """Pinned staging for the per-matrix reports (reused: pinned allocation costs ~1 ms)."""
-    buf = _REP_STAGING.get("buf")
+    """Pinned staging for the per-matrix reports (per thread, reused: a pinned allocation
+    costs ~1 ms)."""
+    buf = getattr(_TLS, "rep", None)
     if buf is None or buf.numel() < nbytes:
         buf = _torch().empty(max(nbytes, 1 << 16), dtype=_torch().uint8, pin_memory=True)
-        _REP_STAGING["buf"] = buf
+        _TLS.rep = buf
     return buf
 
 

@@ -313,3 +313,26 @@ def test_abi_row_stride_ld_greater_than_n(n):
     Lh = Lp.cpu().numpy()
     assert np.array_equal(Lh[:, :, :n], Lc) and (Lh[:, :, n:] == -3.0).all()
     assert rep.cpu().numpy().tobytes() == rc.tobytes()
+
+
+def test_logm_batched_concurrent_threads():
+    """Reentrancy: two host threads calling logm_batched at once get their own
+    results and reports (per-thread streams and pinned staging)."""
+    import threading
+    A1 = synth.config(2, batch=300)
+    A2 = synth.config(2, batch=300, seed=77)
+    ref1, r1 = lp.logm_batched(A1)
+    ref2, r2 = lp.logm_batched(A2)
+    out = {}
+
+    def run(key, A):
+        for _ in range(3):
+            out[key] = lp.logm_batched(A)
+
+    ts = [threading.Thread(target=run, args=("a", A1)), threading.Thread(target=run, args=("b", A2))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert np.array_equal(out["a"][0], ref1) and out["a"][1].tobytes() == r1.tobytes()
+    assert np.array_equal(out["b"][0], ref2) and out["b"][1].tobytes() == r2.tobytes()
