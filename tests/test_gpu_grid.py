@@ -193,3 +193,16 @@ np.savez({repr(str(tmp_path / 'out.npz'))}, L=L, r=r.view(np.uint8), X=X, it=it,
     assert np.array_equal(o["L"], L1) and o["r"].tobytes() == r1.view(np.uint8).tobytes()
     assert np.array_equal(o["X"], X1) and np.array_equal(o["it"], it1) and np.array_equal(o["st"], st1)
     assert np.array_equal(o["B"], B1) and np.array_equal(o["sc"], sc1) and np.array_equal(o["sw"], sw1)
+
+
+@pytest.mark.parametrize("c,B", [("3b", 64), (4, 8)])
+def test_selection_invariant_grid(c, B):
+    """SPEC.md:594 (#7) on Engine G configs: alpha_used <= Theta_k; when s >= 1 the polynomial
+    costs exactly k - 1 products (A_I2 reused), k products when s = 0."""
+    A = synth.config(c, batch=B)
+    L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    ok = reps["status"] == 0
+    assert ok.all()
+    th = np.array(C.THETA)[reps["k"] - 1]
+    assert (reps["alpha_used"] <= th).all()
+    assert (reps["products"] == np.where(reps["s"] >= 1, reps["k"] - 1, reps["k"])).all()

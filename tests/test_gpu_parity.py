@@ -336,3 +336,28 @@ def test_logm_batched_concurrent_threads():
         t.join()
     assert np.array_equal(out["a"][0], ref1) and out["a"][1].tobytes() == r1.tobytes()
     assert np.array_equal(out["b"][0], ref2) and out["b"][1].tobytes() == r2.tobytes()
+
+
+def test_spec_acceptance_6_oracle_accuracy_suite():
+    """SPEC.md:593 (#6): 50 known-log matrices (n = 16..64, cond(V) <= 100):
+    Er <= 1e3 cond(V)^2 u for every matrix; logm(A^2) vs 2 logm(A) within 1e4 u on 20 SPD
+    instances.  Batched per size through the GPU path."""
+    from paper_2401_10089_b200 import harness
+    u = 2.0 ** -53
+    rng = np.random.default_rng(2024)
+    cases = []
+    for q in range(50):
+        n = int(rng.integers(16, 65))
+        kappa = float(10.0 ** rng.uniform(0.0, 2.0))
+        A, Lex = synth.known_log(rng, n, kappa=kappa)
+        cases.append((n, kappa, A, Lex))
+    for n in sorted({c[0] for c in cases}):
+        grp = [c for c in cases if c[0] == n]
+        L, reps = lp.logm_batched(np.stack([c[2] for c in grp]))
+        for (nn, kappa, A, Lex), Lg in zip(grp, L):
+            assert harness.relative_error(Lg, Lex) <= 1e3 * kappa ** 2 * u, (nn, kappa)
+    S = np.stack([synth.spd(rng, 24, -1, 1) for _ in range(20)])
+    L1, _ = lp.logm_batched(S)
+    L2, _ = lp.logm_batched(S @ S)
+    for q in range(20):
+        assert np.linalg.norm(L2[q] - 2 * L1[q]) / np.linalg.norm(2 * L1[q]) <= 1e4 * u
