@@ -179,7 +179,10 @@ void lgm_default_opts(lgm_opts* o) {
   o->theta = nullptr;
 }
 
-int lgm_max_fused_n(void) { return 64; }
+#ifndef LGM_FUSED_MAX
+#define LGM_FUSED_MAX 64
+#endif
+int lgm_max_fused_n(void) { return LGM_FUSED_MAX; }
 
 long long lgm_launch_count(void) { return g_lgm_launches.load(std::memory_order_relaxed); }
 
@@ -195,7 +198,7 @@ static int64_t grid_chunk() {
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
   // n <= 64: one 4 n^2 slot per matrix: polynomial nodes P4..P6 and A_prev / A_I2 (L2 resident)
-  *bytes = n <= 64 ? (size_t)batch * 4 * n * n * sizeof(double)
+  *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * 4 * n * n * sizeof(double)
                    : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
 }
@@ -228,7 +231,7 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   size_t need = 0;
   lgm_workspace_bytes(n, batch, &need);
   if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
-  if (n <= 64) {
+  if (n <= LGM_FUSED_MAX) {
     // FULL instantiations (n == NMAX) carry n as a compile-time constant
     const bool full = (n == 32 || n == 64);
     if (n <= 32)
