@@ -102,23 +102,23 @@ def _alpha(st, AmI, AI2, nA, m, theta):
         nI2 = pr.onenorm(AI2)
         r2 = math.sqrt(nI2)
         if st.le(r2, theta):                      # Eq. 27
-            t1, Pm = r2, nI2 ** (m // 2)
+            t1, Pm = r2, _pow(nI2, m // 2)
         else:
             if m not in st.cache:
                 st.norm_estimations += 1
                 st.cache[m] = pr.est_power_norm(AI2, m // 2, st.counter)
             Pm = st.cache[m]
-            t1 = Pm ** (1.0 / m)
+            t1 = _pow(Pm, 1.0 / m)
     else:
         if m not in st.cache:
             st.norm_estimations += 1
             st.cache[m] = pr.est_power_norm(AmI, m, st.counter)
         Pm = st.cache[m]
-        t1 = Pm ** (1.0 / m)
+        t1 = _pow(Pm, 1.0 / m)
     st.note(t1, theta)
     if t1 > theta:
         return t1
-    bound = (Pm * nA) ** (1.0 / (m + 1))               # Eq. 28
+    bound = _pow(Pm * nA, 1.0 / (m + 1))               # Eq. 28
     if st.le(bound, theta):
         t2 = bound
     else:
@@ -128,7 +128,7 @@ def _alpha(st, AmI, AI2, nA, m, theta):
                 st.cache[m + 1] = pr.est_product_norm([(AI2, m // 2), (AmI, 1)], st.counter)
             else:
                 st.cache[m + 1] = pr.est_power_norm(AmI, m + 1, st.counter)
-        t2 = st.cache[m + 1] ** (1.0 / (m + 1))
+        t2 = _pow(st.cache[m + 1], 1.0 / (m + 1))
     return max(t1, t2)
 
 
@@ -148,9 +148,9 @@ def _select(st, AmI, AI2, nA, alpha_loop):
     mK = mk[K - 1]
     # 1. min_im (Eqs. 29-31)
     if mK in st.cache:
-        min_im = _first_index(st, st.cache[mK] ** (1.0 / mK))
+        min_im = _first_index(st, _pow(st.cache[mK], 1.0 / mK))
         if (mK + 1) in st.cache:
-            min_im = max(min_im, _first_index(st, st.cache[mK + 1] ** (1.0 / (mK + 1))))
+            min_im = max(min_im, _first_index(st, _pow(st.cache[mK + 1], 1.0 / (mK + 1))))
     else:
         min_im = _first_index(st, r2)
     # 2. tabmin_im
@@ -162,7 +162,7 @@ def _select(st, AmI, AI2, nA, alpha_loop):
     max_in, max_bound = K, None
     for j in range(1, K + 1):
         m = mk[j - 1]
-        b = (nI2 ** (m // 2) * nA) ** (1.0 / (m + 1))
+        b = _pow(_pow(nI2, m // 2) * nA, 1.0 / (m + 1))
         if st.le(b, th[j - 1]):
             max_in, max_bound = j, b
             break
@@ -178,6 +178,15 @@ def _select(st, AmI, AI2, nA, alpha_loop):
         if st.le(a, th[j]):
             return j + 1, a
     return max_in, cert_max
+
+
+def _pow(x, y):
+    """x ** y with IEEE overflow to inf (float64 semantics, like the GPU's pow) instead of
+    Python's OverflowError: reachable only when the estimator itself overflowed (norms beyond
+    ~1e300), where Algorithm 1's decisions are meaningless and the result is reported as
+    non-finite."""
+    with np.errstate(over="ignore", invalid="ignore"):
+        return float(np.power(np.float64(x), np.float64(y)))
 
 
 def _report(st, status, k=0, balanced=True, sweeps=0, msg=""):
@@ -250,9 +259,12 @@ def logm_status(A, prims, theta=THETA, order=ORDER, max_k=K_MAX, maxiter=40, do_
     k, cert = _select(st, AmI, AI2, nA, alpha_loop)
     st.alpha_used = cert
     Z = prims.eval_degopt(k, I - B, st.counter, AI2)
-    L = -(2.0 ** st.s) * Z
-    if do_balance:
-        L = P.unbalance(L, scale)
+    with np.errstate(over="ignore", invalid="ignore"):
+        L = -(2.0 ** st.s) * Z
+        if do_balance:
+            L = P.unbalance(L, scale)
+    if not np.all(np.isfinite(L)):  # overflow inside the polynomial (estimator overflow upstream)
+        return L, _report(st, NONFINITE, k=k, balanced=do_balance, sweeps=sweeps, msg="non-finite result")
     return L, _report(st, OK, k=k, balanced=do_balance, sweeps=sweeps)
 
 

@@ -209,7 +209,7 @@ const char* lgm_status_string(int code) {
     case LGM_SINGULAR: return "matrix is exactly singular (zero pivot) in a square-root step";
     case LGM_DB_NOCONV: return "square root did not converge (eigenvalues on the negative real axis?)";
     case LGM_SCALING_MAXITER: return "no convergence after maxiter square roots";
-    case LGM_NONFINITE: return "matrix has non-finite entries";
+    case LGM_NONFINITE: return "non-finite entries (input, or overflow of the result)";
     case LGM_SPECTRUM: return "spectrum check failed";
     case LGM_ERR_ARG: return "invalid argument";
     case LGM_ERR_CUDA: return "CUDA error";

@@ -1219,6 +1219,16 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
     c.degopt(k, BUF_B, AI2, true, BUF_Y, ws, n, n * n, -ldexp(1.0, s), P.balance != 0, Lg, ld, products);
     LGM_PHASE_END(c, 4);
   }
+  // a non-finite logarithm (only when the estimator overflowed upstream: norms ~1e300, where
+  // Algorithm 1's decisions are meaningless) is reported, not returned as a success; the
+  // final L is still staged in BUF_Y
+  bool bad = false;
+  {
+    const double* Lm = c.buf(BUF_Y);
+    for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+      for (int j = c.lane; j < n; j += 32) bad |= !isfinite(Lm[i * Cfg<NMAX>::LDM + j]);
+  }
+  bad = __syncthreads_or(bad);
   R.k = k;
   R.alpha_used = cert;
   R.products = products;
@@ -1226,7 +1236,7 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
   R.estimation_passes = passes;
   R.min_margin = c.mm;
   R.db_plateau = c.plateau;
-  R.status = 0;
+  R.status = bad ? LGM_NONFINITE : 0;
   if (c.tid == 0) *rep = R;
 }
 

@@ -1501,7 +1501,7 @@ __global__ void combine_kernel(Slots S, const int* ids, CombSpec C, int dk) {
 
 // L = mult_b * z * (scale_i / scale_j), z = sum_t c_t P_t + c0 I, written to the output.
 __global__ void final_kernel(Slots S, const int* ids, CombSpec C, const double* mult, const double* scale,
-                             int unbal, double* Lout, long long ld) {
+                             int unbal, double* Lout, long long ld, int* nonfinite) {
   const int b = ids[blockIdx.y];
   const int n = S.n;
   const double* sc = scale + (size_t)b * n;
@@ -1513,6 +1513,7 @@ __global__ void final_kernel(Slots S, const int* ids, CombSpec C, const double* 
     v = mult[b] * v;
     if (unbal) v = v * (sc[i] / sc[j]);
     Lout[(size_t)b * n * ld + (size_t)i * ld + j] = v;
+    if (nonfinite && !isfinite(v)) nonfinite[b] = 1;
   }
 }
 
@@ -1933,7 +1934,7 @@ namespace {
 
 struct MState {
   int status = 0, s = 0, db_iters = 0, nest = 0, passes = 0, products = 0, k = 0, plateau = 0, sweeps = 0;
-  bool finish = false, have_ai2 = false;
+  bool finish = false, have_ai2 = false, post_fail = false;  // post_fail: non-finite L after the polynomial
   double alpha_loop = 0.0, mm = INFINITY, nA = 0.0, cert = 0.0;
   double cache[20];
   unsigned cvalid = 0u;
@@ -2264,9 +2265,17 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     for (int b : grp) mult[b] = -std::ldexp(1.0, ms[b].s);
     CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
     if (G.upload_ids(grp)) return LGM_ERR_CUDA;
-    lgm_count_launch(), final_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, P.balance, L, ld);
+    CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
+    lgm_count_launch(), final_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale,
+                                                                                P.balance, L, ld, G.d_iflag);
     CK(cudaGetLastError());
+    std::vector<int> nf(batch);
+    CK(cudaMemcpyAsync(nf.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    // a non-finite logarithm (estimator overflow upstream, norms ~1e300) is reported, with
+    // the k / products / alpha of the run that produced it
+    for (int b : grp)
+      if (nf[b]) { ms[b].status = LGM_NONFINITE; ms[b].post_fail = true; }
   }
   // reports
   std::vector<lgm_report> R(batch);
@@ -2276,16 +2285,17 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     std::memset(&r, 0, sizeof(r));
     r.status = M.status;
     r.s = M.s;
-    r.k = M.status ? 0 : M.k;
+    const bool keep = !M.status || M.post_fail;
+    r.k = keep ? M.k : 0;
     r.db_iters = M.db_iters;
-    r.products = M.status ? 0 : M.products;
+    r.products = keep ? M.products : 0;
     r.divisions = 2 * M.db_iters;
     r.estimation_passes = M.passes;
     r.norm_estimations = M.nest;
     r.balanced = P.balance;
     r.balance_sweeps = M.sweeps;
     r.db_plateau = M.plateau;
-    r.alpha_used = M.status ? 0.0 : M.cert;
+    r.alpha_used = keep ? M.cert : 0.0;
     r.min_margin = M.mm;
   }
   CK(cudaMemcpyAsync(rep, R.data(), batch * sizeof(lgm_report), cudaMemcpyHostToDevice, st));
@@ -2449,7 +2459,8 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
   CombSpec os = spec(base + k * (k + 3), nn);
   std::vector<double> mult(batch, 1.0);
   CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  lgm_count_launch(), final_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, 0, Z, ld);
+  lgm_count_launch(), final_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, 0, Z, ld,
+                                                                      nullptr);
   CK(cudaGetLastError());
   std::vector<int> pr(batch, prods);
   CK(cudaMemcpyAsync(products, pr.data(), batch * 4, cudaMemcpyHostToDevice, st));

@@ -361,3 +361,19 @@ def test_spec_acceptance_6_oracle_accuracy_suite():
     L2, _ = lp.logm_batched(S @ S)
     for q in range(20):
         assert np.linalg.norm(L2[q] - 2 * L1[q]) / np.linalg.norm(2 * L1[q]) <= 1e4 * u
+
+
+@pytest.mark.parametrize("n,scale", [(19, 1e26), (40, 1e40), (80, 1e30)])
+def test_logm_estimator_overflow_reported_nonfinite(n, scale):
+    """Norms ~1e300 overflow the norm estimator (in the reference arithmetic too), which then
+    certifies s = 0; the resulting logarithm is non-finite.  Both the oracle and the GPU report
+    NONFINITE with the same decisions instead of a 'successful' inf result."""
+    rng = np.random.default_rng(n)
+    A = synth.near_identity(rng, n) * scale
+    L, reps = lp.logm_batched(A[None], lp.LogmOptions(raise_on_error=False))
+    Lo, ro = D.logm_status(A, D.default_prims())
+    assert int(reps[0]["status"]) == ro["status"] == 4
+    cls, g, o = classify(reps[0], ro)
+    assert cls in ("match", "exempt"), (g, o)
+    with pytest.raises(ValueError):
+        lp.logm(A)

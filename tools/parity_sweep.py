@@ -32,6 +32,26 @@ def _oracle(A):
 
 def make(rng, fam, n):
     from paper_2401_10089_b200 import synth
+    if fam == "scaled":        # huge / tiny magnitudes (balancing, many square roots)
+        return synth.near_identity(rng, n) * 10.0 ** rng.uniform(-60, 60)
+    if fam == "illcond":       # SPD with kappa up to 1e12
+        return synth.spd(rng, n, -6.0, 6.0)
+    if fam == "bignorm":       # needs many square roots
+        return synth.spd(rng, n, 2.0, 8.0)
+    if fam == "jordanish":     # identity + strong nilpotent part
+        return np.eye(n) + np.triu(rng.standard_normal((n, n)) * 3.0, 1)
+    if fam == "negdiag":       # an eigenvalue on the negative real axis: DB non-convergence
+        d = 10.0 ** rng.uniform(-1, 1, n)
+        d[int(rng.integers(0, n))] *= -1.0
+        return np.diag(d)
+    if fam == "rotation":      # eigenvalues on the unit circle (principal log exists if no -1)
+        th = rng.uniform(-3.0, 3.0, n // 2)
+        R = np.eye(n)
+        for q, t in enumerate(th):
+            c, s_ = np.cos(t), np.sin(t)
+            R[2 * q:2 * q + 2, 2 * q:2 * q + 2] = [[c, -s_], [s_, c]]
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        return Q @ R @ Q.T
     if fam == "near":
         return synth.near_identity(rng, n)
     if fam == "spd":
@@ -48,11 +68,14 @@ def main():
     ap.add_argument("--nmax", type=int, default=160)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))
+    ap.add_argument("--extreme", action="store_true", help="scaled / ill-conditioned / big-norm / "
+                    "Jordan-like / negative-eigenvalue / rotation families")
     args = ap.parse_args()
     import paper_2401_10089_b200 as lp
     from tests.parity import classify, rel_err, tolerance
     rng = np.random.default_rng(args.seed)
-    fams = ["near", "spd", "nonnormal", "knownlog"]
+    fams = (["scaled", "illcond", "bignorm", "jordanish", "negdiag", "rotation"] if args.extreme
+            else ["near", "spd", "nonnormal", "knownlog"])
     cases = []
     for q in range(args.count):
         n = int(rng.integers(1, args.nmax + 1))
@@ -76,7 +99,8 @@ def main():
         if cls == "mismatch":
             bad.append({"id": c[0], "fam": c[1], "n": c[2], "gpu": g, "oracle": o})
             continue
-        if g["status"] == 0 and o["status"] == 0 and (g["s"], g["k"]) == (o["s"], o["k"]):
+        if g["status"] == 0 and o["status"] == 0 and (g["s"], g["k"]) == (o["s"], o["k"]) and \
+                np.isfinite(Lo).all():
             e, tol = rel_err(Lg, Lo), tolerance(c[3], Lo)
             worst.append((e / tol, c[0], c[1], c[2], e, tol))
             if e > tol:
