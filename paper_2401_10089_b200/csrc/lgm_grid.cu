@@ -138,6 +138,8 @@ __device__ __forceinline__ void tile_mma(const double* As, const double* Bs, dou
 // Batched pivoted Gauss-Jordan inversion.
 struct InvJob {
   double* M;        // n x n row-major, inverted in place (storage permuted, see below)
+  const double* Src;  // G1 only: if set, the first panel reads the matrix from here (M is
+                      // written by then): out-of-place inversion without a copy pass
   int* piv;         // piv[k] = row chosen at step k
   int* rowstep;     // rowstep[i] = step at which row i became pivot (-1 = not yet)
   double* Wb;       // 6 NB x n buffers ("kinds") at stride wst: pivot-row snapshots W (kinds
@@ -196,14 +198,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     double r[32];
     // (per-thread row loads: measured faster than staging through shared memory)
 #pragma unroll
+    // (the first panel reads the source matrix when inverting out of place: every element of
+    // M is written during panel 0 -- K columns by the panel store, the rest by its update)
+    const double* Mr = (k0 == 0 && J.Src) ? J.Src : M;
     for (int c = 0; c < 32; c += 2) {
       if (tid < n && c + 1 < nb && (n & 1) == 0) {
-        const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)tid * n + k0 + c]);
+        const double2 v = *reinterpret_cast<const double2*>(&Mr[(size_t)tid * n + k0 + c]);
         r[c] = v.x;
         r[c + 1] = v.y;
       } else {
-        r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
-        r[c + 1] = (tid < n && c + 1 < nb) ? M[(size_t)tid * n + k0 + c + 1] : 0.0;
+        r[c] = (tid < n && c < nb) ? Mr[(size_t)tid * n + k0 + c] : 0.0;
+        r[c + 1] = (tid < n && c + 1 < nb) ? Mr[(size_t)tid * n + k0 + c + 1] : 0.0;
       }
     }
     double rowscale = 1.0;
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     auto snap = [&](int jb, double* W) {
       for (int idx = tid; idx < 32 * 32; idx += NT) {
         const int c = idx >> 5, jj = idx & 31;
-        W[c * G1_LDW + jj] = (c < nb && jb + jj < n) ? M[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
+        W[c * G1_LDW + jj] = (c < nb && jb + jj < n) ? Mr[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
       }
     };
     // next block's snapshot: loads issued before the block's DMMA work, stored after it
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
 #pragma unroll
       for (int q = 0; q < SNP; ++q) {
         const int idx = tid + q * NT, c = idx >> 5, jj = idx & 31;
-        v[q] = (idx < 1024 && c < nb && jb + jj < n) ? M[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
+        v[q] = (idx < 1024 && c < nb && jb + jj < n) ? Mr[(size_t)piv[k0 + c] * n + jb + jj] : 0.0;
       }
     };
     auto snap_store = [&](const double (&v)[SNP], double* W) {
@@ -330,12 +335,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
           for (int ni = 0; ni < 4; ++ni) {
             const int j = j0 + ni * 8 + 2 * t4;
             if (vec && live_row && j + 1 < n) {
-              const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)i * n + j]);
+              const double2 v = *reinterpret_cast<const double2*>(&Mr[(size_t)i * n + j]);
               acc[mi][ni][0] = v.x;
               acc[mi][ni][1] = v.y;
             } else {
 #pragma unroll
-              for (int e = 0; e < 2; ++e) acc[mi][ni][e] = (live_row && j + e < n) ? M[(size_t)i * n + j + e] : 0.0;
+              for (int e = 0; e < 2; ++e) acc[mi][ni][e] = (live_row && j + e < n) ? Mr[(size_t)i * n + j + e] : 0.0;
             }
           }
         }
@@ -1642,7 +1647,8 @@ struct Grid {
     return 0;
   }
 
-  int invert(const std::vector<int>& mats, const std::vector<int>& which, const std::vector<int>& slot) {
+  int invert(const std::vector<int>& mats, const std::vector<int>& which, const std::vector<int>& slot,
+             const std::vector<int>* src_slot = nullptr) {
     const int nj = (int)mats.size();
     if (!nj) return 0;
     std::vector<InvJob> jobs(nj);
@@ -1650,6 +1656,7 @@ struct Grid {
       int b = mats[q], w = which[q];
       InvJob& J = jobs[q];
       J.M = S.buf(b, slot[q]);
+      J.Src = (src_slot && n <= 512) ? S.buf(b, (*src_slot)[q]) : nullptr;
       J.piv = d_piv + ((size_t)w * batch + b) * n;
       J.rowstep = d_step + ((size_t)w * batch + b) * n;
       J.Wb = d_W + ((size_t)w * batch + b) * NB * n;
@@ -1855,20 +1862,20 @@ struct Grid {
     std::vector<int> scaling(batch, 1);
     if (ew(act, 2, G_Y, G_Y, G_Y)) return LGM_ERR_CUDA;  // Y = I
     for (int it = 1; it <= maxiter && !act.empty(); ++it) {
-      // invert copies: X -> XI (all), Y -> YI (it > 1)
-      if (ew(act, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
-      if (it > 1 && ew(act, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
-      // non-finite check of X (and Y): as_square inside lu_factor (matcore.py:122)
-      std::vector<int> mats2, which, slot;
-      for (int b : act) { mats2.push_back(b); which.push_back(0); slot.push_back(G_XI); }
+      // inversions of X -> XI (all) and Y -> YI (it > 1): out of place inside G1 (n <= 512),
+      // else copy then invert in place
+      const bool oop = n <= 512;
+      if (!oop) {
+        if (ew(act, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
+        if (it > 1 && ew(act, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
+      }
+      std::vector<int> mats2, which, slot, src;
+      for (int b : act) { mats2.push_back(b); which.push_back(0); slot.push_back(G_XI); src.push_back(G_B); }
       if (it > 1)
-        for (int b : act) { mats2.push_back(b); which.push_back(1); slot.push_back(G_YI); }
-      if (upload_ids(act)) return LGM_ERR_CUDA;
-      CK(cudaMemsetAsync(d_iflag, 0, batch * 4, st));
-      // reuse load_kernel's finiteness test via any_nonfinite on XI/YI
+        for (int b : act) { mats2.push_back(b); which.push_back(1); slot.push_back(G_YI); src.push_back(G_Y); }
       {
         PhaseTimer pt(PH_INVERT, st);
-        if (invert(mats2, which, slot)) return LGM_ERR_CUDA;
+        if (invert(mats2, which, slot, oop ? &src : nullptr)) return LGM_ERR_CUDA;
       }
       // (the singular flags are read back together with the norms below: one sync per iteration)
       // update + norms
