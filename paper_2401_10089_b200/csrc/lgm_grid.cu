@@ -977,6 +977,18 @@ __device__ double pw_block(const double* p, size_t stride, int n) {
 }
 
 // Osborne radix-2 balancing (matcore.py:180-215), one CTA per matrix, bit-identical to numpy.
+// number of pairwise-summation leaves of length n (same recursion as pw_leaves)
+static int host_pw_leaves(int n) {
+  if (n <= 128) return 1;
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return host_pw_leaves(n2) + host_pw_leaves(n - n2);
+}
+// launch shape of balance_kernel_g: 64 threads for n <= 256 (one leaf pair per row / column:
+// more CTAs per SM), else 256 / 1024; dynamic smem = the (leaf, accumulator) partials
+static int bal_threads(int n) { return n <= 256 ? 64 : (n >= 2048 ? 1024 : 256); }
+static size_t bal_smem(int n) { return (size_t)2 * host_pw_leaves(n) * 8 * sizeof(double); }
+
 __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids, double* scale, int* sweeps_out,
                                                         int max_sweeps, double* margin) {
   const int b = ids[blockIdx.x];
@@ -985,7 +997,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
   double* sc = scale + (size_t)b * n;
   __shared__ int loff[128], llen[128];
   __shared__ double lsum[2][128];
-  __shared__ double lacc[2][128 * 8];
+  extern __shared__ double lacc_dyn[];  // [2][nleaf * 8] (sized by the host: bal_smem)
   __shared__ int s_nleaf, s_do;
   __shared__ double s_f, s_mm;
   if (threadIdx.x == 0) { s_nleaf = pw_leaves(n, 0, loff, llen, 0); s_mm = margin[b]; }
@@ -1009,7 +1021,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
         const int m8 = len - len % 8;
         double r = fabs(p[a * stride]);
         for (int k = 8 + a; k < m8; k += 8) r += fabs(p[k * stride]);
-        lacc[which][rem] = r;
+        lacc_dyn[which * nleaf * 8 + rem] = r;
       }
       __syncthreads();
       for (int l = threadIdx.x; l < 2 * nleaf; l += blockDim.x) {
@@ -1022,7 +1034,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
           res = 0.0;
           for (int k = 0; k < len; ++k) res += fabs(p[k * stride]);
         } else {
-          const double* r = &lacc[which][q * 8];
+          const double* r = &lacc_dyn[which * nleaf * 8 + q * 8];
           res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
           for (int k = len - len % 8; k < len; ++k) res += fabs(p[k * stride]);
         }
@@ -2086,7 +2098,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     if (P.balance && !live.empty()) {
       if (G.upload_ids(live)) return LGM_ERR_CUDA;
       PhaseTimer pt(PH_BALANCE, st);
-      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), n >= 2048 ? 1024 : 256, 0, st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
+      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), bal_threads(n), bal_smem(n), st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
       CK(cudaGetLastError());
       std::vector<int> sw(batch);
       CK(cudaMemcpyAsync(sw.data(), G.d_sweeps, batch * 4, cudaMemcpyDeviceToHost, st));
@@ -2409,7 +2421,7 @@ int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n64, int
   lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
   std::vector<double> mm0(batch, INFINITY);
   CK(cudaMemcpyAsync(G.d_margin, mm0.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  lgm_count_launch(), balance_kernel_g<<<batch, n >= 2048 ? 1024 : 256, 0, st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
+  lgm_count_launch(), balance_kernel_g<<<batch, bal_threads(n), bal_smem(n), st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
   lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, B, ld);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
