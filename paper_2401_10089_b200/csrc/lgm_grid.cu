@@ -1019,8 +1019,18 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
         const double* p = which == 0 ? B + (size_t)loff[q] * n + i : B + (size_t)i * n + loff[q];
         const size_t stride = which == 0 ? (size_t)n : 1;
         const int m8 = len - len % 8;
-        double r = fabs(p[a * stride]);
-        for (int k = 8 + a; k < m8; k += 8) r += fabs(p[k * stride]);
+        double r;
+        if (m8 == 128) {  // full leaf: all 16 loads in flight, then the in-order sum
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = fabs(p[(a + 8 * u) * stride]);
+          r = v[0];
+#pragma unroll
+          for (int u = 1; u < 16; ++u) r += v[u];
+        } else {
+          r = fabs(p[a * stride]);
+          for (int k = 8 + a; k < m8; k += 8) r += fabs(p[k * stride]);
+        }
         lacc_dyn[which * nleaf * 8 + rem] = r;
       }
       __syncthreads();
