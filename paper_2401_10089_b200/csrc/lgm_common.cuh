@@ -82,6 +82,14 @@ __device__ __forceinline__ double lgm_rcp_rough(double x) {
   return y;
 }
 
+// FP64 tensor-core MMA (SASS DMMA.8x8x4): d[0..1] += A(8x4, row) * B(4x8, col); lane (g, t) =
+// (lane / 4, lane % 4) supplies A[g][t] and B[t][g] and holds D[g][2t], D[g][2t + 1].
+__device__ __forceinline__ void lgm_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double lgm_warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

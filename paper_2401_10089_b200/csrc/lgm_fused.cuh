@@ -816,37 +816,60 @@ struct Ctx {
   };
   static constexpr int TMAX = 7;  // nodes P2..P7
 
-  // acc[jj] = sum_kk L[row][kk] * R[kk][col0 + jj], col0 = team * NMAX/2, with
-  // L = sum_{t=2..nn} crow[t-1] * P_t + crow[0] * I formed on the fly with numpy's _combine
-  // rounding (schemes.py:91-101: sequential over t, zero coefficients skipped, products and
-  // sums rounded separately).
-  __device__ void gemm_comb(const Nodes& nd, int nn, const double* crow, const double* R, double (&acc)[NMAX / 2]) {
-    const int col0 = team * (NMAX / 2);
+  // Polynomial GEMMs on the FP64 tensor cores (mma.sync m8n8k4 -> DMMA): warp w owns output
+  // rows 16w .. 16w+15 (two 8-row tiles) x all NMAX/8 column tiles, so every left-operand
+  // element is formed once per CTA; acc[(mi * FT + ni) * 2 + e] = C[frow(mi)][fcol(ni, e)].
+  // A right operand materialised by combine_rhs uses a swizzled layout (row stride NMAX,
+  // column c of row k stored at c ^ 4(k & 3)): the row-per-warp writes and the B fragment
+  // reads (rows t, columns g) are both bank-conflict free.
+  static constexpr int FT = NMAX / 8;  // column tiles
+  __device__ __forceinline__ static int swz(int k, int c) { return k * NMAX + (c ^ ((k & 3) << 2)); }
+  __device__ __forceinline__ int frow(int mi) const { return 16 * warp + 8 * mi + (lane >> 2); }
+  __device__ __forceinline__ int fcol(int ni, int e) const { return 8 * ni + 2 * (lane & 3) + e; }
+
+  // acc = L * R with L = sum_{t=2..nn} crow[t-1] * P_t + crow[0] * I formed on the fly with
+  // numpy's _combine rounding (schemes.py:91-101: sequential over t, zero coefficients
+  // skipped, products and sums rounded separately).  R: swizzled (rswz) or row stride LDM.
+  __device__ void gemm_comb(const Nodes& nd, int nn, const double* crow, const double* R, bool rswz,
+                            double (&acc)[NMAX / 2]) {
 #pragma unroll
-    for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = 0.0;
-    if (row >= n) return;
-    const double* Lr[TMAX - 1];
+    for (int q = 0; q < NMAX / 2; ++q) acc[q] = 0.0;
     double cf[TMAX - 1];
 #pragma unroll
-    for (int t = 2; t <= TMAX; ++t) {
-      cf[t - 2] = (t <= nn) ? crow[t - 1] : 0.0;
-      Lr[t - 2] = nd.ptr(t) + row * nd.ld(t);
-    }
+    for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? crow[t - 1] : 0.0;
     const double l0 = crow[0];
-    for (int kk = 0; kk < n; ++kk) {
-      double l = 0.0;
+    const int t4 = lane & 3;
+#pragma unroll 2
+    for (int k0 = 0; k0 < n; k0 += 4) {
+      const int kk = k0 + t4;
+      double a[2], b[FT];
 #pragma unroll
-      for (int t = 2; t <= TMAX; ++t)
-        if (cf[t - 2] != 0.0) l = __dadd_rn(l, __dmul_rn(cf[t - 2], Lr[t - 2][kk]));
-      if (kk == row && l0 != 0.0) l = __dadd_rn(l, l0);
-      const double* Rr = R + kk * C::LDM + col0;
+      for (int mi = 0; mi < 2; ++mi) {
+        const int i = frow(mi);
+        double l = 0.0;
+        if (i < n && kk < n) {
 #pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj) acc[jj] = fma(l, Rr[jj], acc[jj]);  // LDM odd: 8 B aligned
+          for (int t = 2; t <= TMAX; ++t)
+            if (cf[t - 2] != 0.0) l = __dadd_rn(l, __dmul_rn(cf[t - 2], nd.ptr(t)[i * nd.ld(t) + kk]));
+          if (kk == i && l0 != 0.0) l = __dadd_rn(l, l0);
+        }
+        a[mi] = l;
+      }
+#pragma unroll
+      for (int ni = 0; ni < FT; ++ni) {
+        const int c = 8 * ni + (lane >> 2);
+        b[ni] = (kk < n && c < n) ? R[rswz ? swz(kk, c) : kk * C::LDM + c] : 0.0;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < FT; ++ni)
+          lgm_dmma(*reinterpret_cast<double(*)[2]>(&acc[(mi * FT + ni) * 2]), a[mi], b[ni]);
     }
   }
 
-  // D[i][j] = sum_{t=2..nn} crow[t-1] P_t[i][j] + crow[0] I (schemes.py:91-101 order)
-  __device__ void combine_into(double* D, const Nodes& nd, int nn, const double* crow) {
+  // D (swizzled) = sum_{t=2..nn} crow[t-1] P_t + crow[0] I (schemes.py:91-101 order)
+  __device__ void combine_rhs(double* D, const Nodes& nd, int nn, const double* crow) {
     double cf[TMAX - 1];
 #pragma unroll
     for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? crow[t - 1] : 0.0;
@@ -858,17 +881,20 @@ struct Ctx {
         for (int t = 2; t <= TMAX; ++t)
           if (cf[t - 2] != 0.0) v = __dadd_rn(v, __dmul_rn(cf[t - 2], nd.ptr(t)[i * nd.ld(t) + j]));
         if (i == j && c0 != 0.0) v = __dadd_rn(v, c0);
-        D[i * C::LDM + j] = v;
+        D[swz(i, j)] = v;
       }
   }
 
-  __device__ void store_half_rows(double* D, int ld, const double (&acc)[NMAX / 2]) {
-    if (row < n) {
-      double* Dr = D + row * ld + team * (NMAX / 2);
+  __device__ void store_frag(double* D, int ld, const double (&acc)[NMAX / 2]) {
 #pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj)
-        if (team * (NMAX / 2) + jj < n) Dr[jj] = acc[jj];
-    }
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < FT; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = frow(mi), c = fcol(ni, e);
+          if (i < n && c < n) D[i * ld + c] = acc[(mi * FT + ni) * 2 + e];
+        }
   }
 
   // P2 = X in buf(bX), P3 = X^2 in buf(b3) (computed here if !have_fp: one product), R temp
@@ -889,65 +915,78 @@ struct Ctx {
     double acc[NMAX / 2];
     if (!have_fp) {  // P3 = P2 * P2
       const double one[2] = {0.0, 1.0};
-      gemm_comb(nd, 2, one, buf(bX), acc);
+      gemm_comb(nd, 2, one, buf(bX), false, acc);
       products++;
       __syncthreads();
-      store_half_rows(b3.p, b3.ld, acc);
+      store_frag(b3.p, b3.ld, acc);
       __syncthreads();
     }
     int nn = 3;  // nodes P1..P3 available
     bool last_in_regs = false;
     for (int j = 1; j < k; ++j) {
-      combine_into(R, nd, nn, lgm_rhs(*P, k, j));
+      combine_rhs(R, nd, nn, lgm_rhs(*P, k, j));
       __syncthreads();
-      gemm_comb(nd, nn, lgm_lhs(*P, k, j), R, acc);
+      gemm_comb(nd, nn, lgm_lhs(*P, k, j), R, true, acc);
       products++;
       nn++;
       __syncthreads();
       if (j < k - 1) {
-        store_half_rows(const_cast<double*>(nd.ptr(nn)), nd.ld(nn), acc);
+        store_frag(const_cast<double*>(nd.ptr(nn)), nd.ld(nn), acc);
         __syncthreads();
       } else {
         last_in_regs = true;
       }
     }
-    // epilogue: z = sum out[t] P_t + out[0] I, L = mult * z * (scale_i / scale_j) into R
+    // epilogue (fragment layout): z = sum out[t] P_t + out[0] I, L = mult * z * (scale_i /
+    // scale_j) into R (row stride LDM); per element the operation order over t is numpy's
     const double* orow = lgm_out(*P, k);
     const double* sc = scale();
-    if (row < n) {
-      const int col0 = team * (NMAX / 2);
+    {
       double cf[TMAX - 1];
 #pragma unroll
       for (int t = 2; t <= TMAX; ++t) cf[t - 2] = (t <= nn) ? orow[t - 1] : 0.0;
-      // node-outer / column-inner: one node's 16 values of this row are loaded together (the
-      // per-element operation order over t is unchanged)
       double z[NMAX / 2];
 #pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj) z[jj] = 0.0;
+      for (int q = 0; q < NMAX / 2; ++q) z[q] = 0.0;
 #pragma unroll
       for (int t = 2; t <= TMAX; ++t) {
         if (cf[t - 2] != 0.0) {
           const bool regs = (t == nn && last_in_regs);
-          const double* src = nd.ptr(t) + row * nd.ld(t) + col0;
+          const double* src = nd.ptr(t);
+          const int sld = nd.ld(t);
           double pv[NMAX / 2];
 #pragma unroll
-          for (int jj = 0; jj < NMAX / 2; ++jj) pv[jj] = regs ? acc[jj] : ((col0 + jj < n) ? src[jj] : 0.0);
+          for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-          for (int jj = 0; jj < NMAX / 2; ++jj) z[jj] = __dadd_rn(z[jj], __dmul_rn(cf[t - 2], pv[jj]));
+            for (int ni = 0; ni < FT; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int q = (mi * FT + ni) * 2 + e, i = frow(mi), c = fcol(ni, e);
+                pv[q] = regs ? acc[q] : ((i < n && c < n) ? src[i * sld + c] : 0.0);
+              }
+#pragma unroll
+          for (int q = 0; q < NMAX / 2; ++q) z[q] = __dadd_rn(z[q], __dmul_rn(cf[t - 2], pv[q]));
         }
       }
 #pragma unroll
-      for (int jj = 0; jj < NMAX / 2; ++jj) {
-        const int col = col0 + jj;
-        if (col < n) {
-          double v = z[jj];
-          if (row == col && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
-          v = mult * v;
-          // sc[] are powers of two within (1e-300, 1e300) (radix-2 balancing), so
-          // sc[row] / sc[col] == sc[row] * 2^-e(col) exactly: the reciprocal is an exponent flip
-          if (unbal) v = v * (sc[row] * __hiloint2double(0x7fe00000 - __double2hiint(sc[col]), 0));
-          R[row * C::LDM + col] = v;
-        }
+      for (int mi = 0; mi < 2; ++mi) {
+        const int i = frow(mi);
+        const double si = unbal && i < n ? sc[i] : 1.0;
+#pragma unroll
+        for (int ni = 0; ni < FT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = (mi * FT + ni) * 2 + e, c = fcol(ni, e);
+            if (i < n && c < n) {
+              double v = z[q];
+              if (i == c && orow[0] != 0.0) v = __dadd_rn(v, orow[0]);
+              v = mult * v;
+              // sc[] are powers of two within (1e-300, 1e300) (radix-2 balancing), so
+              // sc[i] / sc[c] == sc[i] * 2^-e(c) exactly: the reciprocal is an exponent flip
+              if (unbal) v = v * (si * __hiloint2double(0x7fe00000 - __double2hiint(sc[c]), 0));
+              R[i * C::LDM + c] = v;
+            }
+          }
       }
     }
     __syncthreads();
@@ -1190,9 +1229,9 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
     typename Ctx<NMAX, FULL>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), Cfg<NMAX>::LDM, nullptr, 0, 0};  // P2 := A - I
     const double one[2] = {0.0, 1.0};
     double acc[NMAX / 2];
-    c.gemm_comb(nd, 2, one, c.buf(BUF_Y), acc);
+    c.gemm_comb(nd, 2, one, c.buf(BUF_Y), false, acc);
     products++;
-    c.store_half_rows(AI2.p, AI2.ld, acc);
+    c.store_frag(AI2.p, AI2.ld, acc);
     __syncthreads();
     nI2 = c.onenorm_ref(AI2);
   }
