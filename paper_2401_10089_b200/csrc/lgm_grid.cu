@@ -66,6 +66,16 @@ enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7 };
     }                                                                               \
   } while (0)
 
+// One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
+bool est_fused_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("LGM_EST_FUSED");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 __device__ __forceinline__ uint64_t dkey(double nonneg) { return (uint64_t)__double_as_longlong(nonneg) + 1ull; }
 
 // Block-wide argmax of (key, index): max key, ties -> lowest index.  All threads get the result.
@@ -197,10 +207,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     const int nb = min(32, n - k0);
     double r[32];
     // (per-thread row loads: measured faster than staging through shared memory)
-#pragma unroll
     // (the first panel reads the source matrix when inverting out of place: every element of
     // M is written during panel 0 -- K columns by the panel store, the rest by its update)
     const double* Mr = (k0 == 0 && J.Src) ? J.Src : M;
+#pragma unroll
     for (int c = 0; c < 32; c += 2) {
       if (tid < n && c + 1 < nb && (n & 1) == 0) {
         const double2 v = *reinterpret_cast<const double2*>(&Mr[(size_t)tid * n + k0 + c]);
@@ -1281,9 +1291,8 @@ __device__ __forceinline__ void mgap(double& mm, double a, double b) {
 }
 
 // After the forward application: column 1-norms, argmax, estimate update, S = sign(Y).
-__global__ void __launch_bounds__(256) est_after_fwd_kernel(EstJob* jobs, int n, int sweep) {
-  __shared__ double sred[8];
-  EstJob& J = jobs[blockIdx.x];
+// (CTA-wide body: 256 threads per job, shared by the per-step kernels and est_fused_kernel)
+__device__ void est_after_fwd_body(EstJob& J, int n, int sweep, double* sred) {
   if (J.done) return;
   double* Yv = (J.total & 1) ? J.V1 : J.V0;
   const int nc = J.ncols;
@@ -1319,14 +1328,23 @@ __global__ void __launch_bounds__(256) est_after_fwd_kernel(EstJob* jobs, int n,
       }
   }
 }
+__global__ void __launch_bounds__(256) est_after_fwd_kernel(EstJob* jobs, int n, int sweep) {
+  __shared__ double sred[8];
+  est_after_fwd_body(jobs[blockIdx.x], n, sweep, sred);
+}
 
 // After the adjoint: h = row max |Z|, top-(4t+1) order, picks, stopping test, next X.
-__global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n, int sweep) {
-  __shared__ uint64_t skey[8];
-  __shared__ int sidx[8];
-  __shared__ int order[9];
-  __shared__ double hval[9];
-  EstJob& J = jobs[blockIdx.x];
+struct EstAdjSmem {
+  uint64_t skey[8];
+  int sidx[8];
+  int order[9];
+  double hval[9];
+};
+__device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) {
+  uint64_t* skey = sa.skey;
+  int* sidx = sa.sidx;
+  int* order = sa.order;
+  double* hval = sa.hval;
   if (J.done) return;
   const double* Z = (J.total & 1) ? J.V1 : J.V0;
   const int nc = J.ncols;
@@ -1381,6 +1399,110 @@ __global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n,
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     J.V0[i] = (i == order[0]) ? 1.0 : 0.0;
     J.V0[n + i] = (i == order[1]) ? 1.0 : 0.0;
+  }
+}
+__global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n, int sweep) {
+  __shared__ EstAdjSmem sa;
+  est_after_adj_body(jobs[blockIdx.x], n, sweep, sa);
+}
+
+// The whole estimate for one job per CTA (256 threads), M1 resident in shared memory
+// (n <= EST_FUSED_MAXN): one launch instead of 1 + itmax (2 total + 2) per-step launches.
+// Every reduction reproduces the per-step kernels' order exactly (forward: warp per row,
+// lane-strided FMAs + butterfly; adjoint: thread per column, 64-row slabs with 4 accumulators,
+// slab partials summed in order; the after-bodies are shared), so the two paths agree bit for bit.
+constexpr int EST_FUSED_MAXN = 160;
+__global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, int itmax) {
+  extern __shared__ __align__(16) double Ms[];
+  __shared__ double sred[8];
+  __shared__ EstAdjSmem sa;
+  EstJob& J = jobs[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {  // est_init_kernel
+    const int t = n < 2 ? n : 2;
+    for (int i = tid; i < n; i += 256) {
+      J.V0[i] = 1.0 / n;
+      if (t > 1) J.V0[n + i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
+    }
+    if (tid == 0) {
+      J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
+      J.total = J.p1 + (J.M2 ? 1 : 0);
+      J.done = J.zero ? 1 : 0;
+    }
+  }
+  if (J.zero) return;  // (uniform: host-set)
+  for (int idx = tid; idx < n * n; idx += 256) Ms[idx] = J.M1[idx];
+  __syncthreads();
+  const int total = J.p1 + (J.M2 ? 1 : 0);
+  const int splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  for (int sweep = 0; sweep < itmax; ++sweep) {
+    if (J.done) break;
+    const int nc = J.ncols;
+    for (int q = 0; q < total; ++q) {  // forward (est_fwd_kernel)
+      const double* M = (J.M2 && q == 0) ? J.M2 : Ms;
+      const double* x = (q & 1) ? J.V1 : J.V0;
+      double* y = (q & 1) ? J.V0 : J.V1;
+      for (int i = warp; i < n; i += 8) {
+        double a0 = 0.0, a1 = 0.0;
+        const double* Mr = M + (size_t)i * n;
+        for (int j = lane; j < n; j += 32) {
+          const double m = Mr[j];
+          a0 = fma(m, x[j], a0);
+          if (nc > 1) a1 = fma(m, x[n + j], a1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if (lane == 0) {
+          y[i] = a0;
+          if (nc > 1) y[n + i] = a1;
+        }
+      }
+      __syncthreads();
+    }
+    est_after_fwd_body(J, n, sweep, sred);
+    __syncthreads();
+    if (J.done) break;
+    const bool two = J.ncols > 1;
+    for (int q = 0; q < total; ++q) {  // adjoint (est_adj_kernel + est_adj_reduce_kernel)
+      const double* M = (q < J.p1) ? Ms : J.M2;
+      const double* x = (q & 1) ? J.V1 : J.V0;
+      double* y = (q & 1) ? J.V0 : J.V1;
+      const int j = tid;
+      double s0 = 0.0, s1 = 0.0;
+      if (j < n) {
+        for (int sl = 0; sl < splits; ++sl) {
+          const int r0 = sl * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
+          double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+          int r = r0;
+          for (; r + 3 < r1; r += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double m = M[(size_t)(r + u) * n + j];
+              a0[u] = fma(m, x[r + u], a0[u]);
+              if (two) a1[u] = fma(m, x[n + r + u], a1[u]);
+            }
+          }
+          for (; r < r1; ++r) {
+            const double m = M[(size_t)r * n + j];
+            a0[0] = fma(m, x[r], a0[0]);
+            if (two) a1[0] = fma(m, x[n + r], a1[0]);
+          }
+          s0 += (a0[0] + a0[1]) + (a0[2] + a0[3]);
+          s1 += (a1[0] + a1[1]) + (a1[2] + a1[3]);
+        }
+      }
+      __syncthreads();  // every thread has read x before y (the other buffer) is written
+      if (j < n) {
+        y[j] = s0;
+        if (two) y[n + j] = s1;
+      }
+      __syncthreads();
+    }
+    est_after_adj_body(J, n, sweep, sa);
+    __syncthreads();
   }
 }
 
@@ -1814,6 +1936,11 @@ struct Grid {
     }
     CK(cudaMemcpyAsync(d_est, jobs.data(), nj * sizeof(EstJob), cudaMemcpyHostToDevice, st));
     const double rsum = host_pairwise_abs_ramp(n);
+    if (n <= EST_FUSED_MAXN && est_fused_on()) {
+      const int sm = n * n * 8;
+      CK(cudaFuncSetAttribute(est_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      lgm_count_launch(), est_fused_kernel<<<nj, 256, sm, st>>>(d_est, n, rsum, itmax);
+    } else {
     lgm_count_launch(), est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, rsum);
     for (int sweep = 0; sweep < itmax; ++sweep) {
       for (int q = 0; q < maxtot; ++q) lgm_count_launch(), est_fwd_kernel<<<dim3((n + 7) / 8, nj), 256, 0, st>>>(d_est, n, q);
@@ -1823,6 +1950,7 @@ struct Grid {
         lgm_count_launch(), est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
       }
       lgm_count_launch(), est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
+    }
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(jobs.data(), d_est, nj * sizeof(EstJob), cudaMemcpyDeviceToHost, st));

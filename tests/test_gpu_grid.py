@@ -92,7 +92,7 @@ def test_est_zero_and_diag_grid():
     assert est[0] == pytest.approx(8.0, rel=1e-14)
 
 
-@pytest.mark.parametrize("n", [65, 128, 200, 520, 545, 1000, 1024])
+@pytest.mark.parametrize("n", [65, 128, 200, 320, 384, 512, 520, 545, 1000, 1024])
 def test_sqrt_db_grid(n):
     rng = np.random.default_rng(n)
     G = rng.standard_normal((2, n, n))
@@ -206,3 +206,43 @@ def test_selection_invariant_grid(c, B):
     th = np.array(C.THETA)[reps["k"] - 1]
     assert (reps["alpha_used"] <= th).all()
     assert (reps["products"] == np.where(reps["s"] >= 1, reps["k"] - 1, reps["k"])).all()
+
+
+
+def test_est_fused_matches_per_step_kernels(tmp_path):
+    """Engine G's one-launch estimator (est_fused_kernel, n <= 160, M1 in shared memory)
+    reproduces the per-step estimator kernels (LGM_EST_FUSED=0, subprocess) bit for bit: the
+    estimates, pass counts and the whole logm (reports and L) at config-3b shapes."""
+    import subprocess
+    import sys
+    rng = np.random.default_rng(11)
+    mats = {n: rng.standard_normal((3, n, n)) for n in (65, 100, 128, 160)}
+    A3 = synth.config("3b", batch=6)
+    np.savez(tmp_path / "in.npz", A3=A3, **{f"m{n}": m for n, m in mats.items()})
+    ests = {}
+    for n, m in mats.items():
+        for p, two in ((1, False), (3, True), (7, False)):
+            M2 = m[::-1].copy() if two else None
+            ests[f"{n}_{p}"] = lp.primitives._est(m, p, M2, 5, True)
+    L1, r1 = lp.logm_batched(A3, lp.LogmOptions(raise_on_error=False))
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {repr(ROOT)})
+import paper_2401_10089_b200 as lp
+d = np.load({repr(str(tmp_path / 'in.npz'))})
+out = {{}}
+for n in (65, 100, 128, 160):
+    m = d[f"m{{n}}"]
+    for p, two in ((1, False), (3, True), (7, False)):
+        e, ps = lp.primitives._est(m, p, m[::-1].copy() if two else None, 5, True)
+        out[f"e{{n}}_{{p}}"] = e
+        out[f"p{{n}}_{{p}}"] = ps
+L, r = lp.logm_batched(d["A3"], lp.LogmOptions(raise_on_error=False))
+np.savez({repr(str(tmp_path / 'out.npz'))}, L=L, r=r.view(np.uint8), **out)
+"""
+    env = dict(os.environ, LGM_EST_FUSED="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    o = np.load(tmp_path / "out.npz")
+    for key, (e, ps) in ests.items():
+        assert np.array_equal(o["e" + key], e) and np.array_equal(o["p" + key], ps), key
+    assert np.array_equal(o["L"], L1) and o["r"].tobytes() == r1.view(np.uint8).tobytes()
