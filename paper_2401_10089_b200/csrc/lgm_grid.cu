@@ -66,6 +66,20 @@ enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7 };
     }                                                                               \
   } while (0)
 
+// G1 (one CTA per inversion) or G2 (per-panel kernels, rank-64 combined passes)?  Measured at
+// config 4 (n = 512, 512 jobs per DB step): G2 with single-CTA panels 441 ms vs G1 452 ms;
+// at n = 128 G1 (57 ms) beats G2 (81 ms).  By n only, so a matrix's arithmetic does not depend
+// on the batch it is in.  LGM_G1_MAXN=<m> overrides: G1 exactly for n <= m (m <= 512).
+bool use_g1(int n) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = std::getenv("LGM_G1_MAXN");
+    v = e ? std::min(512, std::max(0, std::atoi(e))) : -1;
+  }
+  if (v >= 0) return n <= v;
+  return n <= 256 || (n <= 512 && n % 64 != 0);
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static int on = -1;
@@ -541,6 +555,207 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
   cl.sync();
 }
 
+#ifdef LGM_PANEL_PROF
+__device__ unsigned long long g_panel_cyc[6];  // load, stage-1, factor, store, CTAs
+#define PP_T(v) long long v = clock64()
+#define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
+#else
+#define PP_T(v)
+#define PP_ADD(i, val)
+#endif
+// G2 panel for n <= 512 (many jobs): one CTA of NT >= n threads per inversion, row `tid`
+// of the 32-column panel in registers, the pivot rule and shift-in-FMA frame of G1
+// (gj_inv_cta_kernel).  No cluster: with hundreds of jobs the 8-CTA cluster panel's
+// per-step cluster barriers serialise into many waves.
+template <int NT>
+// s1_a1kind >= 0 (P2 of a rank-64 pair): the stage-1 update of P2's columns by P1 is applied
+// to the loaded rows first (r <- z1 r + A1 W1[:, P2], FMA chain in c' order), replacing the
+// narrow gj_update_kernel launch and its snapshot.
+__global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob* jobs, int n, int k0, int nb, int a1_kind,
+                                                                   int s1_a1kind) {
+  constexpr int NW = NT / 32;
+  __shared__ __align__(16) double prow[2][40];
+  __shared__ unsigned wkey32[2][16];
+  __shared__ double wval[2][16];
+  __shared__ double red[16];
+  const InvJob J = jobs[blockIdx.x];
+  if (*J.status) return;  // uniform per CTA
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 80) (&prow[0][0])[tid] = 0.0;  // pure-rotation steps read it with g = 0
+  PP_T(t0);
+  bool used = tid < n ? (J.rowstep[tid] >= 0) : true;
+  double r[32];
+  double* M = J.M;
+  // full panels move through a per-warp 32 x 33 shared tile: the warp reads / writes its 32
+  // rows' 256-byte segments coalesced (one row per instruction) instead of one strided
+  // 256-byte segment per lane
+  extern __shared__ __align__(16) double ptile[];
+  double* T = ptile + warp * 32 * 33;
+  const bool tiled = nb == 32 && (n & 31) == 0;
+  if (tiled) {
+    if (warp * 32 < n) {
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) r[rr] = M[(size_t)(warp * 32 + rr) * n + k0 + lane];  // all in flight
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = r[rr];
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) r[c] = T[lane * 33 + c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) r[c] = 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      if (tid < n && c + 1 < nb && (n & 1) == 0) {
+        const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)tid * n + k0 + c]);
+        r[c] = v.x;
+        r[c + 1] = v.y;
+      } else {
+        r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
+        r[c + 1] = (tid < n && c + 1 < nb) ? M[(size_t)tid * n + k0 + c + 1] : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+  PP_T(t1);
+  PP_ADD(0, t1 - t0);
+  if (s1_a1kind >= 0) {
+    __shared__ __align__(16) double w1s[32][34];
+    const int p1 = k0 - NB;
+    for (int idx = tid; idx < 32 * 32; idx += NT) {
+      const int c1 = idx >> 5, c = idx & 31;
+      w1s[c1][c] = M[(size_t)J.piv[p1 + c1] * n + k0 + c];
+    }
+    __syncthreads();
+    if (tid < n) {
+      const int rs = J.rowstep[tid];
+      if (rs >= p1 && rs < k0) {  // P1 pivot row: z1 = 0
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = 0.0;
+      }
+      const double* a1 = wkind(J, s1_a1kind) + (size_t)tid * NB;
+#pragma unroll 1
+      for (int c1 = 0; c1 < 32; c1 += 4) {
+        const double2 x01 = *reinterpret_cast<const double2*>(a1 + c1);
+        const double2 x23 = *reinterpret_cast<const double2*>(a1 + c1 + 2);
+        const double av[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const double2 w = *reinterpret_cast<const double2*>(&w1s[c1 + u][c]);
+            r[c] = fma(av[u], w.x, r[c]);
+            r[c + 1] = fma(av[u], w.y, r[c + 1]);
+          }
+      }
+    }
+  }
+  double rowscale = 1.0, mypiv = 1.0;
+  bool piv_here = false;
+  __syncthreads();
+  PP_T(t2);
+  PP_ADD(1, t2 - t1);
+#pragma unroll 1
+  for (int kk = 0; kk < 32; ++kk) {
+    const int par = kk & 1;
+    const double* pr = prow[par];
+    const double r0 = r[0];
+    double g = 0.0, last = r0;  // kk >= nb: pure rotation
+    if (kk < nb) {
+      const bool cand = (tid < n) && !used && r0 != 0.0;
+      const unsigned key = cand ? ((((unsigned)__double2hiint(r0) & 0x7fffffffu) & ~0x3ffu) | (unsigned)(1023 - tid)) : 0u;
+      const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+      const double wv = __shfl_sync(0xffffffffu, r0, (1023 - (int)(wk & 0x3ffu)) & 31);
+      if (lane == 0) {
+        wkey32[par][warp] = wk;
+        wval[par][warp] = wv;
+      }
+      __syncthreads();
+      const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par][lane] : 0u);
+      if (bk == 0u) {  // exact zero pivot (matcore.py:124-125)
+        if (tid == 0) *J.status = 1;
+        return;
+      }
+      const int p = 1023 - (int)(bk & 0x3ffu);
+      const double rp = lgm_rcp(wval[par][p >> 5]);
+      const bool own = (tid == p);
+      if (own) {
+        used = true;
+        piv_here = true;
+        mypiv = r0;
+        rowscale = rp;
+        double* pw = prow[par];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
+        J.rowstep[tid] = k0 + kk;
+        J.piv[k0 + kk] = tid;
+      }
+      __syncthreads();
+      g = own ? 0.0 : r0 * rp;
+      last = own ? 1.0 : -g;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
+      if (c > 0) r[c - 1] = fma(-g, p2.x, r[c]);
+      r[c] = fma(-g, p2.y, r[c + 1]);
+    }
+    r[31] = last;
+  }
+  if (piv_here) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] *= rowscale;
+  }
+  PP_T(t3);
+  PP_ADD(2, t3 - t2);
+  if (tiled) {
+    if (warp * 32 < n) {
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) T[lane * 33 + c] = r[c];
+      __syncwarp();
+      double* A1 = a1_kind >= 0 ? wkind(J, a1_kind) : nullptr;  // rank-64 pair: P1's multipliers
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) {
+        const double v = T[rr * 33 + lane];
+        M[(size_t)(warp * 32 + rr) * n + k0 + lane] = v;
+        if (A1) A1[(size_t)(warp * 32 + rr) * NB + lane] = v;
+      }
+    }
+  } else if (tid < n) {
+    if (nb == 32 && (n & 1) == 0) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 2)
+        *reinterpret_cast<double2*>(&M[(size_t)tid * n + k0 + c]) = make_double2(r[c], r[c + 1]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c < nb) M[(size_t)tid * n + k0 + c] = r[c];
+    }
+    if (a1_kind >= 0) {  // rank-64 pair: P1's multipliers also go to A1 (gj_copy_a1_kernel's layout)
+      double* A1 = wkind(J, a1_kind) + (size_t)tid * NB;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(A1 + c) = make_double2(r[c], r[c + 1]);
+    }
+  }
+  // log|det| of this panel's pivots, CTA sum in warp order, one update per panel
+  double lg = piv_here ? log(fabs(mypiv)) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+  if (lane == 0) red[warp] = lg;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += red[w];
+    *J.logdet += t;
+  }
+  PP_T(t4);
+  PP_ADD(3, t4 - t3);
+  PP_ADD(4, 1);
+}
+
 __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n, int k0, int nb, int in_smem) {
   extern __shared__ __align__(16) double psm[];
   __shared__ uint64_t skey[16];
@@ -747,8 +962,10 @@ __global__ void gj_copy_a1_kernel(const InvJob* jobs, int n, int k0, int ka1) {
 // W2 (into J.W2) from the unmodified pivot rows of P2, A1 and W1 (= J.W); then W1's P1 columns
 // are zeroed for the combined pass.  One thread per column j, the 32 x 32 block A1[p2_c][:] in
 // shared memory.
-__global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, int k0, int q) {
-  __shared__ double a1s[NB][NB + 1];
+// snap = 1: W1 is not snapshotted beforehand -- its rows are read from M (P1's pivot rows,
+// not yet touched by the pass) and written here (one kernel instead of snapshot + W2).
+__global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, int k0, int q, int snap) {
+  __shared__ __align__(16) double a1s[NB][NB + 2];
   __shared__ int p2s[NB];
   const InvJob J = jobs[blockIdx.y];
   if (*J.status) return;
@@ -778,13 +995,25 @@ __global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, i
     return;
   }
   double w[NB];
+  if (snap) {
 #pragma unroll
-  for (int cc = 0; cc < NB; ++cc) w[cc] = W1[(size_t)cc * n + j];
+    for (int cc = 0; cc < NB; ++cc) {
+      w[cc] = J.M[(size_t)J.piv[k0 + cc] * n + j];
+      W1[(size_t)cc * n + j] = w[cc];
+    }
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < NB; ++cc) w[cc] = W1[(size_t)cc * n + j];
+  }
 #pragma unroll 2
   for (int c = 0; c < NB; ++c) {
     double acc = J.M[(size_t)p2s[c] * n + j];
 #pragma unroll
-    for (int cc = 0; cc < NB; ++cc) acc = fma(a1s[c][cc], w[cc], acc);
+    for (int cc = 0; cc < NB; cc += 2) {  // 16-byte broadcast loads, same FMA order
+      const double2 a = *reinterpret_cast<const double2*>(&a1s[c][cc]);
+      acc = fma(a.x, w[cc], acc);
+      acc = fma(a.y, w[cc + 1], acc);
+    }
     W2[(size_t)c * n + j] = acc;
   }
 }
@@ -1800,7 +2029,7 @@ struct Grid {
       int b = mats[q], w = which[q];
       InvJob& J = jobs[q];
       J.M = S.buf(b, slot[q]);
-      J.Src = (src_slot && n <= 512) ? S.buf(b, (*src_slot)[q]) : nullptr;
+      J.Src = (src_slot && use_g1(n)) ? S.buf(b, (*src_slot)[q]) : nullptr;
       J.piv = d_piv + ((size_t)w * batch + b) * n;
       J.rowstep = d_step + ((size_t)w * batch + b) * n;
       J.Wb = d_W + ((size_t)w * batch + b) * NB * n;
@@ -1809,16 +2038,30 @@ struct Grid {
       J.status = d_istat + w * batch + b;
     }
     CK(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(InvJob), cudaMemcpyHostToDevice, st));
-    if (n <= 512) {  // G1: one CTA per inversion, no per-panel launches
+    if (use_g1(n)) {  // G1: one CTA per inversion, no per-panel launches
       if (n <= 128) return launch_g1<128>(nj);
       if (n <= 256) return launch_g1<256>(nj);
       return launch_g1<512>(nj);
     }
     lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
     const int tiles = (n + TM - 1) / TM;
-    auto panel = [&](int k0, cudaStream_t s) {
+    const bool cta_panel = n <= 512;  // one CTA per panel (writes A1 itself: no gj_copy_a1_kernel)
+    auto panel = [&](int k0, cudaStream_t s, int a1_kind = -1, int s1_a1kind = -1) {
       const int nb = std::min(NB, n - k0);
-      if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(gj_panel_cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 33 * 8);
+        cudaFuncSetAttribute(gj_panel_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 33 * 8);
+        cudaFuncSetAttribute(gj_panel_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 32 * 33 * 8);
+        attr = true;
+      }
+      if (n <= 128) {  // many small jobs: one CTA per inversion, no cluster
+        lgm_count_launch(), gj_panel_cta_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+      } else if (n <= 256) {
+        lgm_count_launch(), gj_panel_cta_kernel<256><<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+      } else if (n <= 512) {
+        lgm_count_launch(), gj_panel_cta_kernel<512><<<nj, 512, 16 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+      } else if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
         lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, s>>>(d_jobs, n, k0, nb);
       } else {
         lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, s>>>(d_jobs, n, k0, nb, 0);
@@ -1841,12 +2084,15 @@ struct Grid {
       CK(cudaEventCreateWithFlags(&evN, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
     }
-    panel(0, st);
     static const bool rank64 = [] {  // LGM_G2_RANK64=0 falls back to rank-32 passes (A/B switch)
       const char* e = std::getenv("LGM_G2_RANK64");
       return !(e && e[0] == '0');
     }();
-    if (rank64 && n % (2 * NB) == 0 && n > 512 && nj >= 4) {  // few jobs: the exposed P2 panel costs more
+    // few large jobs: the exposed P2 panel costs more than the second pass (n > 512 only: for
+    // n <= 512 the choice stays independent of the batch)
+    const bool use64 = rank64 && n % (2 * NB) == 0 && (nj >= 4 || n <= 512);
+    panel(0, st, use64 && cta_panel ? 2 : -1);
+    if (use64) {
       // rank-64 delayed update with both panels of the next pair factored on sB during the
       // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
       // rows), A1 (copy of P1's multipliers), stage-1 update of P2's columns, factor P2, W2.
@@ -1855,15 +2101,20 @@ struct Grid {
                               (int)up2_smem<128>()));
       auto prepare_pair = [&](int k0, int q, cudaStream_t s, bool full_snapshot) {
         // P1 = [k0, k0+NB) already factored; everything except the full-width W1 / W2
+        if (cta_panel) {  // stage-1 update fused into P2's panel kernel
+          panel(k0 + NB, s, -1, 3 * q + 2);
+          return;
+        }
         if (full_snapshot) snapshot(k0, 3 * q, 0, n, s);
         else snapshot(k0, 3 * q, k0 + NB, k0 + 2 * NB, s);  // P2's columns only (for stage 1)
-        lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, s>>>(d_jobs, n, k0, 3 * q + 2);
+        if (!cta_panel)
+          lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, s>>>(d_jobs, n, k0, 3 * q + 2);
         lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, s>>>(d_jobs, n, k0, NB, k0 + NB, k0 + NB,
                                                                                k0 + 2 * NB, 0, 0, 3 * q);
         panel(k0 + NB, s);
       };
-      prepare_pair(0, 0, st, true);
-      lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
+      prepare_pair(0, 0, st, !cta_panel);
+      lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, cta_panel);
       for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
         const int kn = k0 + 2 * NB;
         const bool next = kn < n;
@@ -1872,7 +2123,7 @@ struct Grid {
                                                                                            kn + 2 * NB, 0, 0, q);
           CK(cudaEventRecord(evN, st));
           CK(cudaStreamWaitEvent(sB, evN, 0));
-          panel(kn, sB);
+          panel(kn, sB, cta_panel ? 3 * (q ^ 1) + 2 : -1);
           prepare_pair(kn, q ^ 1, sB, false);
           CK(cudaEventRecord(evP, sB));
         }
@@ -1880,8 +2131,8 @@ struct Grid {
                                 d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
         if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
           CK(cudaStreamWaitEvent(st, evP, 0));
-          snapshot(kn, 3 * (q ^ 1));
-          lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
+          if (!cta_panel) snapshot(kn, 3 * (q ^ 1));
+          lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, cta_panel);
         }
       }
       CK(cudaGetLastError());
@@ -2014,7 +2265,7 @@ struct Grid {
     for (int it = 1; it <= maxiter && !act.empty(); ++it) {
       // inversions of X -> XI (all) and Y -> YI (it > 1): out of place inside G1 (n <= 512),
       // else copy then invert in place
-      const bool oop = n <= 512;
+      const bool oop = use_g1(n);
       if (!oop) {
         if (ew(act, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
         if (it > 1 && ew(act, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
@@ -2623,6 +2874,16 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, i
   CK(cudaMemcpyAsync(products, pr.data(), batch * 4, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return 0;
+}
+
+extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
+#ifdef LGM_PANEL_PROF
+  cudaMemcpyFromSymbol(out, g_panel_cyc, sizeof(g_panel_cyc));
+  return 6;
+#else
+  (void)out;
+  return 0;
+#endif
 }
 
 extern "C" int lgm_debug_grid_phase_ms(double* out, int reset) {

@@ -246,3 +246,12 @@ np.savez({repr(str(tmp_path / 'out.npz'))}, L=L, r=r.view(np.uint8), **out)
     for key, (e, ps) in ests.items():
         assert np.array_equal(o["e" + key], e) and np.array_equal(o["p" + key], ps), key
     assert np.array_equal(o["L"], L1) and o["r"].tobytes() == r1.view(np.uint8).tobytes()
+
+
+@pytest.mark.parametrize("n,B", [(384, 1), (448, 3)])
+def test_logm_grid_g2_small_batches_vs_oracle(n, B):
+    """n % 64 == 0, 256 < n <= 512 inverts on the per-panel G2 path (single-CTA panels,
+    rank-64 combined passes) whatever the batch size: one and three matrices."""
+    A = synth.config(4, batch=B, n=n)
+    L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+    _check(A, L, reps)
