@@ -1018,6 +1018,73 @@ __global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, i
   }
 }
 
+// W1 snapshot + W2 on DMMA (the cta-panel path, n % 64 == 0): CTA = 64 columns of one job,
+// W2[c][j] = M[p2_c][j] + sum_cc A1[p2_c][cc] W1[cc][j] as a 32 x 64 x 32 product (warp w:
+// all 32 rows c, columns 16w..16w+15), W1[cc][j] = M[p1_cc][j] read once (not snapshotted
+// beforehand).  P1 columns: W1 = 0, W2 = A1[p2_c][j - k0]; P2 columns: W2 = 0.
+__global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int n, int k0, int q) {
+  __shared__ __align__(16) double a1s[NB][NB + 4];
+  __shared__ __align__(16) double w1s[NB][64 + 4];
+  __shared__ int p1s[NB], p2s[NB];
+  const InvJob J = jobs[blockIdx.y];
+  if (*J.status) return;
+  double* W1 = wkind(J, 3 * q);
+  double* W2 = wkind(J, 3 * q + 1);
+  const double* A1 = wkind(J, 3 * q + 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int j0 = blockIdx.x * 64;
+  if (tid < NB) p1s[tid] = J.piv[k0 + tid];
+  else if (tid < 2 * NB) p2s[tid - NB] = J.piv[k0 + tid];
+  __syncthreads();
+  for (int idx = tid; idx < NB * NB; idx += 128) {
+    const int c = idx >> 5, cc = idx & 31;
+    a1s[c][cc] = A1[(size_t)p2s[c] * NB + cc];
+  }
+  for (int idx = tid; idx < NB * 32; idx += 128) {  // W1 rows, 16-byte chunks
+    const int cc = idx >> 5, jj = (idx & 31) * 2;
+    const int j = j0 + jj;
+    double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)p1s[cc] * n + j]);
+    if (j >= k0 && j < k0 + NB) v = make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(&w1s[cc][jj]) = v;
+    *reinterpret_cast<double2*>(&W1[(size_t)cc * n + j]) = v;
+  }
+  __syncthreads();
+  const int g8 = lane >> 2, t4 = lane & 3, wc = warp * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)p2s[mi * 8 + g8] * n + j0 + wc + ni * 8 + 2 * t4]);
+      acc[mi][ni][0] = v.x;
+      acc[mi][ni][1] = v.y;
+    }
+#pragma unroll
+  for (int k = 0; k < NB; k += 4) {
+    double a[4], b[2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = a1s[mi * 8 + g8][k + t4];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) b[ni] = w1s[k + t4][wc + ni * 8 + g8];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int c = mi * 8 + g8;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int j = j0 + wc + ni * 8 + 2 * t4;  // j, j + 1 on the same side of 32-aligned bounds
+      double2 v = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      if (j >= k0 && j < k0 + NB) v = make_double2(a1s[c][j - k0], a1s[c][j + 1 - k0]);
+      else if (j >= k0 + NB && j < k0 + 2 * NB) v = make_double2(0.0, 0.0);
+      *reinterpret_cast<double2*>(&W2[(size_t)c * n + j]) = v;
+    }
+  }
+}
+
 template <int RT>  // RT = output tile rows (64: 4 warps, 128: 8 warps); 64 columns
 constexpr size_t up2_smem() { return (size_t)(2 * RT * LDA_S + 2 * TK * LDB_S) * 8; }
 
@@ -2114,7 +2181,8 @@ struct Grid {
         panel(k0 + NB, s);
       };
       prepare_pair(0, 0, st, !cta_panel);
-      lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, cta_panel);
+      if (cta_panel) lgm_count_launch(), gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
+      else lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, 0);
       for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
         const int kn = k0 + 2 * NB;
         const bool next = kn < n;
@@ -2131,8 +2199,12 @@ struct Grid {
                                 d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
         if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
           CK(cudaStreamWaitEvent(st, evP, 0));
-          if (!cta_panel) snapshot(kn, 3 * (q ^ 1));
-          lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, cta_panel);
+          if (cta_panel) {
+            lgm_count_launch(), gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
+          } else {
+            snapshot(kn, 3 * (q ^ 1));
+            lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, 0);
+          }
         }
       }
       CK(cudaGetLastError());
