@@ -578,6 +578,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   __shared__ unsigned wkey32[2][16];
   __shared__ double wval[2][16];
   __shared__ double red[16];
+  __shared__ int piv_s[32];
   const InvJob J = jobs[blockIdx.x];
   if (*J.status) return;  // uniform per CTA
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
     }
   }
   double rowscale = 1.0, mypiv = 1.0;
-  bool piv_here = false;
+  int my_step = -1;  // pivots kept on chip in the loop, published at the end (no live global pointers)
   __syncthreads();
   PP_T(t2);
   PP_ADD(1, t2 - t1);
@@ -683,14 +684,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
       const bool own = (tid == p);
       if (own) {
         used = true;
-        piv_here = true;
         mypiv = r0;
         rowscale = rp;
         double* pw = prow[par];
 #pragma unroll
         for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
-        J.rowstep[tid] = k0 + kk;
-        J.piv[k0 + kk] = tid;
+        my_step = k0 + kk;
+        piv_s[kk] = tid;
       }
       __syncthreads();
       g = own ? 0.0 : r0 * rp;
@@ -704,10 +704,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
     }
     r[31] = last;
   }
+  const bool piv_here = my_step >= 0;
   if (piv_here) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) r[c] *= rowscale;
+    J.rowstep[tid] = my_step;
   }
+  if (tid < nb) J.piv[k0 + tid] = piv_s[tid];
   PP_T(t3);
   PP_ADD(2, t3 - t2);
   if (tiled) {
