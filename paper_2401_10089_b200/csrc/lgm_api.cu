@@ -159,8 +159,15 @@ static bool args_ok(const void* p, int64_t n, int64_t batch, int64_t ld) {
 template <int NMAX, bool FULL>
 static int launch_fused(const double* A, double* L, lgm_report* rep, int64_t ld, int64_t n, int64_t batch, void* ws,
                         const LgmParams& P, cudaStream_t s) {
-  if (prep<NMAX>(logm_fused_kernel<NMAX, FULL>)) return LGM_ERR_CUDA;
-  lgm_count_launch(), logm_fused_kernel<NMAX, FULL><<<(unsigned)batch, Cfg<NMAX>::NT, Cfg<NMAX>::SMEM_BYTES, s>>>(
+  // LGM_F_SMEM=<bytes>: launch with at least that much dynamic shared memory (caps the
+  // resident CTAs per SM; occupancy A/B experiments only)
+  static const size_t sm_bytes = [] {
+    const char* e = std::getenv("LGM_F_SMEM");
+    const size_t want = e ? (size_t)std::atol(e) : 0;
+    return want > Cfg<NMAX>::SMEM_BYTES ? want : Cfg<NMAX>::SMEM_BYTES;
+  }();
+  if (prep<NMAX>(logm_fused_kernel<NMAX, FULL>, sm_bytes)) return LGM_ERR_CUDA;
+  lgm_count_launch(), logm_fused_kernel<NMAX, FULL><<<(unsigned)batch, Cfg<NMAX>::NT, sm_bytes, s>>>(
                           A, L, rep, ld, (int)n, (double*)ws, P);
   return check_launch();
 }

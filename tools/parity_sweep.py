@@ -1,6 +1,6 @@
 """Randomized parity sweep: GPU logm vs the CPU oracle over many sizes / families / seeds.
 
-    python tools/parity_sweep.py [--count 600] [--nmax 160] [--seed 0] [--workers 16]
+    python tools/parity_sweep.py [--count 600] [--nmax 160 | --sizes 320,384,448,512] [--seed 0] [--workers 16]
 
 Families: near-identity (config 2 style), SPD with a wide spectrum, non-normal (3b style),
 known-log.  For each matrix: status / s / k / db_iters / counters classified as in
@@ -67,6 +67,7 @@ def main():
     ap.add_argument("--count", type=int, default=600)
     ap.add_argument("--nmax", type=int, default=160)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--sizes", default=None, help="comma-separated n to draw from (default 1..nmax)")
     ap.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1))
     ap.add_argument("--extreme", action="store_true", help="scaled / ill-conditioned / big-norm / "
                     "Jordan-like / negative-eigenvalue / rotation families")
@@ -76,9 +77,10 @@ def main():
     rng = np.random.default_rng(args.seed)
     fams = (["scaled", "illcond", "bignorm", "jordanish", "negdiag", "rotation"] if args.extreme
             else ["near", "spd", "nonnormal", "knownlog"])
+    sizes = [int(x) for x in args.sizes.split(",")] if args.sizes else None
     cases = []
     for q in range(args.count):
-        n = int(rng.integers(1, args.nmax + 1))
+        n = int(rng.choice(sizes)) if sizes else int(rng.integers(1, args.nmax + 1))
         fam = fams[q % len(fams)]
         cases.append((q, fam, n, make(rng, fam, n)))
     # GPU: group by n
