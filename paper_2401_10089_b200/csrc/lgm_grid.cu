@@ -1510,6 +1510,9 @@ __global__ void est_init_kernel(EstJob* jobs, int n, double rsum) {
 // One thin product for every job still running: step q of the forward (trans=0) or adjoint
 // (trans=1) application.  Forward: q = 0 is M2 (if present), then M1; adjoint: M1^T p1
 // times then M2^T.  src = V[q%2], dst = V[(q+1)%2].
+#ifndef EST_FWD_R
+#define EST_FWD_R 4
+#endif
 __global__ void __launch_bounds__(256) est_fwd_kernel(EstJob* jobs, int n, int q) {
   EstJob& J = jobs[blockIdx.y];
   if (J.done || q >= J.total) return;
@@ -1517,24 +1520,38 @@ __global__ void __launch_bounds__(256) est_fwd_kernel(EstJob* jobs, int n, int q
   const double* x = (q & 1) ? J.V1 : J.V0;
   double* y = (q & 1) ? J.V0 : J.V1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 8 + warp;
-  if (i >= n) return;
+  // EST_FWD_R rows per warp (each row accumulated in the plain lane-strided order): the x
+  // loads are shared by the warp's rows and each lane keeps EST_FWD_R row streams in flight
+  const int i0 = (blockIdx.x * 8 + warp) * EST_FWD_R;
+  if (i0 >= n) return;
   const int nc = J.ncols;
-  double a0 = 0.0, a1 = 0.0;
-  const double* Mr = M + (size_t)i * n;
+  double a0[EST_FWD_R], a1[EST_FWD_R];
+#pragma unroll
+  for (int q = 0; q < EST_FWD_R; ++q) a0[q] = a1[q] = 0.0;
+  const double* Mr = M + (size_t)i0 * n;
+  const int nr = min(EST_FWD_R, n - i0);
   for (int j = lane; j < n; j += 32) {
-    const double m = Mr[j];
-    a0 = fma(m, x[j], a0);
-    if (nc > 1) a1 = fma(m, x[n + j], a1);
+    const double x0 = x[j], x1 = nc > 1 ? x[n + j] : 0.0;
+#pragma unroll
+    for (int q = 0; q < EST_FWD_R; ++q) {
+      if (q < nr) {
+        const double m = Mr[(size_t)q * n + j];
+        a0[q] = fma(m, x0, a0[q]);
+        if (nc > 1) a1[q] = fma(m, x1, a1[q]);
+      }
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-  }
-  if (lane == 0) {
-    y[i] = a0;
-    if (nc > 1) y[n + i] = a1;
+  for (int q = 0; q < EST_FWD_R; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0[q] += __shfl_xor_sync(0xffffffffu, a0[q], o);
+      a1[q] += __shfl_xor_sync(0xffffffffu, a1[q], o);
+    }
+    if (lane == 0 && q < nr) {
+      y[i0 + q] = a0[q];
+      if (nc > 1) y[n + i0 + q] = a1[q];
+    }
   }
 }
 
@@ -1567,6 +1584,51 @@ __global__ void __launch_bounds__(128) est_adj_kernel(EstJob* jobs, int n, int q
   }
   J.part[((size_t)blockIdx.y * 2 + 0) * n + j] = (a0[0] + a0[1]) + (a0[2] + a0[3]);
   J.part[((size_t)blockIdx.y * 2 + 1) * n + j] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+}
+
+// Even n: two adjacent columns per thread (16-byte loads: twice the bytes per request of the
+// kernel above, same per-column accumulation order, so the same partial sums).
+__global__ void __launch_bounds__(128) est_adj2_kernel(EstJob* jobs, int n, int q) {
+  EstJob& J = jobs[blockIdx.z];
+  if (J.done || q >= J.total) return;
+  const double* M = (q < J.p1) ? J.M1 : J.M2;
+  const double* x = (q & 1) ? J.V1 : J.V0;
+  const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int r0 = blockIdx.y * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
+  if (j >= n) return;
+  const bool two = J.ncols > 1;
+  double a0[2][4] = {}, a1[2][4] = {};
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+    double2 m[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m[u] = *reinterpret_cast<const double2*>(&M[(size_t)(r + u) * n + j]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double xa = x[r + u];
+      a0[0][u] = fma(m[u].x, xa, a0[0][u]);
+      a0[1][u] = fma(m[u].y, xa, a0[1][u]);
+      if (two) {
+        const double xb = x[n + r + u];
+        a1[0][u] = fma(m[u].x, xb, a1[0][u]);
+        a1[1][u] = fma(m[u].y, xb, a1[1][u]);
+      }
+    }
+  }
+  for (; r < r1; ++r) {
+    const double2 m = *reinterpret_cast<const double2*>(&M[(size_t)r * n + j]);
+    a0[0][0] = fma(m.x, x[r], a0[0][0]);
+    a0[1][0] = fma(m.y, x[r], a0[1][0]);
+    if (two) {
+      a1[0][0] = fma(m.x, x[n + r], a1[0][0]);
+      a1[1][0] = fma(m.y, x[n + r], a1[1][0]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    J.part[((size_t)blockIdx.y * 2 + 0) * n + j + e] = (a0[e][0] + a0[e][1]) + (a0[e][2] + a0[e][3]);
+    J.part[((size_t)blockIdx.y * 2 + 1) * n + j + e] = (a1[e][0] + a1[e][1]) + (a1[e][2] + a1[e][3]);
+  }
 }
 
 __global__ void est_adj_reduce_kernel(EstJob* jobs, int n, int q, int splits) {
@@ -2269,10 +2331,12 @@ struct Grid {
     } else {
     lgm_count_launch(), est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, rsum);
     for (int sweep = 0; sweep < itmax; ++sweep) {
-      for (int q = 0; q < maxtot; ++q) lgm_count_launch(), est_fwd_kernel<<<dim3((n + 7) / 8, nj), 256, 0, st>>>(d_est, n, q);
+      for (int q = 0; q < maxtot; ++q)
+        lgm_count_launch(), est_fwd_kernel<<<dim3((n + 8 * EST_FWD_R - 1) / (8 * EST_FWD_R), nj), 256, 0, st>>>(d_est, n, q);
       lgm_count_launch(), est_after_fwd_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
       for (int q = 0; q < maxtot; ++q) {
-        lgm_count_launch(), est_adj_kernel<<<dim3((n + 127) / 128, splits, nj), 128, 0, st>>>(d_est, n, q);
+        if ((n & 1) == 0) lgm_count_launch(), est_adj2_kernel<<<dim3((n + 255) / 256, splits, nj), 128, 0, st>>>(d_est, n, q);
+        else lgm_count_launch(), est_adj_kernel<<<dim3((n + 127) / 128, splits, nj), 128, 0, st>>>(d_est, n, q);
         lgm_count_launch(), est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
       }
       lgm_count_launch(), est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
