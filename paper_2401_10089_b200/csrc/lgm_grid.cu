@@ -1266,12 +1266,29 @@ __device__ int pw_leaves(int n, int off, int* loff, int* llen, int cnt) {
   cnt = pw_leaves(n2, off, loff, llen, cnt);
   return pw_leaves(n - n2, off + n2, loff, llen, cnt);
 }
-__device__ double pw_combine(int n, const double* leaf, int& pos) {
-  if (n <= 128) return leaf[pos++];
+// The same recursion flattened once into a post-order program (1 = next leaf, 0 = add the
+// top two: left + right), evaluated without recursion per balancing step.
+__device__ int pw_tokens(int n, signed char* tok, int cnt) {
+  if (n <= 128) { tok[cnt] = 1; return cnt + 1; }
   int n2 = n / 2;
   n2 -= n2 % 8;
-  double a = pw_combine(n2, leaf, pos);
-  return a + pw_combine(n - n2, leaf, pos);
+  cnt = pw_tokens(n2, tok, cnt);
+  cnt = pw_tokens(n - n2, tok, cnt);
+  tok[cnt] = 0;
+  return cnt + 1;
+}
+__device__ __forceinline__ double pw_eval(const signed char* tok, int ntok, const double* leaf) {
+  double st[16];  // depth <= log2(number of leaves) + 1
+  int sp = 0, pos = 0;
+  for (int t = 0; t < ntok; ++t) {
+    if (tok[t]) {
+      st[sp++] = leaf[pos++];
+    } else {
+      const double b = st[--sp];
+      st[sp - 1] = st[sp - 1] + b;
+    }
+  }
+  return st[0];
 }
 __device__ double pw_block(const double* p, size_t stride, int n) {
   if (n < 8) {
@@ -1313,9 +1330,14 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
   __shared__ int loff[128], llen[128];
   __shared__ double lsum[2][128];
   extern __shared__ double lacc_dyn[];  // [2][nleaf * 8] (sized by the host: bal_smem)
-  __shared__ int s_nleaf, s_do;
+  __shared__ int s_nleaf, s_do, s_ntok;
   __shared__ double s_f, s_mm;
-  if (threadIdx.x == 0) { s_nleaf = pw_leaves(n, 0, loff, llen, 0); s_mm = margin[b]; }
+  __shared__ signed char tok[256];
+  if (threadIdx.x == 0) {
+    s_nleaf = pw_leaves(n, 0, loff, llen, 0);
+    s_ntok = pw_tokens(n, tok, 0);
+    s_mm = margin[b];
+  }
   for (int i = threadIdx.x; i < n; i += blockDim.x) sc[i] = 1.0;
   __syncthreads();
   const int nleaf = s_nleaf;
@@ -1366,12 +1388,16 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
         lsum[which][q] = res;
       }
       __syncthreads();
+      // column (lane 0) and row (lane 1) sums combined in the recursion's order, in parallel
+      double cr = 0.0, rr = 0.0;
+      if (threadIdx.x < 2) {
+        cr = pw_eval(tok, s_ntok, lsum[threadIdx.x]);
+        rr = __shfl_sync(0x3u, cr, 1);
+      }
       if (threadIdx.x == 0) {
-        int pos = 0;
         double dg = fabs(B[(size_t)i * n + i]);
-        double c = pw_combine(n, lsum[0], pos) - dg;
-        pos = 0;
-        double r = pw_combine(n, lsum[1], pos) - dg;
+        double c = cr - dg;
+        double r = rr - dg;
         double mm = s_mm;
         int go = 0;
         double f = 1.0;
