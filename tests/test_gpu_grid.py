@@ -255,3 +255,21 @@ def test_logm_grid_g2_small_batches_vs_oracle(n, B):
     A = synth.config(4, batch=B, n=n)
     L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
     _check(A, L, reps)
+
+
+def test_sqrt_db_g2_small_failures():
+    """The G2 single-CTA-panel path (n = 320): a zero row is singular at the first step, an
+    eigenvalue on the negative axis does not converge (as in the reference), and a healthy
+    matrix in the same batch is unaffected."""
+    n = 320
+    rng = np.random.default_rng(3)
+    G = rng.standard_normal((n, n))
+    good = np.eye(n) + 0.5 * G / np.linalg.norm(G, 2)
+    zero_row = good.copy()
+    zero_row[11, :] = 0.0
+    neg = np.diag(np.r_[-1.0, np.linspace(2.0, 3.0, n - 1)])
+    X, its, st = lp.sqrt_db_batched(np.stack([good, zero_row, neg]))
+    assert list(st) == [0, 1, 2]
+    assert its[1] == 0 and its[2] == 50
+    Xo, ito = P.sqrt_db(good)
+    assert its[0] == ito and rel_err(X[0], Xo) <= 1e-12
