@@ -2095,6 +2095,7 @@ struct Grid {
   }
   double* d_logdet = nullptr; // [2][batch]
   int* d_istat = nullptr;     // [2][batch]
+  std::vector<InvJob> jobs_up;  // host copy of the job table last uploaded to d_jobs
   InvJob* d_jobs = nullptr;   // [2*batch]
   double* d_scal = nullptr;   // [batch] scratch doubles
   double* d_scal2 = nullptr;
@@ -2201,7 +2202,12 @@ struct Grid {
       J.logdet = d_logdet + w * batch + b;
       J.status = d_istat + w * batch + b;
     }
-    CK(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(InvJob), cudaMemcpyHostToDevice, st));
+    // the job table only changes with the active set: skip the (pageable, host-blocking)
+    // re-upload between DB steps when it is byte-identical to the last one
+    if (jobs_up.size() != jobs.size() || std::memcmp(jobs_up.data(), jobs.data(), nj * sizeof(InvJob)) != 0) {
+      CK(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(InvJob), cudaMemcpyHostToDevice, st));
+      jobs_up = jobs;
+    }
     if (use_g1(n)) {  // G1: one CTA per inversion, no per-panel launches
       if (n <= 128) return launch_g1<128>(nj);
       if (n <= 256) return launch_g1<256>(nj);
