@@ -2149,10 +2149,11 @@ struct Grid {
     d_step = (int*)take(2 * (size_t)batch * n * 4);
     d_W = (double*)take(12 * (size_t)batch * NB * n * 8);
     d_logdet = (double*)take(2 * batch * 8);
-    d_istat = (int*)take(2 * batch * 4);
-    d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
+    // d_scal, d_scal2, d_istat adjacent: the DB step reads all three back in one copy
     d_scal = (double*)take(batch * 8);
     d_scal2 = (double*)take(batch * 8);
+    d_istat = (int*)take(2 * batch * 4);
+    d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
     d_iflag = (int*)take(batch * 4);
     d_scaling = (int*)take(batch * 4);
     d_scale = (double*)take((size_t)batch * n * 8);
@@ -2482,12 +2483,17 @@ struct Grid {
       PhaseTimer pt(PH_DBUPD, st);
       lgm_count_launch(), db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
       CK(cudaGetLastError());
+      // change, size and the singular flags in one device-to-host copy (adjacent in the carve)
+      const char* span0 = (const char*)d_scal;
+      const size_t span = (size_t)((const char*)(d_istat + 2 * batch) - span0);
+      std::vector<char> rb(span);
+      CK(cudaMemcpyAsync(rb.data(), span0, span, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
       std::vector<double> ch(batch), sz(batch);
       std::vector<int> ist(2 * batch);
-      CK(cudaMemcpyAsync(ch.data(), d_scal, batch * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(sz.data(), d_scal2, batch * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(ist.data(), d_istat, 2 * batch * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      std::memcpy(ch.data(), rb.data(), batch * 8);
+      std::memcpy(sz.data(), rb.data() + ((const char*)d_scal2 - span0), batch * 8);
+      std::memcpy(ist.data(), rb.data() + ((const char*)d_istat - span0), 2 * batch * 4);
       std::vector<int> next;
       for (int b : act) {
         iters[b] = it;
