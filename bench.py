@@ -1,15 +1,17 @@
 """Benchmark: batched FP64 logm throughput (matrices/s) on B200, BASELINE.json's metric.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
 One *step* = one pass of the whole logm hot path (balance -> scaling loop with norm
 estimation and DB square roots -> order selection -> graph polynomial -> 2^s rescale ->
 unbalance) over one batch of matrices already resident in HBM.  Default workload is
-BASELINE.json configs[1] (config 2: 4096 float64 32x32 near-identity matrices per GPU,
-weak scaling: each rank owns its own 4096-matrix shard, no data-path collective).
+BASELINE.json configs[3] (config 4: 256 float64 SPD 512x512 matrices, the largest
+single-GPU configuration and north_star's n >= 512 roofline regime), strong scaling: the
+256-matrix global batch is split by matrix across the ranks, no data-path collective, and
+the result gather to rank 0 (NCCL) is inside the timed region.
 Under torchrun each rank drives one GPU; timings are CUDA events on the launching
 stream, the max over ranks is reported.  The L2 (126 MB) is flushed between timed steps
-(256 MiB write) since the config-2 batch (32 MiB) would otherwise stay L2 resident.
+(256 MiB write) so small batches (config 2: 32 MiB) do not stay L2 resident.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the oracle port
 of the reference primitives + restated driver, oracle/; the reference's own driver file
@@ -201,12 +203,13 @@ def host_cores():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="2")
-    ap.add_argument("--batch", type=int, default=None, help="matrices per GPU (default: the config's)")
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--batch", type=int, default=None, help="GLOBAL matrices (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
     args = ap.parse_args()
     cfg = args.config if args.config in ("3b", "5b") else int(args.config)
@@ -223,23 +226,31 @@ def main():
     import torch.distributed as dist
     import paper_2401_10089_b200 as lp
     from paper_2401_10089_b200 import _lib, driver
+    from paper_2401_10089_b200.multigpu import gather_tensor_to, shard_bounds
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    A_np, name = workload(cfg, batch=args.batch, seed_offset=rank)
-    B, n, _ = A_np.shape
+    # strong scaling: the config's GLOBAL batch (config 4: 256 matrices) split by matrix
+    # across the ranks; results gathered to rank 0 inside the timed region
+    A_all, name = workload(cfg, batch=args.batch)
+    Bg, n, _ = A_all.shape
+    lo, hi = shard_bounds(Bg, world)[rank]
+    A_np = np.ascontiguousarray(A_all[lo:hi])
+    B = A_np.shape[0]
     A = torch.from_numpy(A_np).to(dev)
     opts = lp.LogmOptions(raise_on_error=False)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
     def step():
-        return driver.run_device(A, opts, stream)
+        L, rep, ws = driver.run_device(A, opts, stream)
+        Lg = gather_tensor_to(L, rank, world, Bg)          # result gather (NCCL), no-op at N = 1
+        return L, rep, Lg
 
     for _ in range(args.warmup):
-        L, rep, ws = step()
+        L, rep, _ = step()
     torch.cuda.synchronize()
     reps = rep.cpu().numpy().view(_lib.REPORT_DTYPE)[:B]
 
@@ -257,50 +268,56 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            L, rep, ws = step()
+            step()
             e1.record(stream)
             times.append((e0, e1))
         barrier()
     launches = _lib.launch_count() - launches0
     kernel_ms = [a.elapsed_time(b) for a, b in times]
-    total_ms = sum(kernel_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(kernel_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * B * args.steps / (total_ms * 1e-3)
+    value = Bg * args.steps / (total_ms * 1e-3)
 
-    # roofline of the dominant (only) kernel: algorithmic FLOPs per launch / launch time
-    F = sum(flops_per_matrix(n, r) for r in reps)
+    # roofline: algorithmic FLOPs of one step (all ranks' matrices) / step time (max over ranks)
+    Fl = torch.tensor([sum(flops_per_matrix(n, r) for r in reps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(Fl)
+    F = float(Fl.item())
     peak, peak_src = _peak_fp64()
-    avg_launch_s = (sum(kernel_ms) / len(kernel_ms)) * 1e-3
-    achieved = F / avg_launch_s / 1e12
+    step_s = ms_per_step * 1e-3
+    achieved = F / step_s / 1e12
     hbm_peak, hbm_src = _peak_hbm()
-    alg_bytes = B * (16.0 * n * n + _lib.REPORT_DTYPE.itemsize)
-    traffic = None
+    alg_bytes = Bg * (16.0 * n * n + _lib.REPORT_DTYPE.itemsize)
+    traffic, kernel_share = None, None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")))
-        traffic = tr.get(str(args.config), {}).get("dram_bytes_per_launch")
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")))
+        ent = tr.get(str(args.config), {})
+        traffic = ent.get("dram_bytes_per_step")
+        kernel_share = ent.get("kernel_share")
     except Exception:  # noqa: BLE001
         pass
 
-    # end-to-end through the public API with host (pinned) buffers
-    A_host = torch.from_numpy(A_np).pin_memory()
-    L_host = torch.empty_like(A_host).pin_memory()      # the caller's reusable output buffer
-    for _ in range(2):
-        lp.logm_batched(A_host, opts, out=L_host)
-    e2e_times = []
-    for _ in range(max(3, min(args.steps, 20))):
-        barrier()
-        t0 = time.perf_counter()
-        Lh, rh = lp.logm_batched(A_host, opts, out=L_host)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_s = sum(e2e_times) / len(e2e_times)
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B / float(te.item())
+    # end-to-end through the public API with host (pinned) buffers: H2D of this rank's inputs,
+    # the whole logm, D2H of L and the reports, every step
+    e2e_value = None
+    if not args.no_e2e:
+        A_host = torch.from_numpy(A_np).pin_memory()
+        L_host = torch.empty_like(A_host).pin_memory()      # the caller's reusable output buffer
+        for _ in range(2):
+            lp.logm_batched(A_host, opts, out=L_host)
+        e2e_times = []
+        for _ in range(max(3, min(args.steps, 10))):
+            barrier()
+            t0 = time.perf_counter()
+            lp.logm_batched(A_host, opts, out=L_host)
+            e2e_times.append(time.perf_counter() - t0)
+        te = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_value = Bg / float(te.item())
 
     if rank != 0:
         if world > 1:
@@ -320,26 +337,29 @@ def main():
                          f"{secs:.2f} s wall"}
 
     status_counts = {int(s): int(c) for s, c in zip(*np.unique(reps["status"], return_counts=True))}
+    engine = "F (fused, 1 CTA/matrix)" if n <= 64 else "G (batched grid, device-driven)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy generator, synth.py)",
-        "config": {"workload": f"config{args.config}:{name}", "n": n, "batch_per_gpu": B,
-                   "global_batch": B * world, "parallelism": f"batch-sharded x{world} (no collective)",
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "engine": "F (fused, 1 CTA/matrix)" if n <= 64 else "G (batched grid)"},
+        "config": {"workload": f"config{args.config}:{name}", "n": n, "global_batch": Bg,
+                   "batch_per_gpu": B, "parallelism": f"batch-sharded x{world} (no collective; result gather "
+                                                      f"to rank 0 inside the timed region)",
+                   "l2": "flushed between timed steps (256 MiB write)", "engine": engine},
         "achieved_tflops": achieved,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": ("logm_fused_kernel<32>" if n <= 32 else "logm_fused_kernel<64>") if n <= 64
-                     else "whole Engine-G step (gj_inv_cta_kernel dominant; achieved = step FLOPs / step time)",
-                     "alg_flops_per_launch": F,
-                     "hbm": {"achieved_gbs": alg_bytes / avg_launch_s / 1e9, "peak_gbs": hbm_peak,
-                             "frac": alg_bytes / avg_launch_s / 1e9 / hbm_peak, "alg_bytes_per_launch": alg_bytes,
+                     else "whole Engine-G logm step (achieved = step algorithmic FLOPs / step time)",
+                     "kernel_share": kernel_share,
+                     "alg_flops_per_step": F,
+                     "hbm": {"achieved_gbs": alg_bytes / step_s / 1e9, "peak_gbs": hbm_peak,
+                             "frac": alg_bytes / step_s / 1e9 / hbm_peak, "alg_bytes_per_step": alg_bytes,
                              "peak_source": hbm_src}},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * n * n * 8),
-                "d2h_bytes_per_step": int(B * n * n * 8 + B * _lib.REPORT_DTYPE.itemsize)},
+        "e2e": None if e2e_value is None else
+        {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(B * n * n * 8),
+         "d2h_bytes_per_step": int(B * n * n * 8 + B * _lib.REPORT_DTYPE.itemsize)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "report_summary": {"status_counts": status_counts, "s_mean": float(reps["s"].mean()),
@@ -362,21 +382,33 @@ def run_reference(args, cfg, rank, world):
     sample = args.cpu_sample or (256 if n <= 64 else min(B, 4 * cores) if n <= 256 else
                                  min(B, cores) if n <= 1024 else 1)
     sample = min(sample, B)
-    for _ in range(min(args.warmup, 1)):
-        cpu_time(A_np[:min(sample, cores if cpu_mode(n) == "pool" else 1)], cores)
+    # one persistent pool (or one all-core-BLAS child) for the whole run; warm-up steps first
+    pool_mode = cpu_mode(n) == "pool"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1" if pool_mode else str(cores)
+    ctx = mp.get_context("spawn")
+    procs = cores if pool_mode else 1
+    init, iargs = (_cpu_worker_init, ()) if pool_mode else (_cpu_serial_init, (cores,))
     secs = []
-    for s in range(args.steps):
-        lo = (s * sample) % B
-        chunk = A_np[lo:lo + sample] if lo + sample <= B else A_np[:sample]
-        secs.append(cpu_time(chunk, cores))
+    with ctx.Pool(procs, initializer=init, initargs=iargs) as pool:
+        def one_step(chunk):
+            parts = [c for c in np.array_split(chunk, max(1, min(len(chunk), procs * 4))) if len(c)]
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, parts, chunksize=1)
+            return time.perf_counter() - t0
+        for _ in range(min(args.warmup, 1)):
+            one_step(A_np[:min(sample, procs)])
+        for s in range(args.steps):
+            lo = (s * sample) % B
+            chunk = A_np[lo:lo + sample] if lo + sample <= B else A_np[:sample]
+            secs.append(one_step(chunk))
     total = sum(secs)
     value = sample * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded numpy generator, synth.py)",
-        "config": {"workload": f"config{args.config}:{name}", "n": n, "batch_per_gpu": B},
+        "config": {"workload": f"config{args.config}:{name}", "n": n, "global_batch": B},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{sample} matrices of config {args.config} per step, oracle port "
                                    f"(oracle/driver.py: restated driver over the numpy/scipy restatement of the "

@@ -1128,8 +1128,14 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
   c.zero_all();
   __syncthreads();
   c.init_ramp();
+  // a failed matrix gets an all-NaN L: a caller ignoring the status never reads stale data
+  auto fail_fill = [&]() {
+    for (int i = c.warp; i < n; i += Cfg<NMAX>::NT / 32)
+      for (int j = c.lane; j < n; j += 32) Lg[(long long)i * ld + j] = __longlong_as_double(0x7ff8000000000000LL);
+  };
   if (c.load(BUF_B, Ag, ld)) {
     R.status = LGM_NONFINITE;
+    fail_fill();
     if (c.tid == 0) *rep = R;
     return;
   }
@@ -1219,6 +1225,7 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
     R.status = status ? status : LGM_SCALING_MAXITER;
     R.min_margin = c.mm;
     R.db_plateau = c.plateau;
+    fail_fill();
     if (c.tid == 0) *rep = R;
     return;
   }

@@ -31,9 +31,8 @@ namespace {
 enum { PH_BALANCE = 0, PH_ALPHA, PH_INVERT, PH_DBUPD, PH_SELECT, PH_POLY, PH_OTHER, PH_N };
 double g_phase_ms[PH_N];
 bool prof_on() {
-  static int on = -1;
-  if (on < 0) on = std::getenv("LGM_GRID_PROFILE") ? 1 : 0;
-  return on == 1;
+  static const bool on = std::getenv("LGM_GRID_PROFILE") != nullptr;  // thread-safe once-init
+  return on;
 }
 struct PhaseTimer {
   int ph;
@@ -71,23 +70,21 @@ enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7 };
 // at n = 128 G1 (57 ms) beats G2 (81 ms).  By n only, so a matrix's arithmetic does not depend
 // on the batch it is in.  LGM_G1_MAXN=<m> overrides: G1 exactly for n <= m (m <= 512).
 bool use_g1(int n) {
-  static int v = -2;
-  if (v == -2) {
+  static const int v = [] {  // thread-safe once-init
     const char* e = std::getenv("LGM_G1_MAXN");
-    v = e ? std::min(512, std::max(0, std::atoi(e))) : -1;
-  }
+    return e ? std::min(512, std::max(0, std::atoi(e))) : -1;
+  }();
   if (v >= 0) return n <= v;
   return n <= 256 || (n <= 512 && n % 64 != 0);
 }
 
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
-  static int on = -1;
-  if (on < 0) {
+  static const bool on = [] {  // thread-safe once-init
     const char* e = std::getenv("LGM_EST_FUSED");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 __device__ __forceinline__ uint64_t dkey(double nonneg) { return (uint64_t)__double_as_longlong(nonneg) + 1ull; }
@@ -2069,6 +2066,15 @@ __global__ void store_kernel(Slots S, const int* ids, int k, double* out, long l
   }
 }
 
+// L of a failed matrix: all NaN (a caller ignoring the status never reads stale data)
+__global__ void nan_fill_kernel(const int* ids, int n, double* out, long long ld) {
+  const int b = ids[blockIdx.y];
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
+    int i = idx / n, j = idx - (size_t)i * n;
+    out[(size_t)b * n * ld + (size_t)i * ld + j] = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Host side
 double host_pairwise_abs_ramp(int n) {
@@ -2217,15 +2223,12 @@ struct Grid {
     lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
     const int tiles = (n + TM - 1) / TM;
     const bool cta_panel = n <= 512;  // one CTA per panel (writes A1 itself: no gj_copy_a1_kernel)
+    // dynamic shared memory limits are per device: set them on every call (no process-wide flag)
+    if (n <= 128) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 33 * 8));
+    else if (n <= 256) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 33 * 8));
+    else if (n <= 512) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 32 * 33 * 8));
     auto panel = [&](int k0, cudaStream_t s, int a1_kind = -1, int s1_a1kind = -1) {
       const int nb = std::min(NB, n - k0);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(gj_panel_cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 33 * 8);
-        cudaFuncSetAttribute(gj_panel_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 33 * 8);
-        cudaFuncSetAttribute(gj_panel_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 32 * 33 * 8);
-        attr = true;
-      }
       if (n <= 128) {  // many small jobs: one CTA per inversion, no cluster
         lgm_count_launch(), gj_panel_cta_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
       } else if (n <= 256) {
@@ -2259,9 +2262,9 @@ struct Grid {
       const char* e = std::getenv("LGM_G2_RANK64");
       return !(e && e[0] == '0');
     }();
-    // few large jobs: the exposed P2 panel costs more than the second pass (n > 512 only: for
-    // n <= 512 the choice stays independent of the batch)
-    const bool use64 = rank64 && n % (2 * NB) == 0 && (nj >= 4 || n <= 512);
+    // rank-64 vs rank-32 passes round differently: the choice depends on n only, so a
+    // matrix's arithmetic never depends on its batch-mates or on how many have converged
+    const bool use64 = rank64 && n % (2 * NB) == 0;
     panel(0, st, use64 && cta_panel ? 2 : -1);
     if (use64) {
       // rank-64 delayed update with both panels of the next pair factored on sB during the
@@ -2867,6 +2870,16 @@ int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int6
     // the k / products / alpha of the run that produced it
     for (int b : grp)
       if (nf[b]) { ms[b].status = LGM_NONFINITE; ms[b].post_fail = true; }
+  }
+  {
+    std::vector<int> failed;
+    for (int b = 0; b < batch; ++b)
+      if (ms[b].status && !ms[b].post_fail) failed.push_back(b);
+    if (!failed.empty()) {
+      if (G.upload_ids(failed)) return LGM_ERR_CUDA;
+      lgm_count_launch(), nan_fill_kernel<<<G.ew_grid((int)failed.size()), 256, 0, st>>>(G.d_ids, n, L, ld);
+      CK(cudaGetLastError());
+    }
   }
   // reports
   std::vector<lgm_report> R(batch);

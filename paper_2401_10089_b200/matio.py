@@ -1,80 +1,103 @@
-"""Plain-text matrix I/O in the reference's format (``logmpoly/matcore.py:362-431``).
+"""Plain-text matrix files, byte-compatible with the reference's serializer.
 
-Format: first non-comment line holds n, then n rows of n whitespace-separated scalars;
-blank lines and lines starting with ``#`` are ignored.  Reals are written with 17
-significant digits (``%.17g``, round-trip exact); complex entries as ``re+imi``.  Malformed
-input raises ``SchemeFormatError`` (a ``ValueError``), as in the reference.
+Written from the format statement in SPEC.md:125 (the reference implements it in
+``logmpoly/matcore.py:362-431``): a size line ``n``, then ``n`` lines of ``n``
+whitespace-separated decimal scalars; a complex scalar is one token ``<re><sign><im>i``;
+reals carry 17 significant digits so every double round-trips exactly.  Lines that are
+blank or whose first non-blank character is ``#`` carry no data.  Byte equality with the
+reference's writer is pinned by ``tests/golden/matio_ref*.txt``.
+
+Grammar used by the reader (one token)::
+
+    real    := python float literal (what ``float()`` accepts)
+    complex := NUM SIGN UNUM "i"        NUM = [sign] digits[.digits][e[sign]digits]
+
+Anything else -- or a file whose row / column counts disagree with its size line -- raises
+``SchemeFormatError`` (a ``ValueError``); non-finite values are rejected like ``as_square``.
 """
+import re
+
 import numpy as np
 
 from .exceptions import SchemeFormatError
 
+_UNUM = r"(?:\d+(?:\.\d*)?|\.\d+)(?:[eE][+-]?\d+)?"
+_COMPLEX = re.compile(rf"^(?P<re>[+-]?{_UNUM})(?P<im>[+-]{_UNUM})[iI]$")
 
-def _fmt(x):
-    if np.iscomplexobj(x):
+
+def _text_of(x, is_complex):
+    if is_complex:
         z = complex(x)
-        return f"{z.real:.17g}{z.imag:+.17g}i"
-    return f"{float(x):.17g}"
+        return "%.17g%+.17gi" % (z.real, z.imag)
+    return "%.17g" % float(x)
 
 
-def _token(tok):
-    t = tok.strip()
-    if t[-1:] in ("i", "I"):
-        body = t[:-1]
-        # the imaginary part starts at the last sign that is not an exponent sign
-        cut = next((k for k in range(len(body) - 1, 0, -1) if body[k] in "+-" and body[k - 1] not in "eE"), -1)
-        if cut <= 0:
-            raise SchemeFormatError(f"malformed complex token: {tok!r}")
-        try:
-            return complex(float(body[:cut]), float(body[cut:]))
-        except ValueError as exc:
-            raise SchemeFormatError(f"malformed complex token: {tok!r}") from exc
+def _value_of(token):
+    if token[-1] in "iI":
+        m = _COMPLEX.match(token)
+        if m is None:
+            raise SchemeFormatError(f"cannot read complex scalar {token!r}")
+        return complex(float(m.group("re")), float(m.group("im")))
     try:
-        return float(t)
-    except ValueError as exc:
-        raise SchemeFormatError(f"malformed scalar token: {tok!r}") from exc
+        return float(token)
+    except ValueError:
+        raise SchemeFormatError(f"cannot read scalar {token!r}") from None
 
 
-def _square(A):
-    A = np.asarray(A)
-    if A.ndim != 2 or A.shape[0] != A.shape[1] or A.shape[0] < 1:
-        raise ValueError(f"matrix must be square, got shape {A.shape}")
-    if not np.all(np.isfinite(A)):
+def _checked(M):
+    M = np.asarray(M)
+    if M.ndim != 2 or M.shape[0] < 1 or M.shape[0] != M.shape[1]:
+        raise ValueError(f"matrix must be square, got shape {M.shape}")
+    if not np.isfinite(M).all():
         raise ValueError("matrix has non-finite entries")
-    return A.astype(np.complex128 if np.iscomplexobj(A) else np.float64)
+    return M.astype(np.complex128) if np.iscomplexobj(M) else M.astype(np.float64)
 
 
 def format_matrix(A):
-    """Text form of a square matrix (matcore.py:393-401)."""
-    A = _square(A)
-    rows = [" ".join(_fmt(x) for x in row) for row in A]
-    return "\n".join([str(A.shape[0])] + rows) + "\n"
+    """Serialize one square matrix (size line, then one line per row, trailing newline)."""
+    M = _checked(A)
+    cplx = np.iscomplexobj(M)
+    out = [f"{M.shape[0]}"]
+    out.extend(" ".join(_text_of(v, cplx) for v in row) for row in M)
+    out.append("")
+    return "\n".join(out)
+
+
+def _data_lines(text):
+    for raw in text.splitlines():
+        s = raw.strip()
+        if s and not s.startswith("#"):
+            yield s
 
 
 def parse_matrix(text):
-    """Inverse of ``format_matrix`` (matcore.py:404-421)."""
-    lines = [ln for ln in text.splitlines() if ln.strip() and not ln.lstrip().startswith("#")]
-    if not lines:
-        raise SchemeFormatError("empty matrix file")
-    try:
-        n = int(lines[0].strip())
-    except ValueError as exc:
-        raise SchemeFormatError(f"bad dimension line: {lines[0]!r}") from exc
-    if n < 1 or len(lines) < n + 1:
-        raise SchemeFormatError(f"expected {n} rows, found {len(lines) - 1}")
-    rows = []
-    for ln in lines[1:n + 1]:
-        toks = ln.split()
+    """Read the text form back (inverse of ``format_matrix``; exact for doubles)."""
+    lines = _data_lines(text)
+    head = next(lines, None)
+    if head is None:
+        raise SchemeFormatError("no data in matrix text")
+    if not head.isdigit():
+        raise SchemeFormatError(f"first data line must be the size n, got {head!r}")
+    n = int(head)
+    if n == 0:
+        raise SchemeFormatError("matrix size must be at least 1")
+    entries = []
+    for r in range(n):
+        line = next(lines, None)
+        if line is None:
+            raise SchemeFormatError(f"size line says {n} rows, text ends after {r}")
+        toks = line.split()
         if len(toks) != n:
-            raise SchemeFormatError(f"expected {n} entries per row, got {len(toks)}")
-        rows.append([_token(t) for t in toks])
-    vals = np.array(rows)
-    return _square(vals if np.iscomplexobj(vals) else vals.astype(np.float64))
+            raise SchemeFormatError(f"row {r} has {len(toks)} entries, size line says {n}")
+        entries.append([_value_of(t) for t in toks])
+    vals = np.array(entries)
+    return _checked(vals)
 
 
 def write_matrix(path, A):
+    text = format_matrix(A)
     with open(path, "w") as fh:
-        fh.write(format_matrix(A))
+        fh.write(text)
 
 
 def read_matrix(path):

@@ -49,3 +49,30 @@ def run_sharded(A, rank, world, compute, dst=0, group=None):
     chunk, _ = local_shard(A, rank, world)
     L, R = compute(chunk)
     return gather_to(L, R, rank, world, dst=dst, group=group)
+
+
+def gather_tensor_to(local, rank, world, global_batch, dst=0, group=None):
+    """Tensor gather of per-rank (b_r, ...) chunks to one (global_batch, ...) tensor on
+    ``dst`` (rank order, contiguous shards as ``shard_bounds``).  Chunks are padded to the
+    largest shard so one ``dist.gather`` moves them (NCCL over NVLink, or gloo); returns the
+    gathered tensor on dst, None elsewhere.  world == 1 returns ``local`` unchanged."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return local
+    bounds = shard_bounds(global_batch, world)
+    cap = max(hi - lo for lo, hi in bounds)
+    lo, hi = bounds[rank]
+    if local.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} holds {local.shape[0]} items, shard is {hi - lo}")
+    if local.shape[0] == cap:
+        send = local.contiguous()
+    else:
+        send = torch.zeros((cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        send[:local.shape[0]] = local
+    bufs = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
+    dist.gather(send, bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([bufs[r][:hi_ - lo_] for r, (lo_, hi_) in enumerate(bounds)])

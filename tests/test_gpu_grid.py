@@ -5,7 +5,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.parity import classify, rel_err, tolerance
+from tests.parity import check_batch, rel_err, tolerance
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -116,19 +116,8 @@ def test_sqrt_db_grid_failures():
 
 
 def _check(As, L, reps, allow_mismatch=0):
-    counts = {"match": 0, "exempt": 0, "db_plateau": 0, "mismatch": 0}
-    for b in range(As.shape[0]):
-        Lr, rr = D.logm_status(As[b], D.default_prims())
-        cls, g, o = classify(reps[b], rr)
-        counts[cls] += 1
-        if cls == "mismatch":
-            print("MISMATCH", b, g, o, float(reps[b]["min_margin"]), rr["min_margin"])
-        both_ok = rr["status"] == 0 and int(reps[b]["status"]) == 0
-        if both_ok and (cls == "match" or (cls == "db_plateau" and (g["s"], g["k"]) == (o["s"], o["k"]))):
-            e, tol = rel_err(L[b], Lr), tolerance(As[b], Lr)
-            assert e <= tol, (b, e, tol)
-    print(counts)
-    assert counts["mismatch"] <= allow_mismatch, counts
+    counts, _ = check_batch(As, L, reps, allow_mismatch)
+    return counts
 
 
 @pytest.mark.parametrize("c,n,B", [("3b", 96, 6), (4, 80, 4), ("3b", 128, 4), (2, 100, 6), (3, 72, 2)])

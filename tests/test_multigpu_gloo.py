@@ -67,3 +67,30 @@ def test_two_rank_gloo_shard_and_gather(tmp_path):
     L1, R1 = _oracle_compute(A)
     assert np.array_equal(got["L"], L1)
     assert np.array_equal(got["R"], R1)
+
+
+def _tensor_worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+    from paper_2401_10089_b200.multigpu import gather_tensor_to, shard_bounds as sb
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    G = 7                                             # unequal shards: 3 + 4
+    full = torch.arange(G * 4, dtype=torch.float64).view(G, 2, 2)
+    lo, hi = sb(G, world)[rank]
+    got = gather_tensor_to(full[lo:hi].clone(), rank, world, G)
+    if rank == 0:
+        torch.save(got, out_path)
+    else:
+        assert got is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_tensor_gather_unequal_shards(tmp_path):
+    import torch
+    out = str(tmp_path / "t.pt")
+    tmp.spawn(_tensor_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = torch.load(out)
+    assert torch.equal(got, torch.arange(28, dtype=torch.float64).view(7, 2, 2))
