@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
   unsigned* wkey32 = reinterpret_cast<unsigned*>(wkey);     // [2][16] per-warp best key
 
   const InvJob J = jobs[blockIdx.x];
+  if (!J.M) return;  // unused slot of the device-built job table
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   double* M = J.M;
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
 
 __global__ void gj_init_kernel(const InvJob* jobs, int n) {
   const InvJob J = jobs[blockIdx.y];
+  if (!J.M) return;  // unused slot of the device-built job table (its status reads 1)
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) J.rowstep[i] = -1;
   if (blockIdx.x == 0 && threadIdx.x == 0) { *J.logdet = 0.0; *J.status = 0; }
 }
@@ -1194,29 +1196,43 @@ struct Slots {
   __device__ __host__ double* buf(int b, int k) const { return ws + ((size_t)b * NBUF + k) * (size_t)n * n; }
 };
 
-__global__ void load_kernel(const double* A, long long ld, Slots S, const int* ids, int* bad) {
-  const int b = ids[blockIdx.y];
+// Device-built matrix lists: ids[0 .. *cnt) (ascending matrix indices), capacity = batch.
+// The list kernels below stride over (entry, element) with a grid sized for the device, so a
+// short or empty list costs one small launch whatever the capacity.
+struct DList {
+  const int* ids;
+  const int* cnt;
+};
+constexpr int EW_BLOCKS = 148 * 8;  // grid of the element-wise list kernels
+
+#define LIST_LOOP(L, nn)                                                                                    \
+  const size_t per_ = (nn);                                                                                \
+  const size_t tot_ = (size_t)(*(L).cnt) * per_;                                                           \
+  for (size_t g_ = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g_ < tot_; g_ += (size_t)gridDim.x * blockDim.x) { \
+    const int e_ = (int)(g_ / per_);                                                                       \
+    const size_t idx = g_ - (size_t)e_ * per_;                                                             \
+    const int b = (L).ids[e_];
+
+__global__ void load_kernel(const double* const* Ap, const long long* ldp, Slots S, DList L, int* bad) {
   const int n = S.n;
-  double* B = S.buf(b, G_B);
-  bool nf = false;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
+  const double* A = *Ap;
+  const long long ld = *ldp;
+  LIST_LOOP(L, (size_t)n * n)
     int i = idx / n, j = idx - (size_t)i * n;
     double v = A[(size_t)b * n * ld + (size_t)i * ld + j];
-    nf |= !isfinite(v);
-    B[idx] = v;
+    S.buf(b, G_B)[idx] = v;
+    if (!isfinite(v)) bad[b] = 1;
   }
-  if (__syncthreads_or(nf) && threadIdx.x == 0) bad[b] = 1;
 }
 
 // dst = src - I (op 0), copy (op 1), identity (op 2), dst = src - 2*src2 + I (op 3, A_I2),
 // dst = I - src (op 4)
-__global__ void ew_kernel(Slots S, const int* ids, int op, int dk, int sk, int s2k) {
-  const int b = ids[blockIdx.y];
+__global__ void ew_kernel(Slots S, DList L, int op, int dk, int sk, int s2k) {
   const int n = S.n;
-  double* D = S.buf(b, dk);
-  const double* X = S.buf(b, sk);
-  const double* X2 = S.buf(b, s2k);
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
+  LIST_LOOP(L, (size_t)n * n)
+    double* D = S.buf(b, dk);
+    const double* X = S.buf(b, sk);
+    const double* X2 = S.buf(b, s2k);
     int i = idx / n, j = idx - (size_t)i * n;
     double v;
     switch (op) {
@@ -1230,27 +1246,17 @@ __global__ void ew_kernel(Slots S, const int* ids, int op, int dk, int sk, int s
   }
 }
 
-// onenorm exactly as numpy (column sums accumulated over rows in order), max via atomicMax.
-__global__ void onenorm_kernel(Slots S, const int* ids, int k, double* out) {
-  const int b = ids[blockIdx.y];
+// onenorm exactly as numpy (column sums accumulated over rows in order), max via atomicMax
+// into out[b] (zeroed beforehand).
+__global__ void onenorm_kernel(Slots S, DList L, int k, double* out) {
   const int n = S.n;
-  const double* M = S.buf(b, k);
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) {
+  LIST_LOOP(L, (size_t)n)
+    const double* M = S.buf(b, k);
+    const int j = (int)idx;
     double acc = 0.0;
     for (int i = 0; i < n; ++i) acc = (i == 0) ? fabs(M[(size_t)i * n + j]) : acc + fabs(M[(size_t)i * n + j]);
     atomic_max_nonneg(&out[b], acc);
   }
-}
-
-__global__ void any_nonzero_kernel(Slots S, const int* ids, int k, int* out) {
-  const int b = ids[blockIdx.y];
-  const int n = S.n;
-  const double* M = S.buf(b, k);
-  bool nz = false;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x)
-    nz |= M[idx] != 0.0;
-  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&out[b], 1);
 }
 
 // numpy pairwise sum (n < 8: sequential; n <= 128: 8 accumulators; else split n/2 - (n/2)%8)
@@ -1318,9 +1324,10 @@ static int host_pw_leaves(int n) {
 static int bal_threads(int n) { return n <= 256 ? 64 : (n >= 2048 ? 1024 : 256); }
 static size_t bal_smem(int n) { return (size_t)2 * host_pw_leaves(n) * 8 * sizeof(double); }
 
-__global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids, double* scale, int* sweeps_out,
+__global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, double* scale, int* sweeps_out,
                                                         int max_sweeps, double* margin) {
-  const int b = ids[blockIdx.x];
+  if (blockIdx.x >= *L.cnt) return;
+  const int b = L.ids[blockIdx.x];
   const int n = S.n;
   double* B = S.buf(b, G_B);
   double* sc = scale + (size_t)b * n;
@@ -1430,7 +1437,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, const int* ids
 // Scaled DB update (sqrtm.py:57-67) fused with the column sums of |X'-X| and |X'|.
 struct DbArgs {
   Slots S;
-  const int* ids;
+  DList L;
   const int* xpiv;   // [b][n] pivot rows of the X inversion (piv)
   const int* xstep;  // [b][n] rowstep of the X inversion
   const int* ypiv;
@@ -1446,7 +1453,8 @@ struct DbArgs {
 };
 
 __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
-  const int b = a.ids[blockIdx.y];
+  if (blockIdx.y >= *a.L.cnt) return;
+  const int b = a.L.ids[blockIdx.y];
   const int n = a.S.n;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
@@ -1511,7 +1519,10 @@ struct EstJob {
   const double* M1;
   const double* M2;   // nullable: operator M1^p1 * M2
   int p1;
-  int zero;           // zero-matrix shortcut applies and M1 == 0 -> est 0, no passes
+  int live;           // slot in use (device-built tables are capacity-sized)
+  int zchk;           // est_power_norm's zero-matrix shortcut applies (matcore.py:309-310)
+  int nzf;            // set by est_nz_kernel when M1 has a nonzero entry
+  int owner, key;     // matrix index and cache key (power) of the request
   double* V0;         // ping
   double* V1;         // pong
   double* part;       // adjoint partial sums [splits][2][n]
@@ -1532,8 +1543,19 @@ __global__ void est_init_kernel(EstJob* jobs, int n, double rsum) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
     J.total = J.p1 + (J.M2 ? 1 : 0);
-    J.done = J.zero ? 1 : 0;
+    J.done = (!J.live || (J.zchk && !J.nzf)) ? 1 : 0;
   }
+}
+
+// est_power_norm's zero shortcut: flag jobs whose M1 has a nonzero entry (CTAs skip the scan
+// once the flag is set)
+__global__ void est_nz_kernel(EstJob* jobs, int n) {
+  EstJob& J = jobs[blockIdx.y];
+  if (!J.live || !J.zchk || *(volatile int*)&J.nzf) return;
+  bool nz = false;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x)
+    nz |= J.M1[idx] != 0.0;
+  if (__syncthreads_or(nz) && threadIdx.x == 0) J.nzf = 1;
 }
 
 // One thin product for every job still running: step q of the forward (trans=0) or adjoint
@@ -1817,10 +1839,10 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
     if (tid == 0) {
       J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
       J.total = J.p1 + (J.M2 ? 1 : 0);
-      J.done = J.zero ? 1 : 0;
+      J.done = (!J.live || (J.zchk && !J.nzf)) ? 1 : 0;
     }
   }
-  if (J.zero) return;  // (uniform: host-set)
+  if (!J.live || (J.zchk && !J.nzf)) return;  // (uniform: set before the launch)
   for (int idx = tid; idx < n * n; idx += 256) Ms[idx] = J.M1[idx];
   __syncthreads();
   const int total = J.p1 + (J.M2 ? 1 : 0);
@@ -1911,9 +1933,10 @@ struct CombSpec {
 // once both combinations are materialised (combine_kernel): measured 2.2x faster at n = 512
 // than building the left combination inside the A-tile load (gemm_comb_kernel).
 constexpr int GP_A = TM * LDA_S, GP_B = TK * LDB_S;
-__global__ void __launch_bounds__(128) gemm_plain_kernel(Slots S, const int* ids, int ak, int bk, int ck) {
+__global__ void __launch_bounds__(128) gemm_plain_kernel(Slots S, DList L, int ak, int bk, int ck) {
   extern __shared__ __align__(16) double gsm[];
-  const int b = ids[blockIdx.z];
+  if (blockIdx.z >= *L.cnt) return;
+  const int b = L.ids[blockIdx.z];
   const int n = S.n;
   const int col0 = blockIdx.x * TN, row0 = blockIdx.y * TM;
   const double* A = S.buf(b, ak);
@@ -1974,10 +1997,11 @@ __global__ void __launch_bounds__(128) gemm_plain_kernel(Slots S, const int* ids
   }
 }
 
-__global__ void __launch_bounds__(128) gemm_comb_kernel(Slots S, const int* ids, CombSpec L, int rk, int ck) {
+__global__ void __launch_bounds__(128) gemm_comb_kernel(Slots S, DList DL, CombSpec L, int rk, int ck) {
   __shared__ __align__(16) double As[TM * LDA_S];
   __shared__ __align__(16) double Bs[TK * LDB_S];
-  const int b = ids[blockIdx.z];
+  if (blockIdx.z >= *DL.cnt) return;
+  const int b = DL.ids[blockIdx.z];
   const int n = S.n;
   const int col0 = blockIdx.x * TN, row0 = blockIdx.y * TM;
   const double* R = S.buf(b, rk);
@@ -2021,57 +2045,6 @@ __global__ void __launch_bounds__(128) gemm_comb_kernel(Slots S, const int* ids,
         const int j = c0 + ni * 8 + 2 * t + e;
         if (j < n) Cm[(size_t)i * n + j] = acc[mi][ni][e];
       }
-  }
-}
-
-// dst = sum_t c_t P_t + c0 I (elementwise, schemes.py:91-101 order)
-__global__ void combine_kernel(Slots S, const int* ids, CombSpec C, int dk) {
-  const int b = ids[blockIdx.y];
-  const int n = S.n;
-  double* D = S.buf(b, dk);
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
-    int i = idx / n, j = idx - (size_t)i * n;
-    double v = 0.0;
-    for (int q = 0; q < C.nterm; ++q) v = __dadd_rn(v, __dmul_rn(C.coef[q], S.buf(b, C.node[q])[idx]));
-    if (i == j && C.c0 != 0.0) v = __dadd_rn(v, C.c0);
-    D[idx] = v;
-  }
-}
-
-// L = mult_b * z * (scale_i / scale_j), z = sum_t c_t P_t + c0 I, written to the output.
-__global__ void final_kernel(Slots S, const int* ids, CombSpec C, const double* mult, const double* scale,
-                             int unbal, double* Lout, long long ld, int* nonfinite) {
-  const int b = ids[blockIdx.y];
-  const int n = S.n;
-  const double* sc = scale + (size_t)b * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
-    int i = idx / n, j = idx - (size_t)i * n;
-    double v = 0.0;
-    for (int q = 0; q < C.nterm; ++q) v = __dadd_rn(v, __dmul_rn(C.coef[q], S.buf(b, C.node[q])[idx]));
-    if (i == j && C.c0 != 0.0) v = __dadd_rn(v, C.c0);
-    v = mult[b] * v;
-    if (unbal) v = v * (sc[i] / sc[j]);
-    Lout[(size_t)b * n * ld + (size_t)i * ld + j] = v;
-    if (nonfinite && !isfinite(v)) nonfinite[b] = 1;
-  }
-}
-
-__global__ void store_kernel(Slots S, const int* ids, int k, double* out, long long ld) {
-  const int b = ids[blockIdx.y];
-  const int n = S.n;
-  const double* M = S.buf(b, k);
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
-    int i = idx / n, j = idx - (size_t)i * n;
-    out[(size_t)b * n * ld + (size_t)i * ld + j] = M[idx];
-  }
-}
-
-// L of a failed matrix: all NaN (a caller ignoring the status never reads stale data)
-__global__ void nan_fill_kernel(const int* ids, int n, double* out, long long ld) {
-  const int b = ids[blockIdx.y];
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < (size_t)n * n; idx += (size_t)gridDim.x * blockDim.x) {
-    int i = idx / n, j = idx - (size_t)i * n;
-    out[(size_t)b * n * ld + (size_t)i * ld + j] = __longlong_as_double(0x7ff8000000000000LL);
   }
 }
 

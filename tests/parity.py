@@ -14,6 +14,14 @@ different square roots), and either side recorded a stop test with rel within a 
 of tol.  The caller still checks L against the accuracy tolerance for it.  Any other
 difference -- a different status, s or k -- is a ``mismatch`` unless the margin exemption
 applies.
+
+``db_stall``: the noise floor itself.  On kappa ~ 1e8 inputs at small n, rel/tol settles at
+O(1) rounding noise (e.g. 1.03 .. 1.99 for 40 iterations) and whether it ever dips below 1
+before the 50-iteration cap depends on the inversion's rounding: the oracle (LAPACK
+getrf/getrs) stalls on some matrices where Gauss-Jordan converges and vice versa.  A record
+is ``db_stall`` only when one side is DB_NOCONV after >= 10 plateau stop tests (it sat at the
+noise floor, never within reach of the scaling decisions) and the other side converged after
+at least one plateau stop test.  Tests state how many they allow (0 on the BASELINE configs).
 """
 import multiprocessing as mp
 import os
@@ -25,6 +33,7 @@ FIELDS = ("status", "s", "k", "db_iters", "products", "divisions", "estimation_p
 # fields a db_plateau record may differ in (everything else must be equal)
 PLATEAU_FREE = ("db_iters", "divisions", "estimation_passes")
 EXEMPT_MARGIN = 1e-10
+STALL_PLATEAU = 10
 
 
 def gpu_fields(rec):
@@ -39,9 +48,13 @@ def classify(gpu_rec, oracle_rep):
     m = min(float(gpu_rec["min_margin"]), float(oracle_rep["min_margin"]))
     if m < EXEMPT_MARGIN:
         return "exempt", g, o
-    plateau = int(gpu_rec["db_plateau"]) > 0 or int(oracle_rep.get("db_plateau", 0)) > 0
-    if plateau and all(g[f] == o[f] for f in FIELDS if f not in PLATEAU_FREE):
+    gp, op = int(gpu_rec["db_plateau"]), int(oracle_rep.get("db_plateau", 0))
+    if (gp > 0 or op > 0) and all(g[f] == o[f] for f in FIELDS if f not in PLATEAU_FREE):
         return "db_plateau", g, o
+    if {g["status"], o["status"]} == {0, 2}:
+        stalled, conv = (gp, op) if g["status"] == 2 else (op, gp)
+        if stalled >= STALL_PLATEAU and conv >= 1:
+            return "db_stall", g, o
     return "mismatch", g, o
 
 
@@ -108,18 +121,18 @@ def oracle_reports(As, Ls, reps, procs=None):
         return pool.map(_oracle_check_one, items, chunksize=max(1, B // (4 * procs)))
 
 
-def check_batch(As, L, reps, allow_mismatch=0, procs=None, verbose=True):
+def check_batch(As, L, reps, allow_mismatch=0, procs=None, verbose=True, allow_stall=0):
     """Compare GPU (L, reports) with the oracle per matrix.  match / db_plateau records with
     status OK on both sides must meet the L tolerance; mismatches are counted (<= allowed).
     An exempt record with equal (status, s, k) is held to the L tolerance as well."""
-    counts = {"match": 0, "exempt": 0, "db_plateau": 0, "mismatch": 0}
+    counts = {"match": 0, "exempt": 0, "db_plateau": 0, "db_stall": 0, "mismatch": 0}
     worst = 0.0
     res = oracle_reports(As, L, reps, procs)
     for b, (rr, err, tol) in enumerate(res):
         cls, g, o = classify(reps[b], rr)
         counts[cls] += 1
-        if cls == "mismatch" and verbose:
-            print("MISMATCH", b, "gpu", g, "oracle", o, "margins", float(reps[b]["min_margin"]), rr["min_margin"])
+        if cls in ("mismatch", "db_stall") and verbose:
+            print(cls.upper(), b, "gpu", g, "oracle", o, "margins", float(reps[b]["min_margin"]), rr["min_margin"])
         both_ok = rr["status"] == 0 and int(reps[b]["status"]) == 0
         same = (g["status"], g["s"], g["k"]) == (o["status"], o["s"], o["k"])
         if both_ok and same and cls != "mismatch":
@@ -129,4 +142,5 @@ def check_batch(As, L, reps, allow_mismatch=0, procs=None, verbose=True):
     if verbose:
         print(counts, "worst err/tol", worst)
     assert counts["mismatch"] <= allow_mismatch, counts
+    assert counts["db_stall"] <= allow_stall, counts
     return counts, res

@@ -115,8 +115,8 @@ def test_sqrt_db_grid_failures():
     assert list(its) == [50, 0, 1]
 
 
-def _check(As, L, reps, allow_mismatch=0):
-    counts, _ = check_batch(As, L, reps, allow_mismatch)
+def _check(As, L, reps, allow_mismatch=0, allow_stall=0):
+    counts, _ = check_batch(As, L, reps, allow_mismatch, allow_stall=allow_stall)
     return counts
 
 
@@ -124,7 +124,7 @@ def _check(As, L, reps, allow_mismatch=0):
 def test_logm_grid_config_shapes(c, n, B):
     A = synth.config(c, batch=B, n=n)
     L, reps = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
-    _check(A, L, reps)
+    _check(A, L, reps, allow_stall=1 if c == 4 else 0)   # (see tests/parity.py db_stall)
 
 
 def test_logm_grid_near_identity_orders():
