@@ -17,11 +17,20 @@
  * Conventions: every matrix pointer is a DEVICE pointer to `batch` row-major n x n
  * float64 matrices with row stride `ld` >= n and matrix stride n*ld elements;
  * inputs are never written; outputs never alias inputs.  All calls are
- * stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream), do no
- * hidden allocation and return synchronously-detected argument / launch errors
+ * stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream): they
+ * never block the host (n > 64 runs as one CUDA graph whose loops are device-side
+ * conditional nodes).  No hidden device allocation: scratch comes from the caller's
+ * `workspace` (lgm_workspace_bytes / lgm_block_workspace_bytes; none is needed by the
+ * building blocks for n <= 64).  Argument / launch errors are returned synchronously
  * (< 0).  Per-matrix numerical outcomes are reported per matrix through status
  * codes (LGM_OK ... LGM_NONFINITE), which the Python layer maps onto the
- * reference's exceptions (exceptions.py:6-18).  Reentrant; no global mutable state.
+ * reference's exceptions (exceptions.py:6-18); a failed matrix's L is all NaN.
+ *
+ * Threading: reentrant.  Calls on different workspaces may run concurrently on any
+ * streams / devices; calls sharing one workspace must be ordered by the caller (as any
+ * two users of one buffer).  Process-wide state: a mutex-guarded cache of instantiated
+ * CUDA graphs keyed by (device, workspace address, n, batch, entry point), and the
+ * monotonic launch counters behind lgm_launch_count.
  */
 #ifndef LOGMPOLY_B200_H
 #define LOGMPOLY_B200_H
@@ -84,8 +93,12 @@ typedef struct lgm_report { /* per matrix, written to device memory */
 
 void lgm_default_opts(lgm_opts* opts);
 
-/* Workspace the caller must provide to lgm_logm_f64 (0 for the fused n <= 64 path). */
+/* Workspace the caller must provide to lgm_logm_f64: 4 n^2 doubles per matrix for the
+ * fused n <= 64 path (polynomial nodes, A_I2), the Engine G slots and tables beyond. */
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes);
+
+/* Workspace of the building blocks below (0 for n <= 64). */
+int lgm_block_workspace_bytes(int64_t n, int64_t batch, size_t* bytes);
 
 /* Largest n handled by the fused one-CTA-per-matrix engine. */
 int lgm_max_fused_n(void);
@@ -97,31 +110,35 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
 /* X = A^(1/2) by the scaled coupled DB iteration; iters/status: int32[batch] device. */
 int lgm_sqrt_db_f64(const double* A, double* X, int64_t n, int64_t batch, int64_t ld,
                     double tol, int32_t maxiter, int32_t* iters_dev, int32_t* status_dev,
-                    lgm_stream_t stream);
+                    void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
 /* est = lower bound of ||M^p||_1; passes = estimation_passes; double/int32[batch] device. */
 int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld, int32_t p,
                            int32_t itmax, double* est_dev, int32_t* passes_dev,
-                           lgm_stream_t stream);
+                           void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
 /* est = lower bound of ||M1^p1 M2||_1 (M2 may be NULL: ||M1^p1||_1 without the zero shortcut). */
 int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int64_t n,
                              int64_t batch, int64_t ld, int32_t itmax, double* est_dev,
-                             int32_t* passes_dev, lgm_stream_t stream);
+                             int32_t* passes_dev, void* workspace, size_t workspace_bytes,
+                             lgm_stream_t stream);
 
 /* B = T^-1 A T with radix-2 scales; scale: double[batch*n] device; sweeps: int32[batch]. */
 int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_t batch,
-                    int64_t ld, int32_t max_sweeps, int32_t* sweeps_dev, lgm_stream_t stream);
+                    int64_t ld, int32_t max_sweeps, int32_t* sweeps_dev, void* workspace,
+                    size_t workspace_bytes, lgm_stream_t stream);
 
 /* Z = z(X) for shipped scheme k; first_product (X^2, may be NULL) saves one product. */
 int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z, int64_t n,
                         int64_t batch, int64_t ld, int32_t k, int32_t* products_dev,
-                        lgm_stream_t stream);
+                        void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
 const char* lgm_status_string(int code);
 
-/* Number of CUDA kernels this library has launched so far (process-wide, monotonic);
- * bench.py reports the difference across its timed region as gpu_launches. */
+/* Number of CUDA kernels this library has launched so far (process-wide, monotonic):
+ * direct launches plus the kernels executed inside Engine G graphs (counted on the device;
+ * reading them synchronises, so call it outside timed regions).  bench.py reports the
+ * difference across its timed region as gpu_launches. */
 long long lgm_launch_count(void);
 
 #ifdef __cplusplus

@@ -1,8 +1,8 @@
 // C-ABI entry points (include/logmpoly_b200.h) and the kernels behind them.
 //
 // n <= 64: Engine F (lgm_fused.cuh), one CTA per matrix, the whole pipeline in one launch.
-// n  > 64: Engine G (lgm_grid.cu), host-orchestrated batched kernels over a caller-owned
-//          workspace (lgm_workspace_bytes).
+// n  > 64: Engine G (lgm_grid.cu), device-driven batched kernels in one CUDA graph per call
+//          over a caller-owned workspace (lgm_workspace_bytes).
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -191,7 +191,30 @@ void lgm_default_opts(lgm_opts* o) {
 #endif
 int lgm_max_fused_n(void) { return LGM_FUSED_MAX; }
 
-long long lgm_launch_count(void) { return g_lgm_launches.load(std::memory_order_relaxed); }
+// devices on which Engine G graphs have run (their device-side executed-kernel counters)
+static std::atomic<unsigned long long> g_grid_devs{0};
+static void note_grid_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) == cudaSuccess && d < 64) g_grid_devs.fetch_or(1ull << d, std::memory_order_relaxed);
+}
+
+// Direct launches (Engine F, graph setup kernels) + kernels executed inside Engine G graphs
+// (counted on the device by the graphs' decide kernels; read back synchronously -- call it
+// after synchronising, as bench.py does).
+long long lgm_launch_count(void) {
+  long long v = g_lgm_launches.load(std::memory_order_relaxed);
+  const unsigned long long m = g_grid_devs.load(std::memory_order_relaxed);
+  if (m) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int d = 0; d < 64; ++d)
+      if ((m >> d) & 1ull) {
+        if (cudaSetDevice(d) == cudaSuccess) v += (long long)lgm_grid_exec_nodes();
+      }
+    cudaSetDevice(cur);
+  }
+  return v;
+}
 
 // Engine G launches index matrices (and their X / Y inversion jobs) in grid.y / grid.z, so a
 // larger batch runs as consecutive passes of at most this many matrices over one workspace.
@@ -208,6 +231,18 @@ int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * 4 * n * n * sizeof(double)
                    : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
+}
+
+int lgm_block_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
+  if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
+  *bytes = n <= LGM_FUSED_MAX ? 0 : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
+  return 0;
+}
+
+static bool block_ws_ok(int64_t n, int64_t batch, const void* ws, size_t ws_bytes) {
+  size_t need = 0;
+  lgm_block_workspace_bytes(n, batch, &need);
+  return need == 0 || (ws && ws_bytes >= need);
 }
 
 const char* lgm_status_string(int code) {
@@ -247,6 +282,7 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
     return full ? launch_fused<64, true>(A, L, rep, ld, n, batch, ws, P, s)
                 : launch_fused<64, false>(A, L, rep, ld, n, batch, ws, P, s);
   }
+  note_grid_device();
   const int64_t ch = grid_chunk();
   for (int64_t b0 = 0; b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
@@ -271,31 +307,35 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   } while (0)
 
 int lgm_sqrt_db_f64(const double* A, double* X, int64_t n, int64_t batch, int64_t ld, double tol, int32_t maxiter,
-                    int32_t* iters, int32_t* status, lgm_stream_t stream) {
+                    int32_t* iters, int32_t* status, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(A, n, batch, ld) || !X || !iters || !status || maxiter < 1) return LGM_ERR_ARG;
+  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(sqrt_db_kernel, A, X, ld, (int)n, tol, maxiter, iters, status, P);
   for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    note_grid_device();
     const int rc = lgm_grid_sqrt_db(A + b0 * n * ld, X + b0 * n * ld, n, cnt, ld, tol, maxiter, iters + b0,
-                                    status + b0, (cudaStream_t)stream);
+                                    status + b0, ws, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return 0;
 }
 
 int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld, int32_t p, int32_t itmax,
-                           double* est, int32_t* passes, lgm_stream_t stream) {
+                           double* est, int32_t* passes, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(M, n, batch, ld) || !est || !passes || p < 1 || itmax < 1) return LGM_ERR_ARG;
+  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(est_kernel, M, p, (const double*)nullptr, ld, (int)n, itmax, 1, est, passes, P);
   for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
-    const int rc = lgm_grid_est(M + b0 * n * ld, p, nullptr, n, cnt, ld, itmax, 1, est + b0, passes + b0,
+    note_grid_device();
+    const int rc = lgm_grid_est(M + b0 * n * ld, p, nullptr, n, cnt, ld, itmax, 1, est + b0, passes + b0, ws,
                                 (cudaStream_t)stream);
     if (rc) return rc;
   }
@@ -303,40 +343,46 @@ int lgm_est_power_norm_f64(const double* M, int64_t n, int64_t batch, int64_t ld
 }
 
 int lgm_est_product_norm_f64(const double* M1, int32_t p1, const double* M2, int64_t n, int64_t batch, int64_t ld,
-                             int32_t itmax, double* est, int32_t* passes, lgm_stream_t stream) {
+                             int32_t itmax, double* est, int32_t* passes, void* ws, size_t ws_bytes,
+                             lgm_stream_t stream) {
   if (!args_ok(M1, n, batch, ld) || !est || !passes || p1 < 1 || itmax < 1) return LGM_ERR_ARG;
+  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(est_kernel, M1, p1, M2, ld, (int)n, itmax, 0, est, passes, P);
   for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    note_grid_device();
     const int rc = lgm_grid_est(M1 + b0 * n * ld, p1, M2 ? M2 + b0 * n * ld : nullptr, n, cnt, ld, itmax, 0,
-                                est + b0, passes + b0, (cudaStream_t)stream);
+                                est + b0, passes + b0, ws, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return 0;
 }
 
 int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_t batch, int64_t ld,
-                    int32_t max_sweeps, int32_t* sweeps, lgm_stream_t stream) {
+                    int32_t max_sweeps, int32_t* sweeps, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(A, n, batch, ld) || !B || !scale || !sweeps || max_sweeps < 1) return LGM_ERR_ARG;
+  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
   LGM_DISPATCH_SMALL(balance_kernel, A, B, scale, ld, (int)n, max_sweeps, sweeps, P);
   for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    note_grid_device();
     const int rc = lgm_grid_balance(A + b0 * n * ld, B + b0 * n * ld, scale + b0 * n, n, cnt, ld, max_sweeps,
-                                    sweeps + b0, (cudaStream_t)stream);
+                                    sweeps + b0, ws, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return 0;
 }
 
 int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
-                        int32_t* products, lgm_stream_t stream) {
+                        int32_t* products, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(X, n, batch, ld) || !Z || !products || k < 1 || k > LGM_K_MAX) return LGM_ERR_ARG;
+  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
@@ -354,8 +400,9 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
   }
   for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
     const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    note_grid_device();
     const int rc = lgm_grid_degopt(X + b0 * n * ld, FP ? FP + b0 * n * ld : nullptr, Z + b0 * n * ld, n, cnt, ld, k,
-                                   products + b0, P, (cudaStream_t)stream);
+                                   products + b0, P, ws, (cudaStream_t)stream);
     if (rc) return rc;
   }
   return 0;

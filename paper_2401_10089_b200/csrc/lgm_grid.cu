@@ -26,29 +26,6 @@
 
 namespace {
 
-// Optional host-side phase timing (LGM_GRID_PROFILE=1): stream-synchronised wall time per
-// phase, read back with lgm_debug_grid_phase_ms (tools/grid_prof.py).  Off by default.
-enum { PH_BALANCE = 0, PH_ALPHA, PH_INVERT, PH_DBUPD, PH_SELECT, PH_POLY, PH_OTHER, PH_N };
-double g_phase_ms[PH_N];
-bool prof_on() {
-  static const bool on = std::getenv("LGM_GRID_PROFILE") != nullptr;  // thread-safe once-init
-  return on;
-}
-struct PhaseTimer {
-  int ph;
-  cudaStream_t st;
-  std::chrono::steady_clock::time_point t0;
-  PhaseTimer(int p, cudaStream_t s) : ph(p), st(s) {
-    if (prof_on()) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
-  }
-  ~PhaseTimer() {
-    if (prof_on()) {
-      cudaStreamSynchronize(st);
-      g_phase_ms[ph] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    }
-  }
-};
-
 constexpr int NB = 32;      // Gauss-Jordan panel width
 #ifndef G2_RT
 #define G2_RT 64            // rows per tile of the rank-64 combined pass (64: 4 warps; 128 measured equal)
@@ -1325,8 +1302,10 @@ static int bal_threads(int n) { return n <= 256 ? 64 : (n >= 2048 ? 1024 : 256);
 static size_t bal_smem(int n) { return (size_t)2 * host_pw_leaves(n) * 8 * sizeof(double); }
 
 __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, double* scale, int* sweeps_out,
-                                                        int max_sweeps, double* margin) {
-  if (blockIdx.x >= *L.cnt) return;
+                                                        int max_sweeps, double* margin, const int* enable,
+                                                        const int* max_sweeps_p) {
+  if (blockIdx.x >= *L.cnt || (enable && !*enable)) return;
+  if (max_sweeps_p) max_sweeps = *max_sweeps_p;
   const int b = L.ids[blockIdx.x];
   const int n = S.n;
   double* B = S.buf(b, G_B);
@@ -1535,6 +1514,10 @@ struct EstJob {
 
 __global__ void est_init_kernel(EstJob* jobs, int n, double rsum) {
   EstJob& J = jobs[blockIdx.y];
+  if (!J.live) {  // unused slot of a device-built table (its vectors are not assigned)
+    if (blockIdx.x == 0 && threadIdx.x == 0) J.done = 1;
+    return;
+  }
   const int t = n < 2 ? n : 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     J.V0[i] = 1.0 / n;
@@ -1830,6 +1813,10 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
   __shared__ EstAdjSmem sa;
   EstJob& J = jobs[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!J.live) {  // unused slot of a device-built table
+    if (tid == 0) J.done = 1;
+    return;
+  }
   {  // est_init_kernel
     const int t = n < 2 ? n : 2;
     for (int i = tid; i < n; i += 256) {
@@ -2048,1001 +2035,1520 @@ __global__ void __launch_bounds__(128) gemm_comb_kernel(Slots S, DList DL, CombS
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// Host side
-double host_pairwise_abs_ramp(int n) {
-  // numpy pairwise sum of |(-1)^i (1 + i/max(1, n-1))| (matcore.py:270-271)
-  auto get = [n](int i) { return std::fabs(((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))); };
-  return lgm_pairwise_sum(get, n);
-}
+// ==========================================================================================
+// Device-resident Algorithm 1 (north_star item 3): every decision of oracle/driver.py --
+// the scaling-loop alpha test with the Eq. 27/28 skips, the DB stop test and mu switch,
+// select_order's min_im / max_in / sweep, the estimate cache and the active-set compaction --
+// runs in single-CTA "decide" kernels on per-matrix state held in the workspace.  The heavy
+// kernels read the device-built lists / job tables (capacity = batch; unused entries exit at
+// once).  The whole call is one CUDA graph: the scaling loop, the DB iterations and the
+// select sweep are WHILE conditional nodes whose conditions the decide kernels set with
+// cudaGraphSetConditional, so lgm_logm_f64 never blocks the host and is stream-ordered.
+// Graphs are captured once per (device, workspace, n, batch, entry point) and cached; the
+// per-call pointers and parameters travel in a CallDesc written by a setup kernel.
 
-struct Grid {
-  int n = 0, batch = 0;
-  cudaStream_t st = nullptr;
-  Slots S{};
-  // device arrays
-  int* d_ids = nullptr;       // [batch] scratch id list
-  int* d_piv = nullptr;       // [2][batch][n]
-  int* d_step = nullptr;      // [2][batch][n]
-  double* d_W = nullptr;      // [6 kinds][2][batch][NB*n]
-  cudaStream_t sB = nullptr;  // G2 look-ahead: panel stream (higher priority)
-  cudaEvent_t evN = nullptr, evP = nullptr;
-  ~Grid() {
-    if (sB) cudaStreamDestroy(sB);
-    if (evN) cudaEventDestroy(evN);
-    if (evP) cudaEventDestroy(evP);
-  }
-  double* d_logdet = nullptr; // [2][batch]
-  int* d_istat = nullptr;     // [2][batch]
-  std::vector<InvJob> jobs_up;  // host copy of the job table last uploaded to d_jobs
-  InvJob* d_jobs = nullptr;   // [2*batch]
-  double* d_scal = nullptr;   // [batch] scratch doubles
-  double* d_scal2 = nullptr;
-  int* d_iflag = nullptr;     // [batch]
-  int* d_scaling = nullptr;   // [batch]
-  double* d_scale = nullptr;  // [batch][n] balancing scales
-  double* d_margin = nullptr; // [batch]
-  int* d_sweeps = nullptr;    // [batch]
-  EstJob* d_est = nullptr;    // [batch]
-  double* d_vec = nullptr;    // [batch][2 vectors][2n]
-  double* d_part = nullptr;   // [batch][splits][2][n]
-  int* d_hist = nullptr;      // [batch][16]
-  int splits = 1;
-
-  static size_t bytes(int64_t n, int64_t batch) {
-    int64_t splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
-    size_t s = 0;
-    auto add = [&](size_t b) { s += (b + 255) & ~size_t(255); };
-    add((size_t)batch * NBUF * n * n * 8);
-    add(batch * 4);
-    add(2 * batch * n * 4);
-    add(2 * batch * n * 4);
-    add(12 * batch * NB * n * 8);
-    add(2 * batch * 8);
-    add(2 * batch * 4);
-    add(2 * batch * sizeof(InvJob));
-    add(batch * 8);
-    add(batch * 8);
-    add(batch * 4);
-    add(batch * 4);
-    add(batch * n * 8);
-    add(batch * 8);
-    add(batch * 4);
-    add(batch * sizeof(EstJob));
-    add(batch * 4 * n * 8);
-    add(batch * splits * 2 * n * 8);
-    add(batch * 16 * 4);
-    return s;
-  }
-
-  void carve(void* ws, int n_, int batch_) {
-    n = n_;
-    batch = batch_;
-    splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
-    char* p = (char*)ws;
-    auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return (void*)r; };
-    S.ws = (double*)take((size_t)batch * NBUF * n * n * 8);
-    S.n = n;
-    d_ids = (int*)take(batch * 4);
-    d_piv = (int*)take(2 * (size_t)batch * n * 4);
-    d_step = (int*)take(2 * (size_t)batch * n * 4);
-    d_W = (double*)take(12 * (size_t)batch * NB * n * 8);
-    d_logdet = (double*)take(2 * batch * 8);
-    // d_scal, d_scal2, d_istat adjacent: the DB step reads all three back in one copy
-    d_scal = (double*)take(batch * 8);
-    d_scal2 = (double*)take(batch * 8);
-    d_istat = (int*)take(2 * batch * 4);
-    d_jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
-    d_iflag = (int*)take(batch * 4);
-    d_scaling = (int*)take(batch * 4);
-    d_scale = (double*)take((size_t)batch * n * 8);
-    d_margin = (double*)take(batch * 8);
-    d_sweeps = (int*)take(batch * 4);
-    d_est = (EstJob*)take(batch * sizeof(EstJob));
-    d_vec = (double*)take((size_t)batch * 4 * n * 8);
-    d_part = (double*)take((size_t)batch * splits * 2 * n * 8);
-    d_hist = (int*)take(batch * 16 * 4);
-  }
-
-  dim3 ew_grid(int count) const {
-    size_t nn = (size_t)n * n;
-    int bx = (int)std::min<size_t>((nn + 255) / 256, 1024);
-    return dim3(bx, count);
-  }
-
-  int upload_ids(const std::vector<int>& ids) {
-    CK(cudaMemcpyAsync(d_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st));
-    return 0;
-  }
-
-  // ---- batched inversion of slot `k` of the listed matrices (jobs: which = 0 for X, 1 for Y)
-  template <int NT>
-  int launch_g1(int nj) {
-    const size_t sm = G1Smem<NT>::bytes;
-    CK(cudaFuncSetAttribute(gj_inv_cta_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    lgm_count_launch(), gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(d_jobs, n);
-    CK(cudaGetLastError());
-    return 0;
-  }
-
-  int invert(const std::vector<int>& mats, const std::vector<int>& which, const std::vector<int>& slot,
-             const std::vector<int>* src_slot = nullptr) {
-    const int nj = (int)mats.size();
-    if (!nj) return 0;
-    std::vector<InvJob> jobs(nj);
-    for (int q = 0; q < nj; ++q) {
-      int b = mats[q], w = which[q];
-      InvJob& J = jobs[q];
-      J.M = S.buf(b, slot[q]);
-      J.Src = (src_slot && use_g1(n)) ? S.buf(b, (*src_slot)[q]) : nullptr;
-      J.piv = d_piv + ((size_t)w * batch + b) * n;
-      J.rowstep = d_step + ((size_t)w * batch + b) * n;
-      J.Wb = d_W + ((size_t)w * batch + b) * NB * n;
-      J.wst = (long long)2 * batch * NB * n;
-      J.logdet = d_logdet + w * batch + b;
-      J.status = d_istat + w * batch + b;
-    }
-    // the job table only changes with the active set: skip the (pageable, host-blocking)
-    // re-upload between DB steps when it is byte-identical to the last one
-    if (jobs_up.size() != jobs.size() || std::memcmp(jobs_up.data(), jobs.data(), nj * sizeof(InvJob)) != 0) {
-      CK(cudaMemcpyAsync(d_jobs, jobs.data(), nj * sizeof(InvJob), cudaMemcpyHostToDevice, st));
-      jobs_up = jobs;
-    }
-    if (use_g1(n)) {  // G1: one CTA per inversion, no per-panel launches
-      if (n <= 128) return launch_g1<128>(nj);
-      if (n <= 256) return launch_g1<256>(nj);
-      return launch_g1<512>(nj);
-    }
-    lgm_count_launch(), gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
-    const int tiles = (n + TM - 1) / TM;
-    const bool cta_panel = n <= 512;  // one CTA per panel (writes A1 itself: no gj_copy_a1_kernel)
-    // dynamic shared memory limits are per device: set them on every call (no process-wide flag)
-    if (n <= 128) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 33 * 8));
-    else if (n <= 256) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 32 * 33 * 8));
-    else if (n <= 512) CK(cudaFuncSetAttribute(gj_panel_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 32 * 33 * 8));
-    auto panel = [&](int k0, cudaStream_t s, int a1_kind = -1, int s1_a1kind = -1) {
-      const int nb = std::min(NB, n - k0);
-      if (n <= 128) {  // many small jobs: one CTA per inversion, no cluster
-        lgm_count_launch(), gj_panel_cta_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
-      } else if (n <= 256) {
-        lgm_count_launch(), gj_panel_cta_kernel<256><<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
-      } else if (n <= 512) {
-        lgm_count_launch(), gj_panel_cta_kernel<512><<<nj, 512, 16 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
-      } else if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
-        lgm_count_launch(), gj_panel_cluster_kernel<<<nj * CL, 512, 0, s>>>(d_jobs, n, k0, nb);
-      } else {
-        lgm_count_launch(), gj_panel_kernel<<<nj, 512, 0, s>>>(d_jobs, n, k0, nb, 0);
-      }
-    };
-    auto snapshot = [&](int k0, int kind, int jlo = 0, int jhi = -1, cudaStream_t s = nullptr) {
-      const int nb = std::min(NB, n - k0);
-      if (jhi < 0) jhi = n;
-      lgm_count_launch(), gj_snapshot_kernel<<<dim3((nb * (jhi - jlo) + 255) / 256, nj), 256, 0, s ? s : st>>>(
-                              d_jobs, n, k0, nb, kind, jlo, jhi);
-    };
-    // Look-ahead: panel k+1 is factored on a second (higher-priority) stream while the
-    // trailing update of panel k runs on `st`.  Per panel k: the next panel's columns are
-    // updated first (narrow launch), then its factorisation is released to sB, then the
-    // full update skips both panels; the snapshot of panel k+1's pivot rows waits for both.
-    if (!sB) {
-      int lo = 0, hi = 0;
-      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CK(cudaStreamCreateWithPriority(&sB, cudaStreamNonBlocking, hi));
-      CK(cudaEventCreateWithFlags(&evN, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&evP, cudaEventDisableTiming));
-    }
-    static const bool rank64 = [] {  // LGM_G2_RANK64=0 falls back to rank-32 passes (A/B switch)
-      const char* e = std::getenv("LGM_G2_RANK64");
-      return !(e && e[0] == '0');
-    }();
-    // rank-64 vs rank-32 passes round differently: the choice depends on n only, so a
-    // matrix's arithmetic never depends on its batch-mates or on how many have converged
-    const bool use64 = rank64 && n % (2 * NB) == 0;
-    panel(0, st, use64 && cta_panel ? 2 : -1);
-    if (use64) {
-      // rank-64 delayed update with both panels of the next pair factored on sB during the
-      // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
-      // rows), A1 (copy of P1's multipliers), stage-1 update of P2's columns, factor P2, W2.
-      CK(cudaFuncSetAttribute(gj_update2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up2_smem<64>()));
-      CK(cudaFuncSetAttribute(gj_update2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)up2_smem<128>()));
-      auto prepare_pair = [&](int k0, int q, cudaStream_t s, bool full_snapshot) {
-        // P1 = [k0, k0+NB) already factored; everything except the full-width W1 / W2
-        if (cta_panel) {  // stage-1 update fused into P2's panel kernel
-          panel(k0 + NB, s, -1, 3 * q + 2);
-          return;
-        }
-        if (full_snapshot) snapshot(k0, 3 * q, 0, n, s);
-        else snapshot(k0, 3 * q, k0 + NB, k0 + 2 * NB, s);  // P2's columns only (for stage 1)
-        if (!cta_panel)
-          lgm_count_launch(), gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, s>>>(d_jobs, n, k0, 3 * q + 2);
-        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, s>>>(d_jobs, n, k0, NB, k0 + NB, k0 + NB,
-                                                                               k0 + 2 * NB, 0, 0, 3 * q);
-        panel(k0 + NB, s);
-      };
-      prepare_pair(0, 0, st, !cta_panel);
-      if (cta_panel) lgm_count_launch(), gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
-      else lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, 0);
-      for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
-        const int kn = k0 + 2 * NB;
-        const bool next = kn < n;
-        if (next) {  // finish the next pair's columns, then factor both of its panels on sB
-          lgm_count_launch(), gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0, kn, kn,
-                                                                                           kn + 2 * NB, 0, 0, q);
-          CK(cudaEventRecord(evN, st));
-          CK(cudaStreamWaitEvent(sB, evN, 0));
-          panel(kn, sB, cta_panel ? 3 * (q ^ 1) + 2 : -1);
-          prepare_pair(kn, q ^ 1, sB, false);
-          CK(cudaEventRecord(evP, sB));
-        }
-        lgm_count_launch(), gj_update2_kernel<G2_RT><<<dim3(tiles, n / G2_RT, nj), 2 * G2_RT, up2_smem<G2_RT>(), st>>>(
-                                d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
-        if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
-          CK(cudaStreamWaitEvent(st, evP, 0));
-          if (cta_panel) {
-            lgm_count_launch(), gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
-          } else {
-            snapshot(kn, 3 * (q ^ 1));
-            lgm_count_launch(), gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, 0);
-          }
-        }
-      }
-      CK(cudaGetLastError());
-      return 0;
-    }
-    snapshot(0, 0);
-    for (int k0 = 0, par = 0; k0 < n; k0 += NB, par ^= 1) {
-      const int nb = std::min(NB, n - k0);
-      const int kn = k0 + NB, nbn = kn < n ? std::min(NB, n - kn) : 0;
-      if (kn < n) {
-        lgm_count_launch(), gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, kn, kn, kn + nbn, 0, 0,
-                                                                                par);
-        CK(cudaEventRecord(evN, st));
-        CK(cudaStreamWaitEvent(sB, evN, 0));
-        panel(kn, sB);
-        CK(cudaEventRecord(evP, sB));
-      }
-      lgm_count_launch(), gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, 0, 0, n, kn,
-                                                                                   kn + nbn, par);
-      if (kn < n) {
-        CK(cudaStreamWaitEvent(st, evP, 0));
-        snapshot(kn, par ^ 1);
-      }
-    }
-    CK(cudaGetLastError());
-    return 0;
-  }
-
-  // ---- batched estimator: est[q] for the listed jobs (operator M1^p1 * M2)
-  int estimate(const std::vector<const double*>& M1, const std::vector<int>& p1, const std::vector<const double*>& M2,
-               const std::vector<int>& zero, int itmax, std::vector<double>& est, std::vector<int>& passes,
-               std::vector<double>& mm) {
-    const int nj = (int)M1.size();
-    est.assign(nj, 0.0);
-    passes.assign(nj, 0);
-    mm.assign(nj, INFINITY);
-    if (!nj) return 0;
-    std::vector<EstJob> jobs(nj);
-    int maxtot = 0;
-    for (int q = 0; q < nj; ++q) {
-      EstJob& J = jobs[q];
-      std::memset(&J, 0, sizeof(J));
-      J.M1 = M1[q];
-      J.M2 = M2[q];
-      J.p1 = p1[q];
-      J.zero = zero[q];
-      J.V0 = d_vec + (size_t)q * 4 * n;
-      J.V1 = J.V0 + 2 * n;
-      J.part = d_part + (size_t)q * splits * 2 * n;
-      J.hist = d_hist + q * 16;
-      maxtot = std::max(maxtot, p1[q] + (M2[q] ? 1 : 0));
-    }
-    CK(cudaMemcpyAsync(d_est, jobs.data(), nj * sizeof(EstJob), cudaMemcpyHostToDevice, st));
-    const double rsum = host_pairwise_abs_ramp(n);
-    if (n <= EST_FUSED_MAXN && est_fused_on()) {
-      const int sm = n * n * 8;
-      CK(cudaFuncSetAttribute(est_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      lgm_count_launch(), est_fused_kernel<<<nj, 256, sm, st>>>(d_est, n, rsum, itmax);
-    } else {
-    lgm_count_launch(), est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, rsum);
-    for (int sweep = 0; sweep < itmax; ++sweep) {
-      for (int q = 0; q < maxtot; ++q)
-        lgm_count_launch(), est_fwd_kernel<<<dim3((n + 8 * EST_FWD_R - 1) / (8 * EST_FWD_R), nj), 256, 0, st>>>(d_est, n, q);
-      lgm_count_launch(), est_after_fwd_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
-      for (int q = 0; q < maxtot; ++q) {
-        if ((n & 1) == 0) lgm_count_launch(), est_adj2_kernel<<<dim3((n + 255) / 256, splits, nj), 128, 0, st>>>(d_est, n, q);
-        else lgm_count_launch(), est_adj_kernel<<<dim3((n + 127) / 128, splits, nj), 128, 0, st>>>(d_est, n, q);
-        lgm_count_launch(), est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_est, n, q, splits);
-      }
-      lgm_count_launch(), est_after_adj_kernel<<<nj, 256, 0, st>>>(d_est, n, sweep);
-    }
-    }
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(jobs.data(), d_est, nj * sizeof(EstJob), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int q = 0; q < nj; ++q) {
-      est[q] = jobs[q].est;
-      passes[q] = jobs[q].passes;
-      mm[q] = jobs[q].mm;
-    }
-    return 0;
-  }
-
-  int onenorms(const std::vector<int>& mats, int k, std::vector<double>& out) {
-    const int c = (int)mats.size();
-    out.assign(batch, 0.0);
-    if (!c) return 0;
-    if (upload_ids(mats)) return LGM_ERR_CUDA;
-    CK(cudaMemsetAsync(d_scal, 0, batch * 8, st));
-    lgm_count_launch(), onenorm_kernel<<<dim3((n + 127) / 128, c), 128, 0, st>>>(S, d_ids, k, d_scal);
-    CK(cudaMemcpyAsync(out.data(), d_scal, batch * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return 0;
-  }
-
-  int any_nonzero(const std::vector<int>& mats, int k, std::vector<int>& out) {
-    out.assign(batch, 0);
-    if (mats.empty()) return 0;
-    if (upload_ids(mats)) return LGM_ERR_CUDA;
-    CK(cudaMemsetAsync(d_iflag, 0, batch * 4, st));
-    lgm_count_launch(), any_nonzero_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, k, d_iflag);
-    CK(cudaMemcpyAsync(out.data(), d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return 0;
-  }
-
-  // plain C = A * B over the matrices in d_ids (first `count`), n even
-  int gemm_plain(int count, int ak, int bk, int ck) {
-    const size_t sm = 2 * (size_t)(GP_A + GP_B) * 8;
-    CK(cudaFuncSetAttribute(gemm_plain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const int tiles = (n + TM - 1) / TM;
-    lgm_count_launch(), gemm_plain_kernel<<<dim3(tiles, tiles, count), 128, sm, st>>>(S, d_ids, ak, bk, ck);
-    CK(cudaGetLastError());
-    return 0;
-  }
-
-  int ew(const std::vector<int>& mats, int op, int dk, int sk, int s2k) {
-    if (mats.empty()) return 0;
-    if (upload_ids(mats)) return LGM_ERR_CUDA;
-    lgm_count_launch(), ew_kernel<<<ew_grid((int)mats.size()), 256, 0, st>>>(S, d_ids, op, dk, sk, s2k);
-    CK(cudaGetLastError());
-    return 0;
-  }
-
-  // ---- scaled DB square root of slot G_B for the listed matrices (sqrtm.py:27-78)
-  // Returns per-matrix status (0 / LGM_SINGULAR / LGM_DB_NOCONV) and iterations.
-  int sqrt_db(const std::vector<int>& mats, double tol_in, int maxiter, std::vector<int>& status,
-              std::vector<int>& iters, std::vector<double>& mm, std::vector<int>& plateau) {
-    std::vector<int> act = mats;
-    std::vector<int> scaling(batch, 1);
-    if (ew(act, 2, G_Y, G_Y, G_Y)) return LGM_ERR_CUDA;  // Y = I
-    for (int it = 1; it <= maxiter && !act.empty(); ++it) {
-      // inversions of X -> XI (all) and Y -> YI (it > 1): out of place inside G1 (n <= 512),
-      // else copy then invert in place
-      const bool oop = use_g1(n);
-      if (!oop) {
-        if (ew(act, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
-        if (it > 1 && ew(act, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
-      }
-      std::vector<int> mats2, which, slot, src;
-      for (int b : act) { mats2.push_back(b); which.push_back(0); slot.push_back(G_XI); src.push_back(G_B); }
-      if (it > 1)
-        for (int b : act) { mats2.push_back(b); which.push_back(1); slot.push_back(G_YI); src.push_back(G_Y); }
-      {
-        PhaseTimer pt(PH_INVERT, st);
-        if (invert(mats2, which, slot, oop ? &src : nullptr)) return LGM_ERR_CUDA;
-      }
-      // (the singular flags are read back together with the norms below: one sync per iteration)
-      // update + norms
-      std::vector<int> hs(batch);
-      for (int b = 0; b < batch; ++b) hs[b] = scaling[b];
-      CK(cudaMemcpyAsync(d_scaling, hs.data(), batch * 4, cudaMemcpyHostToDevice, st));
-      if (upload_ids(act)) return LGM_ERR_CUDA;
-      if (it == 1) CK(cudaMemsetAsync(d_logdet + batch, 0, batch * 8, st));
-      CK(cudaMemsetAsync(d_scal, 0, batch * 8, st));
-      CK(cudaMemsetAsync(d_scal2, 0, batch * 8, st));
-      DbArgs a;
-      a.S = S;
-      a.ids = d_ids;
-      a.xpiv = d_piv;
-      a.xstep = d_step;
-      a.ypiv = d_piv + (size_t)batch * n;
-      a.ystep = d_step + (size_t)batch * n;
-      a.xlog = d_logdet;
-      a.ylog = d_logdet + batch;
-      a.scaling = d_scaling;
-      a.first = it == 1;
-      a.change = d_scal;
-      a.size = d_scal2;
-      a.istat = d_istat;
-      a.batch = batch;
-      PhaseTimer pt(PH_DBUPD, st);
-      lgm_count_launch(), db_update_kernel<<<dim3((n + 127) / 128, (int)act.size()), 128, 0, st>>>(a);
-      CK(cudaGetLastError());
-      // change, size and the singular flags in one device-to-host copy (adjacent in the carve)
-      const char* span0 = (const char*)d_scal;
-      const size_t span = (size_t)((const char*)(d_istat + 2 * batch) - span0);
-      std::vector<char> rb(span);
-      CK(cudaMemcpyAsync(rb.data(), span0, span, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      std::vector<double> ch(batch), sz(batch);
-      std::vector<int> ist(2 * batch);
-      std::memcpy(ch.data(), rb.data(), batch * 8);
-      std::memcpy(sz.data(), rb.data() + ((const char*)d_scal2 - span0), batch * 8);
-      std::memcpy(ist.data(), rb.data() + ((const char*)d_istat - span0), 2 * batch * 4);
-      std::vector<int> next;
-      for (int b : act) {
-        iters[b] = it;
-        if (ist[b] || (it > 1 && ist[batch + b])) { status[b] = LGM_SINGULAR; iters[b] = it - 1; continue; }
-        const double tol = tol_in > 0.0 ? tol_in : 10.0 * n * LGM_UNIT_ROUNDOFF;
-        if (!std::isfinite(ch[b]) || !std::isfinite(sz[b])) { status[b] = LGM_NONFINITE; continue; }
-        if (sz[b] == 0.0) { status[b] = LGM_DB_NOCONV; continue; }
-        const double rel = ch[b] / sz[b];
-        auto note = [&](double x, double thr) { mm[b] = std::fmin(mm[b], std::fabs(x - thr) / std::fabs(thr)); };
-        note(rel, LGM_SCALING_SWITCH);
-        if (rel < LGM_SCALING_SWITCH) scaling[b] = 0;
-        note(rel, tol);
-        if (tol / 10.0 <= rel && rel <= 10.0 * tol) plateau[b]++;
-        if (rel <= tol) continue;  // converged
-        if (it == maxiter) { status[b] = LGM_DB_NOCONV; continue; }
-        next.push_back(b);
-      }
-      act = next;
-    }
-    return 0;
-  }
+enum {
+  LS_ALL = 0, LS_LIVE, LS_ACT, LS_ACTAI2, LS_ROOTS, LS_DB, LS_OK, LS_SEL, LS_NEED, LS_NEEDAI2, LS_CUR, LS_FAILED,
+  LS_POLY0,                   // LS_POLY0 + j, j = 1..K_MAX-1: selected matrices with k > j
+  LS_N = LS_POLY0 + LGM_K_MAX
 };
 
-}  // namespace
-
-// ============================================================================ Algorithm 1 host
-
-namespace {
-
-struct MState {
-  int status = 0, s = 0, db_iters = 0, nest = 0, passes = 0, products = 0, k = 0, plateau = 0, sweeps = 0;
-  bool finish = false, have_ai2 = false, post_fail = false;  // post_fail: non-finite L after the polynomial
-  double alpha_loop = 0.0, mm = INFINITY, nA = 0.0, cert = 0.0;
+// per-matrix Algorithm-1 state (oracle/driver.py _State + the running root / request)
+struct MDev {
+  int status, s, db_iters, nest, passes, products, k, plateau, sweeps;
+  int finish, have_ai2, post_fail;
+  int dbit, dbst, dbplat;           // running square root: iterations, status, plateau tests
+  int jcur, max_in;                 // select sweep
+  int am, need1, need2, adone;      // alpha request (power m) and its progress
+  unsigned cvalid;                  // estimate cache validity bits, by power
+  double dbmm;                      // running root's margin
+  double th, t1, Pm, t2, aout;      // alpha request threshold and terms
+  double alpha_loop, mm, nA, nI2, cert, cert_max;
   double cache[20];
-  unsigned cvalid = 0u;
-  void note(double x, double thr) {
-    double d = std::fabs(thr);
-    mm = std::fmin(mm, d > 0 ? std::fabs(x - thr) / d : std::fabs(x - thr));
+  __device__ void note(double x, double thr) {
+    const double d = fabs(thr);
+    mm = fmin(mm, d > 0 ? fabs(x - thr) / d : fabs(x - thr));
   }
-  bool le(double x, double thr) { note(x, thr); return x <= thr; }
+  __device__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
 };
 
-// Batched alpha (oracle/driver.py _alpha) for requests (matrix, m, theta).  AmI is in slot
-// G_AM, A_I2 in slot G_AP.  Returns alpha per request.
-int alpha_batched(Grid& G, std::vector<MState>& ms, const std::vector<int>& mats, const std::vector<int>& mv,
-                  const std::vector<double>& th, int itmax, std::vector<double>& out) {
-  const int R = (int)mats.size();
-  out.assign(R, 0.0);
-  std::vector<double> t1(R), Pm(R);
-  std::vector<int> need1;  // request indices needing the m-term estimate
-  // phase A
-  std::vector<int> ai2mats;
-  for (int r = 0; r < R; ++r) if (ms[mats[r]].have_ai2) ai2mats.push_back(mats[r]);
-  std::vector<double> nI2;
-  if (G.onenorms(ai2mats, G_AP, nI2)) return LGM_ERR_CUDA;
-  for (int r = 0; r < R; ++r) {
-    MState& M = ms[mats[r]];
-    const int m = mv[r];
-    if (M.have_ai2) {
-      const double r2 = std::sqrt(nI2[mats[r]]);
-      if (M.le(r2, th[r])) { t1[r] = r2; Pm[r] = std::pow(nI2[mats[r]], (double)(m / 2)); continue; }
-    }
-    if ((M.cvalid >> m) & 1u) { Pm[r] = M.cache[m]; t1[r] = std::pow(Pm[r], 1.0 / m); }
-    else need1.push_back(r);
-  }
-  auto run = [&](const std::vector<int>& reqs, bool second) -> int {
-    if (reqs.empty()) return 0;
-    // zero-matrix shortcut applies to est_power_norm only (matcore.py:309-310)
-    std::vector<int> zm_ai2, zm_ami;
-    for (int r : reqs) {
-      MState& M = ms[mats[r]];
-      bool product = second && M.have_ai2;
-      if (!product) (M.have_ai2 ? zm_ai2 : zm_ami).push_back(mats[r]);
-    }
-    std::vector<int> nz_ai2, nz_ami;
-    if (G.any_nonzero(zm_ai2, G_AP, nz_ai2)) return LGM_ERR_CUDA;
-    if (G.any_nonzero(zm_ami, G_AM, nz_ami)) return LGM_ERR_CUDA;
-    std::vector<const double*> M1, M2;
-    std::vector<int> p1, zero;
-    for (int r : reqs) {
-      const int b = mats[r], m = mv[r];
-      MState& M = ms[b];
-      if (M.have_ai2) {
-        M1.push_back(G.S.buf(b, G_AP));
-        p1.push_back(m / 2);
-        M2.push_back(second ? G.S.buf(b, G_AM) : nullptr);
-        zero.push_back(second ? 0 : (nz_ai2[b] ? 0 : 1));
-      } else {
-        M1.push_back(G.S.buf(b, G_AM));
-        p1.push_back(second ? m + 1 : m);
-        M2.push_back(nullptr);
-        zero.push_back(nz_ami[b] ? 0 : 1);
-      }
-    }
-    std::vector<double> est, mm;
-    std::vector<int> passes;
-    if (G.estimate(M1, p1, M2, zero, itmax, est, passes, mm)) return LGM_ERR_CUDA;
-    for (size_t q = 0; q < reqs.size(); ++q) {
-      const int r = reqs[q], b = mats[r], m = mv[r];
-      MState& M = ms[b];
-      M.nest++;
-      M.passes += passes[q];
-      M.mm = std::fmin(M.mm, mm[q]);
-      const int key = second ? m + 1 : m;
-      M.cache[key] = est[q];
-      M.cvalid |= 1u << key;
-    }
-    return 0;
-  };
-  if (run(need1, false)) return LGM_ERR_CUDA;
-  for (int r : need1) {
-    MState& M = ms[mats[r]];
-    Pm[r] = M.cache[mv[r]];
-    t1[r] = std::pow(Pm[r], 1.0 / mv[r]);
-  }
-  // phase B
-  std::vector<int> need2;
-  std::vector<double> t2(R, -1.0);
-  std::vector<char> doneq(R, 0);
-  for (int r = 0; r < R; ++r) {
-    MState& M = ms[mats[r]];
-    const int m = mv[r];
-    M.note(t1[r], th[r]);
-    if (t1[r] > th[r]) { out[r] = t1[r]; doneq[r] = 1; continue; }
-    const double bound = std::pow(Pm[r] * M.nA, 1.0 / (m + 1));
-    if (M.le(bound, th[r])) { t2[r] = bound; continue; }
-    if ((M.cvalid >> (m + 1)) & 1u) t2[r] = std::pow(M.cache[m + 1], 1.0 / (m + 1));
-    else need2.push_back(r);
-  }
-  if (run(need2, true)) return LGM_ERR_CUDA;
-  for (int r : need2) t2[r] = std::pow(ms[mats[r]].cache[mv[r] + 1], 1.0 / (mv[r] + 1));
-  for (int r = 0; r < R; ++r)
-    if (!doneq[r]) out[r] = std::fmax(t1[r], t2[r]);
-  return 0;
+// per-call pointers and parameters (the graph's kernels read them from the workspace)
+struct CallDesc {
+  const double* A;     // input batch (lgm_logm_f64: A; building blocks: their first operand)
+  const double* A2;    // est_product_norm's M2 / eval_degopt's first_product (nullable)
+  double* L;           // output batch (logm: L; sqrt_db: X; balance: B; degopt: Z)
+  long long ld;
+  lgm_report* rep;
+  int* iout;           // sqrt_db iters / est passes / balance sweeps / degopt products
+  int* iout2;          // sqrt_db status
+  double* dout;        // est values / balance scales
+  int p1, kblk, zero_shortcut, max_sweeps;
+  double tol;          // sqrt_db block tol (0 -> 10 n u)
+  int maxiter;
+  LgmParams P;
+};
+
+struct Ctl {  // device pointers into the workspace (fixed per workspace)
+  int n, batch, splits;
+  Slots S;
+  CallDesc* desc;
+  MDev* ms;
+  int* lists;   // [LS_N][batch]
+  int* cnt;     // [LS_N]
+  InvJob* jobs; // [2 batch]
+  EstJob* est;  // [batch]
+  int* piv;
+  int* step;
+  double* W;
+  double* logdet;
+  int* istat;
+  int* dead;    // == 1: the status of unused job-table slots
+  int* scaling;
+  double* nrm;
+  double* nrm2;
+  double* change;
+  double* size;
+  int* flag;
+  double* scale;
+  double* margin;
+  int* sweeps;
+  double* vec;
+  double* part;
+  int* hist;
+  __host__ __device__ DList list(int id) const { return DList{lists + (size_t)id * batch, cnt + id}; }
+  __host__ __device__ int* ids(int id) const { return lists + (size_t)id * batch; }
+};
+
+size_t ctl_bytes(int64_t n, int64_t batch) {
+  const int64_t splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  size_t s = 0;
+  auto add = [&](size_t b) { s += (b + 255) & ~size_t(255); };
+  add((size_t)batch * NBUF * n * n * 8);   // slots
+  add(sizeof(CallDesc));
+  add(batch * sizeof(MDev));
+  add((size_t)LS_N * batch * 4);
+  add(LS_N * 4);
+  add(2 * batch * sizeof(InvJob));
+  add(batch * sizeof(EstJob));
+  add(2 * batch * n * 4);                  // piv
+  add(2 * batch * n * 4);                  // step
+  add(12 * batch * NB * n * 8);            // W
+  add(2 * batch * 8);                      // logdet
+  add(2 * batch * 4);                      // istat
+  add(4);                                  // dead
+  add(batch * 4);                          // scaling
+  for (int q = 0; q < 4; ++q) add(batch * 8);  // nrm, nrm2, change, size
+  add(batch * 4);                          // flag
+  add((size_t)batch * n * 8);              // scale
+  add(batch * 8);                          // margin
+  add(batch * 4);                          // sweeps
+  add((size_t)batch * 4 * n * 8);          // vec
+  add((size_t)batch * splits * 2 * n * 8); // part
+  add(batch * 16 * 4);                     // hist
+  return s;
 }
 
-int first_index(MState& M, double x, const LgmParams& P) {
+Ctl ctl_carve(void* ws, int n, int batch) {
+  Ctl c{};
+  c.n = n;
+  c.batch = batch;
+  c.splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  char* p = (char*)ws;
+  auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return (void*)r; };
+  c.S.ws = (double*)take((size_t)batch * NBUF * n * n * 8);
+  c.S.n = n;
+  c.desc = (CallDesc*)take(sizeof(CallDesc));
+  c.ms = (MDev*)take(batch * sizeof(MDev));
+  c.lists = (int*)take((size_t)LS_N * batch * 4);
+  c.cnt = (int*)take(LS_N * 4);
+  c.jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
+  c.est = (EstJob*)take(batch * sizeof(EstJob));
+  c.piv = (int*)take(2 * (size_t)batch * n * 4);
+  c.step = (int*)take(2 * (size_t)batch * n * 4);
+  c.W = (double*)take(12 * (size_t)batch * NB * n * 8);
+  c.logdet = (double*)take(2 * batch * 8);
+  c.istat = (int*)take(2 * batch * 4);
+  c.dead = (int*)take(4);
+  c.scaling = (int*)take(batch * 4);
+  c.nrm = (double*)take(batch * 8);
+  c.nrm2 = (double*)take(batch * 8);
+  c.change = (double*)take(batch * 8);
+  c.size = (double*)take(batch * 8);
+  c.flag = (int*)take(batch * 4);
+  c.scale = (double*)take((size_t)batch * n * 8);
+  c.margin = (double*)take(batch * 8);
+  c.sweeps = (int*)take(batch * 4);
+  c.vec = (double*)take((size_t)batch * 4 * n * 8);
+  c.part = (double*)take((size_t)batch * c.splits * 2 * n * 8);
+  c.hist = (int*)take(batch * 16 * 4);
+  return c;
+}
+
+// ------------------------------------------------------------------ decide-kernel helpers
+constexpr int CT = 1024;  // decide kernels: one CTA of CT threads
+
+// Order-preserving block-wide append: every thread of the CTA calls it (uniformly) with its
+// predicate; returns the slot for predicated threads and advances `off` by the total.
+__device__ int blk_append(bool pred, int* s_w, int& off) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) s_w[warp] = __popc(m);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < nw ? s_w[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    s_w[lane] = incl - v;
+    if (lane == 31) s_w[32] = incl;
+  }
+  __syncthreads();
+  const int pos = off + s_w[warp] + __popc(m & ((1u << lane) - 1u));
+  off += s_w[32];
+  return pos;
+}
+
+// Loop over the entries of list `src` in chunks of CT (uniform trip count), b = -1 off the end.
+#define FOR_LIST(c, src)                                                           \
+  const int* src_ids_ = (c).ids(src);                                             \
+  const int src_n_ = (c).cnt[src];                                                \
+  for (int base_ = 0; base_ < src_n_; base_ += CT) {                              \
+    const int e_ = base_ + (int)threadIdx.x;                                      \
+    const int b = e_ < src_n_ ? src_ids_[e_] : -1;
+
+__device__ __forceinline__ double dpow(double x, double y) { return pow(x, y); }
+
+__device__ unsigned long long g_exec_nodes;  // kernel nodes executed inside graphs (lgm_launch_count)
+
+__device__ __forceinline__ void count_nodes(int nodes) {
+  if (threadIdx.x == 0) atomicAdd(&g_exec_nodes, (unsigned long long)nodes);
+}
+
+// ------------------------------------------------------------------ setup / init / load
+__global__ void setup_kernel(CallDesc* d, CallDesc v) { *d = v; }
+
+__global__ void __launch_bounds__(CT) ctl_init_kernel(Ctl c) {
+  for (int b = threadIdx.x; b < c.batch; b += CT) {
+    MDev& M = c.ms[b];
+    memset(&M, 0, sizeof(MDev));
+    M.mm = INFINITY;
+    M.dbmm = INFINITY;
+    c.ids(LS_ALL)[b] = b;
+    c.flag[b] = 0;
+    c.margin[b] = INFINITY;
+    c.sweeps[b] = 0;
+  }
+  if (threadIdx.x == 0) {
+    c.cnt[LS_ALL] = c.batch;
+    for (int l = 1; l < LS_N; ++l) c.cnt[l] = 0;
+    *c.dead = 1;
+  }
+}
+
+__global__ void fill_kernel(double* p, size_t count, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// as_square (matcore.py:64-65): non-finite input -> NONFINITE; the rest is the live list
+__global__ void __launch_bounds__(CT) decide_live_kernel(Ctl c) {
+  __shared__ int s_w[33];
+  int off = 0;
+  FOR_LIST(c, LS_ALL)
+    const bool bad = b >= 0 && c.flag[b];
+    if (bad) c.ms[b].status = LGM_NONFINITE;
+    const int pos = blk_append(b >= 0 && !bad, s_w, off);
+    if (b >= 0 && !bad) c.ids(LS_LIVE)[pos] = b;
+  }
+  if (threadIdx.x == 0) c.cnt[LS_LIVE] = off;
+}
+
+// finish = ||B - I||_1 <= Theta_K, after balancing
+__global__ void __launch_bounds__(CT) decide_start_kernel(Ctl c) {
+  const LgmParams& P = c.desc->P;
+  const double thK = P.theta[P.max_k - 1];
+  FOR_LIST(c, LS_LIVE)
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      M.sweeps = c.sweeps[b];
+      M.mm = c.margin[b];
+      M.alpha_loop = c.nrm[b];
+      M.finish = M.le(c.nrm[b], thK);
+    }
+  }
+}
+
+__device__ __forceinline__ bool scal_active(const MDev& M, const LgmParams& P) {
+  return !M.finish && M.status == 0 && M.s < P.maxiter_s;
+}
+
+// scaling-loop head: act = live matrices still scaling; act_ai2 = those with A_I2
+__global__ void __launch_bounds__(CT) decide_act_kernel(Ctl c) {
+  __shared__ int s_w[33];
+  const LgmParams& P = c.desc->P;
+  int off = 0, off2 = 0;
+  FOR_LIST(c, LS_LIVE)
+    const bool a = b >= 0 && scal_active(c.ms[b], P);
+    const int pos = blk_append(a, s_w, off);
+    if (a) c.ids(LS_ACT)[pos] = b;
+    const bool a2 = a && c.ms[b].have_ai2;
+    const int pos2 = blk_append(a2, s_w, off2);
+    if (a2) c.ids(LS_ACTAI2)[pos2] = b;
+  }
+  if (threadIdx.x == 0) { c.cnt[LS_ACT] = off; c.cnt[LS_ACTAI2] = off2; }
+}
+
+// ------------------------------------------------------------------ alpha (A.2)
+// The request of matrix b: power m = M.am (even), threshold M.th, nA = M.nA, nI2 = M.nI2.
+__device__ void est_slot(Ctl& c, int q, int b, const double* M1, int p1, const double* M2, int zchk, int key) {
+  EstJob& J = c.est[q];
+  J.M1 = M1;
+  J.M2 = M2;
+  J.p1 = p1;
+  J.live = 1;
+  J.zchk = zchk;
+  J.nzf = 0;
+  J.owner = b;
+  J.key = key;
+  J.V0 = c.vec + (size_t)q * 4 * c.n;
+  J.V1 = J.V0 + 2 * c.n;
+  J.part = c.part + (size_t)q * c.splits * 2 * c.n;
+  J.hist = c.hist + q * 16;
+}
+__device__ void est_kill_tail(Ctl& c, int from) {
+  for (int q = from + (int)threadIdx.x; q < c.batch; q += CT) c.est[q].live = 0;
+}
+// fold the finished estimates of the table into the owners' state (counters, margin, cache)
+__device__ void est_absorb(Ctl& c, int count) {
+  for (int q = threadIdx.x; q < count; q += CT) {
+    const EstJob& J = c.est[q];
+    MDev& M = c.ms[J.owner];
+    M.nest++;
+    M.passes += J.passes;
+    M.mm = fmin(M.mm, J.mm);
+    M.cache[J.key] = J.est;
+    M.cvalid |= 1u << J.key;
+  }
+}
+
+// phase A: Eq. 27 skip, cached p_m, else an estimate of ||A_I2^{m/2}|| or ||(A - I)^m||
+__global__ void __launch_bounds__(CT) alpha_a_kernel(Ctl c, int lst) {
+  __shared__ int s_w[33];
+  int off = 0;
+  FOR_LIST(c, lst)
+    bool need = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      const int m = M.am;
+      M.adone = 0;
+      M.need1 = M.need2 = 0;
+      bool skip = false;
+      if (M.have_ai2) {
+        const double r2 = sqrt(M.nI2);
+        if (M.le(r2, M.th)) { M.t1 = r2; M.Pm = dpow(M.nI2, (double)(m / 2)); skip = true; }
+      }
+      if (!skip) {
+        if ((M.cvalid >> m) & 1u) { M.Pm = M.cache[m]; M.t1 = dpow(M.Pm, 1.0 / m); }
+        else need = true;
+      }
+      M.need1 = need;
+    }
+    const int q = blk_append(need, s_w, off);
+    if (need) {
+      const MDev& M = c.ms[b];
+      if (M.have_ai2) est_slot(c, q, b, c.S.buf(b, G_AP), M.am / 2, nullptr, 1, M.am);
+      else est_slot(c, q, b, c.S.buf(b, G_AM), M.am, nullptr, 1, M.am);
+    }
+  }
+  __syncthreads();
+  est_kill_tail(c, off);
+  if (threadIdx.x == 0) c.cnt[LS_NEED] = off;
+}
+
+// phase B: absorb the m-term estimates; t1 > Theta early exit; Eq. 28 bound; cached or new
+// (m+1)-term estimate (product form ||A_I2^{m/2} (A - I)|| when A_I2 exists)
+__global__ void __launch_bounds__(CT) alpha_b_kernel(Ctl c, int lst) {
+  __shared__ int s_w[33];
+  est_absorb(c, c.cnt[LS_NEED]);
+  __syncthreads();
+  int off = 0;
+  FOR_LIST(c, lst)
+    bool need = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      const int m = M.am;
+      if (M.need1) { M.Pm = M.cache[m]; M.t1 = dpow(M.Pm, 1.0 / m); }
+      M.note(M.t1, M.th);
+      if (M.t1 > M.th) {
+        M.aout = M.t1;
+        M.adone = 1;
+      } else {
+        const double bound = dpow(M.Pm * M.nA, 1.0 / (m + 1));
+        if (M.le(bound, M.th)) M.t2 = bound;
+        else if ((M.cvalid >> (m + 1)) & 1u) M.t2 = dpow(M.cache[m + 1], 1.0 / (m + 1));
+        else need = true;
+      }
+      M.need2 = need;
+    }
+    const int q = blk_append(need, s_w, off);
+    if (need) {
+      const MDev& M = c.ms[b];
+      if (M.have_ai2) est_slot(c, q, b, c.S.buf(b, G_AP), M.am / 2, c.S.buf(b, G_AM), 0, M.am + 1);
+      else est_slot(c, q, b, c.S.buf(b, G_AM), M.am + 1, nullptr, 1, M.am + 1);
+    }
+  }
+  __syncthreads();
+  est_kill_tail(c, off);
+  if (threadIdx.x == 0) c.cnt[LS_NEED] = off;
+}
+
+__global__ void __launch_bounds__(CT) alpha_c_kernel(Ctl c, int lst) {
+  est_absorb(c, c.cnt[LS_NEED]);
+  __syncthreads();
+  FOR_LIST(c, lst)
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      const int m = M.am;
+      if (M.need2) M.t2 = dpow(M.cache[m + 1], 1.0 / (m + 1));
+      if (!M.adone) M.aout = fmax(M.t1, M.t2);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ scaling loop (A.1 step 5)
+// nA / nI2 from the norms; the scaling-loop alpha request (m_K, Theta_K)
+__global__ void __launch_bounds__(CT) scal_req_kernel(Ctl c) {
+  const LgmParams& P = c.desc->P;
+  const int K = P.max_k;
+  FOR_LIST(c, LS_ACT)
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      M.nA = c.nrm[b];
+      if (M.have_ai2) M.nI2 = c.nrm2[b];
+      M.am = P.order[K - 1];
+      M.th = P.theta[K - 1];
+    }
+  }
+}
+
+// finish = alpha <= Theta_K; roots = matrices taking another square root
+__global__ void __launch_bounds__(CT) decide_roots_kernel(Ctl c) {
+  __shared__ int s_w[33];
+  const LgmParams& P = c.desc->P;
+  const double thK = P.theta[P.max_k - 1];
+  int off = 0;
+  FOR_LIST(c, LS_ACT)
+    bool r = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      M.alpha_loop = M.aout;
+      M.finish = M.le(M.aout, thK);
+      r = !M.finish;
+      if (r) { M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbmm = INFINITY; c.scaling[b] = 1; }
+    }
+    const int pos = blk_append(r, s_w, off);
+    if (r) c.ids(LS_ROOTS)[pos] = b;
+  }
+  if (threadIdx.x == 0) { c.cnt[LS_ROOTS] = off; c.cnt[LS_DB] = off; }
+  __syncthreads();
+  for (int e = threadIdx.x; e < off; e += CT) c.ids(LS_DB)[e] = c.ids(LS_ROOTS)[e];
+}
+
+// after the roots: fold the DB outcome; s++ and A_I2 pending for the converged ones; the
+// scaling loop continues while some live matrix is still active
+__global__ void __launch_bounds__(CT) decide_post_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes) {
+  __shared__ int s_w[33];
+  __shared__ int s_any;
+  const LgmParams& P = c.desc->P;
+  if (threadIdx.x == 0) s_any = 0;
+  int off = 0;
+  FOR_LIST(c, LS_ROOTS)
+    bool ok = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      M.db_iters += M.dbit;
+      M.mm = fmin(M.mm, M.dbmm);
+      M.plateau += M.dbplat;
+      if (M.dbst) {
+        M.status = M.dbst;
+      } else {
+        M.s++;
+        M.have_ai2 = 1;
+        M.cvalid = 0u;
+        ok = true;
+      }
+    }
+    const int pos = blk_append(ok, s_w, off);
+    if (ok) c.ids(LS_OK)[pos] = b;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < c.cnt[LS_LIVE]; e += CT)
+    if (scal_active(c.ms[c.ids(LS_LIVE)[e]], P)) s_any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.cnt[LS_OK] = off;
+    cudaGraphSetConditional(h, s_any ? 1u : 0u);
+  }
+  count_nodes(nodes);
+}
+
+// ------------------------------------------------------------------ DB square root (sqrtm.py:27-78)
+// Job table for this iteration: X of every DB-active matrix, then (it > 1) Y; unused slots
+// carry M = nullptr and the always-1 status.  Also zeroes the per-iteration accumulators.
+__global__ void __launch_bounds__(CT) build_jobs_kernel(Ctl c, int first, int oop) {
+  const int na = c.cnt[LS_DB];
+  const int nj = first ? na : 2 * na;
+  const int cap = first ? c.batch : 2 * c.batch;
+  for (int q = threadIdx.x; q < cap; q += CT) {
+    InvJob J{};
+    if (q < nj) {
+      const int w = q < na ? 0 : 1;
+      const int b = c.ids(LS_DB)[w ? q - na : q];
+      J.M = c.S.buf(b, w ? G_YI : G_XI);
+      J.Src = oop ? c.S.buf(b, w ? G_Y : G_B) : nullptr;
+      J.piv = c.piv + ((size_t)w * c.batch + b) * c.n;
+      J.rowstep = c.step + ((size_t)w * c.batch + b) * c.n;
+      J.Wb = c.W + ((size_t)w * c.batch + b) * NB * c.n;
+      J.wst = (long long)2 * c.batch * NB * c.n;
+      J.logdet = c.logdet + w * c.batch + b;
+      J.status = c.istat + w * c.batch + b;
+      if (w == 0) {
+        c.change[b] = 0.0;
+        c.size[b] = 0.0;
+        if (first) c.logdet[c.batch + b] = 0.0;
+      }
+    } else {
+      J.M = nullptr;
+      J.status = c.dead;
+    }
+    c.jobs[q] = J;
+  }
+}
+
+// sqrt_db building block: every live matrix takes one root
+__global__ void __launch_bounds__(CT) decide_db_start_kernel(Ctl c) {
+  const int na = c.cnt[LS_LIVE];
+  for (int e = threadIdx.x; e < na; e += CT) {
+    const int b = c.ids(LS_LIVE)[e];
+    MDev& M = c.ms[b];
+    M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbmm = INFINITY;
+    c.scaling[b] = 1;
+    c.ids(LS_ROOTS)[e] = b;
+    c.ids(LS_DB)[e] = b;
+  }
+  if (threadIdx.x == 0) { c.cnt[LS_ROOTS] = na; c.cnt[LS_DB] = na; }
+}
+
+// stop test of the iteration just done (sqrtm.py:66-78), mu switch, next DB list
+__global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes, int first,
+                                                        int block_mode) {
+  __shared__ int s_w[33];
+  const CallDesc& D = *c.desc;
+  const int n = c.n;
+  const double tol_in = block_mode ? D.tol : D.P.db_tol;
+  const int maxiter = block_mode ? D.maxiter : D.P.db_maxiter;
+  const double tol = tol_in > 0.0 ? tol_in : 10.0 * n * LGM_UNIT_ROUNDOFF;
+  int off = 0;
+  FOR_LIST(c, LS_DB)
+    bool next = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      const int it = ++M.dbit;
+      const bool sing = c.istat[b] || (!first && c.istat[c.batch + b]);
+      const double ch = c.change[b], sz = c.size[b];
+      if (sing) {
+        M.dbst = LGM_SINGULAR;
+        M.dbit = it - 1;
+      } else if (!isfinite(ch) || !isfinite(sz)) {
+        M.dbst = LGM_NONFINITE;
+      } else if (sz == 0.0) {
+        M.dbst = LGM_DB_NOCONV;
+      } else {
+        const double rel = ch / sz;
+        auto note = [&](double x, double thr) { M.dbmm = fmin(M.dbmm, fabs(x - thr) / fabs(thr)); };
+        note(rel, LGM_SCALING_SWITCH);
+        if (rel < LGM_SCALING_SWITCH) c.scaling[b] = 0;
+        note(rel, tol);
+        if (tol / 10.0 <= rel && rel <= 10.0 * tol) M.dbplat++;
+        if (rel > tol) {
+          if (it == maxiter) M.dbst = LGM_DB_NOCONV;
+          else next = true;
+        }
+      }
+    }
+    const int pos = blk_append(next, s_w, off);
+    if (next) c.ids(LS_DB)[pos] = b;  // in place: pos <= e_, ascending, read before written
+  }
+  if (threadIdx.x == 0) {
+    c.cnt[LS_DB] = off;
+    cudaGraphSetConditional(h, off > 0 ? 1u : 0u);
+  }
+  count_nodes(nodes);
+}
+
+// ------------------------------------------------------------------ select_order (A.3)
+__global__ void __launch_bounds__(CT) decide_sel_kernel(Ctl c) {
+  __shared__ int s_w[33];
+  int off = 0, off2 = 0;
+  FOR_LIST(c, LS_LIVE)
+    bool sel = false, need = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      if (M.status == 0 && !M.finish) M.status = LGM_SCALING_MAXITER;
+      sel = M.status == 0;
+      need = sel && !M.have_ai2;
+    }
+    const int pos = blk_append(sel, s_w, off);
+    if (sel) c.ids(LS_SEL)[pos] = b;
+    const int pos2 = blk_append(need, s_w, off2);
+    if (need) c.ids(LS_NEEDAI2)[pos2] = b;
+  }
+  if (threadIdx.x == 0) { c.cnt[LS_SEL] = off; c.cnt[LS_NEEDAI2] = off2; }
+}
+
+__device__ int first_index(MDev& M, double x, const LgmParams& P) {
   for (int j = 1; j <= P.max_k; ++j)
     if (M.le(x, P.theta[j - 1])) return j;
   return P.max_k;
 }
 
-}  // namespace
-
-size_t lgm_grid_workspace_bytes(int64_t n, int64_t batch) { return Grid::bytes(n, batch); }
-
-int lgm_grid_logm(const double* A, double* L, int64_t n64, int64_t batch64, int64_t ld, const LgmParams& P,
-                  lgm_report* rep, void* ws, cudaStream_t st) {
-  const int n = (int)n64, batch = (int)batch64;
-  Grid G;
-  G.st = st;
-  G.carve(ws, n, batch);
-  std::vector<MState> ms(batch);
-  std::vector<int> all(batch);
-  for (int b = 0; b < batch; ++b) all[b] = b;
-  // load + finiteness (as_square, matcore.py:64-65)
-  CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
-  std::vector<int> bad(batch);
-  CK(cudaMemcpyAsync(bad.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  std::vector<int> live;
-  for (int b = 0; b < batch; ++b) {
-    if (bad[b]) ms[b].status = LGM_NONFINITE;
-    else live.push_back(b);
-  }
-  // balance (matcore.py:180-215)
-  {
-    std::vector<double> mm0(batch, INFINITY);
-    CK(cudaMemcpyAsync(G.d_margin, mm0.data(), batch * 8, cudaMemcpyHostToDevice, st));
-    std::vector<double> ones((size_t)batch * n, 1.0);
-    CK(cudaMemcpyAsync(G.d_scale, ones.data(), ones.size() * 8, cudaMemcpyHostToDevice, st));
-    if (P.balance && !live.empty()) {
-      if (G.upload_ids(live)) return LGM_ERR_CUDA;
-      PhaseTimer pt(PH_BALANCE, st);
-      lgm_count_launch(), balance_kernel_g<<<(int)live.size(), bal_threads(n), bal_smem(n), st>>>(G.S, G.d_ids, G.d_scale, G.d_sweeps, 100, G.d_margin);
-      CK(cudaGetLastError());
-      std::vector<int> sw(batch);
-      CK(cudaMemcpyAsync(sw.data(), G.d_sweeps, batch * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(mm0.data(), G.d_margin, batch * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      for (int b : live) { ms[b].sweeps = sw[b]; ms[b].mm = mm0[b]; }
-    }
-  }
+// min_im (Eqs. 29-31 + tabmin_im), max_in (Eqs. 32-34); immediate choice or the sweep list
+__global__ void __launch_bounds__(CT) select_init_kernel(Ctl c, cudaGraphConditionalHandle h) {
+  __shared__ int s_w[33];
+  const LgmParams& P = c.desc->P;
   const int K = P.max_k;
-  const double thK = P.theta[K - 1];
   const int mK = P.order[K - 1];
-  // finish = ||B - I||_1 <= Theta_K
-  if (G.ew(live, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
-  std::vector<double> nrm;
-  if (G.onenorms(live, G_AM, nrm)) return LGM_ERR_CUDA;
-  for (int b : live) {
-    ms[b].alpha_loop = nrm[b];
-    ms[b].finish = ms[b].le(nrm[b], thK);
-  }
-  // scaling loop
-  while (true) {
-    std::vector<int> act;
-    for (int b : live)
-      if (!ms[b].finish && ms[b].status == 0 && ms[b].s < P.maxiter_s) act.push_back(b);
-    if (act.empty()) break;
-    if (G.ew(act, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
-    if (G.onenorms(act, G_AM, nrm)) return LGM_ERR_CUDA;
-    for (int b : act) ms[b].nA = nrm[b];
-    std::vector<int> mv(act.size(), mK);
-    std::vector<double> th(act.size(), thK), al;
-    {
-      PhaseTimer pt(PH_ALPHA, st);
-      if (alpha_batched(G, ms, act, mv, th, P.est_itmax, al)) return LGM_ERR_CUDA;
-    }
-    std::vector<int> roots;
-    for (size_t q = 0; q < act.size(); ++q) {
-      MState& M = ms[act[q]];
-      M.alpha_loop = al[q];
-      M.finish = M.le(al[q], thK);
-      if (!M.finish) roots.push_back(act[q]);
-    }
-    if (roots.empty()) continue;
-    if (G.ew(roots, 1, G_AP, G_B, G_B)) return LGM_ERR_CUDA;  // A_prev = B
-    std::vector<int> dst(batch, 0), dit(batch, 0), plat(batch, 0);
-    std::vector<double> dmm(batch, INFINITY);
-    if (G.sqrt_db(roots, P.db_tol, P.db_maxiter, dst, dit, dmm, plat)) return LGM_ERR_CUDA;
-    std::vector<int> ok;
-    for (int b : roots) {
-      MState& M = ms[b];
-      M.db_iters += dit[b];
-      M.mm = std::fmin(M.mm, dmm[b]);
-      M.plateau += plat[b];
-      if (dst[b]) { M.status = dst[b]; continue; }
-      M.s++;
-      M.have_ai2 = true;
-      M.cvalid = 0u;
-      ok.push_back(b);
-    }
-    if (G.ew(ok, 3, G_AP, G_AP, G_B)) return LGM_ERR_CUDA;  // A_I2 = A_prev - 2B + I
-  }
-  // select (oracle/driver.py _select) for the finished matrices
-  std::vector<int> sel;
-  for (int b : live) {
-    MState& M = ms[b];
-    if (M.status == 0 && !M.finish) M.status = LGM_SCALING_MAXITER;
-    if (M.status == 0) sel.push_back(b);
-  }
-  if (G.ew(sel, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
-  if (G.onenorms(sel, G_AM, nrm)) return LGM_ERR_CUDA;
-  std::vector<int> need_ai2;
-  for (int b : sel) {
-    ms[b].nA = nrm[b];
-    if (!ms[b].have_ai2) need_ai2.push_back(b);
-  }
-  if (!need_ai2.empty()) {  // s = 0: A_I2 = (B - I)^2, one product
-    if (G.upload_ids(need_ai2)) return LGM_ERR_CUDA;
-    CombSpec cs{};
-    cs.nterm = 1;
-    cs.node[0] = G_AM;
-    cs.coef[0] = 1.0;
-    const int tiles = (n + TM - 1) / TM;
-    if ((n & 1) == 0) {
-      if (G.gemm_plain((int)need_ai2.size(), G_AM, G_AM, G_AP)) return LGM_ERR_CUDA;
-    } else {
-      lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, (int)need_ai2.size()), 128, 0, st>>>(G.S, G.d_ids, cs, G_AM, G_AP);
-    }
-    CK(cudaGetLastError());
-    for (int b : need_ai2) { ms[b].products++; ms[b].have_ai2 = true; }
-  }
-  {
-    std::vector<double> nI2;
-    if (G.onenorms(sel, G_AP, nI2)) return LGM_ERR_CUDA;
-    std::vector<int> min_im(batch), max_in(batch);
-    std::vector<double> cert_max(batch);
-    std::vector<int> cur;  // matrices still sweeping
-    for (int b : sel) {
-      MState& M = ms[b];
-      const double r2 = std::sqrt(nI2[b]);
+  int off = 0;
+  FOR_LIST(c, LS_SEL)
+    bool cur = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      M.nA = c.nrm[b];
+      if (!M.have_ai2) { M.products++; M.have_ai2 = 1; }  // s = 0: A_I2 = (B - I)^2
+      M.nI2 = c.nrm2[b];
+      const double r2 = sqrt(M.nI2);
       int mi;
       if ((M.cvalid >> mK) & 1u) {
-        mi = first_index(M, std::pow(M.cache[mK], 1.0 / mK), P);
-        if ((M.cvalid >> (mK + 1)) & 1u) mi = std::max(mi, first_index(M, std::pow(M.cache[mK + 1], 1.0 / (mK + 1)), P));
+        mi = first_index(M, dpow(M.cache[mK], 1.0 / mK), P);
+        if ((M.cvalid >> (mK + 1)) & 1u) mi = max(mi, first_index(M, dpow(M.cache[mK + 1], 1.0 / (mK + 1)), P));
       } else {
         mi = first_index(M, r2, P);
       }
-      static const int tabmin[5] = {1, 2, 3, 4, 4};
+      const int tabmin[LGM_K_MAX] = {1, 2, 3, 4, 4};
       mi = tabmin[mi - 1];
       M.note(r2, P.theta[0]);
-      mi = (r2 > P.theta[0]) ? std::max(mi, 2) : 1;
+      mi = (r2 > P.theta[0]) ? max(mi, 2) : 1;
       int mx = K;
       double mb = -1.0;
       bool found = false;
       for (int j = 1; j <= K; ++j) {
         const int m = P.order[j - 1];
-        const double bnd = std::pow(std::pow(nI2[b], (double)(m / 2)) * M.nA, 1.0 / (m + 1));
+        const double bnd = dpow(dpow(M.nI2, (double)(m / 2)) * M.nA, 1.0 / (m + 1));
         if (M.le(bnd, P.theta[j - 1])) { mx = j; mb = bnd; found = true; break; }
       }
-      cert_max[b] = found ? mb : M.alpha_loop;
-      min_im[b] = mi;
-      max_in[b] = mx;
-      if (mi >= mx) { M.k = mx; M.cert = cert_max[b]; }
-      else cur.push_back(b);
-    }
-    std::vector<int> jcur(batch);
-    for (int b : cur) jcur[b] = min_im[b];
-    while (!cur.empty()) {
-      std::vector<int> mv;
-      std::vector<double> th, al;
-      for (int b : cur) { mv.push_back(P.order[jcur[b] - 1]); th.push_back(P.theta[jcur[b] - 1]); }
-      PhaseTimer pt(PH_SELECT, st);
-      if (alpha_batched(G, ms, cur, mv, th, P.est_itmax, al)) return LGM_ERR_CUDA;
-      std::vector<int> next;
-      for (size_t q = 0; q < cur.size(); ++q) {
-        const int b = cur[q], j = jcur[b];
-        MState& M = ms[b];
-        if (M.le(al[q], P.theta[j - 1])) { M.k = j; M.cert = al[q]; continue; }
-        if (M.le(al[q], P.theta[j])) { M.k = j + 1; M.cert = al[q]; continue; }
-        if (j + 1 < max_in[b]) { jcur[b] = j + 1; next.push_back(b); }
-        else { M.k = max_in[b]; M.cert = cert_max[b]; }
-      }
-      cur = next;
-    }
-  }
-  // polynomial: P2 = I - B (slot G_B), P3 = A_I2 (G_AP), R temp (G_Y), P4.. in G_XI, G_YI, G_P6, G_P7
-  PhaseTimer pt_poly(PH_POLY, st);
-  if (G.ew(sel, 4, G_B, G_B, G_B)) return LGM_ERR_CUDA;
-  const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
-  for (int kk = 1; kk <= K; ++kk) {
-    std::vector<int> grp;
-    for (int b : sel)
-      if (ms[b].k == kk) grp.push_back(b);
-    if (grp.empty()) continue;
-    const double* base = P.coef + P.coef_off[kk - 1];
-    auto spec = [&](const double* row, int nn) {
-      CombSpec cs{};
-      cs.c0 = row[0];
-      for (int t = 2; t <= nn; ++t)
-        if (row[t - 1] != 0.0) { cs.node[cs.nterm] = node_slot[t]; cs.coef[cs.nterm] = row[t - 1]; cs.nterm++; }
-      return cs;
-    };
-    const int tiles = (n + TM - 1) / TM;
-    int nn = 3;
-    for (int j = 1; j < kk; ++j) {
-      const double* lrow = base + j * (j + 3) / 2;
-      const double* rrow = base + kk * (kk + 3) / 2 + j * (j + 3) / 2;
-      if (G.upload_ids(grp)) return LGM_ERR_CUDA;
-      CombSpec rs = spec(rrow, nn);
-      lgm_count_launch(), combine_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
-      CombSpec ls = spec(lrow, nn);
-      if ((n & 1) == 0) {  // materialise L too (slot G_AM is free after select), then a plain GEMM
-        lgm_count_launch(), combine_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, ls, G_AM);
-        if (G.gemm_plain((int)grp.size(), G_AM, G_Y, node_slot[nn + 1])) return LGM_ERR_CUDA;
+      M.cert_max = found ? mb : M.alpha_loop;
+      M.max_in = mx;
+      if (mi >= mx) {
+        M.k = mx;
+        M.cert = M.cert_max;
       } else {
-        lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, (int)grp.size()), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
+        cur = true;
+        M.jcur = mi;
+        M.am = P.order[mi - 1];
+        M.th = P.theta[mi - 1];
       }
-      CK(cudaGetLastError());
-      nn++;
-      for (int b : grp) ms[b].products++;
     }
-    const double* orow = base + kk * (kk + 3);
-    CombSpec os = spec(orow, nn);
-    std::vector<double> mult(batch, 0.0);
-    for (int b : grp) mult[b] = -std::ldexp(1.0, ms[b].s);
-    CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
-    if (G.upload_ids(grp)) return LGM_ERR_CUDA;
-    CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
-    lgm_count_launch(), final_kernel<<<G.ew_grid((int)grp.size()), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale,
-                                                                                P.balance, L, ld, G.d_iflag);
-    CK(cudaGetLastError());
-    std::vector<int> nf(batch);
-    CK(cudaMemcpyAsync(nf.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    // a non-finite logarithm (estimator overflow upstream, norms ~1e300) is reported, with
-    // the k / products / alpha of the run that produced it
-    for (int b : grp)
-      if (nf[b]) { ms[b].status = LGM_NONFINITE; ms[b].post_fail = true; }
+    const int pos = blk_append(cur, s_w, off);
+    if (cur) c.ids(LS_CUR)[pos] = b;
   }
+  if (threadIdx.x == 0) {
+    c.cnt[LS_CUR] = off;
+    cudaGraphSetConditional(h, off > 0 ? 1u : 0u);
+  }
+}
+
+__global__ void __launch_bounds__(CT) select_step_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes) {
+  __shared__ int s_w[33];
+  const LgmParams& P = c.desc->P;
+  int off = 0;
+  FOR_LIST(c, LS_CUR)
+    bool next = false;
+    if (b >= 0) {
+      MDev& M = c.ms[b];
+      const int j = M.jcur;
+      if (M.le(M.aout, P.theta[j - 1])) { M.k = j; M.cert = M.aout; }
+      else if (M.le(M.aout, P.theta[j])) { M.k = j + 1; M.cert = M.aout; }
+      else if (j + 1 < M.max_in) { M.jcur = j + 1; M.am = P.order[j]; M.th = P.theta[j]; next = true; }
+      else { M.k = M.max_in; M.cert = M.cert_max; }
+    }
+    const int pos = blk_append(next, s_w, off);
+    if (next) c.ids(LS_CUR)[pos] = b;
+  }
+  if (threadIdx.x == 0) {
+    c.cnt[LS_CUR] = off;
+    cudaGraphSetConditional(h, off > 0 ? 1u : 0u);
+  }
+  count_nodes(nodes);
+}
+
+// ------------------------------------------------------------------ polynomial (schemes.py:91-126)
+// node slots: P2 = I - B (G_B), P3 = A_I2 (G_AP), P4.. (G_XI, G_YI, G_P6, G_P7); R temp G_Y,
+// L temp G_AM.  Scheme k_b's coefficient rows come from the call's parameter block.
+__constant__ int c_node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+
+__global__ void __launch_bounds__(CT) decide_poly_kernel(Ctl c) {
+  __shared__ int s_w[33];
+  for (int j = 1; j < LGM_K_MAX; ++j) {
+    int off = 0;
+    FOR_LIST(c, LS_SEL)
+      const bool in = b >= 0 && c.ms[b].k > j;
+      const int pos = blk_append(in, s_w, off);
+      if (in) c.ids(LS_POLY0 + j)[pos] = b;
+    }
+    if (threadIdx.x == 0) c.cnt[LS_POLY0 + j] = off;
+  }
+}
+
+// dst = sum_t c_t P_t + c0 I over the matrices of list `lst`, row `j` of side (0 lhs, 1 rhs)
+// of each matrix's own scheme (numpy _combine rounding: separate multiply and add)
+__global__ void poly_combine_kernel(Slots S, DList L, const CallDesc* d, const MDev* ms, int j, int side, int dk) {
+  const int n = S.n;
+  const LgmParams& P = d->P;
+  LIST_LOOP(L, (size_t)n * n)
+    const int k = ms[b].k;
+    const double* row = side ? lgm_rhs(P, k, j) : lgm_lhs(P, k, j);
+    const int i = idx / n, jj = idx - (size_t)i * n;
+    double v = 0.0;
+    for (int t = 2; t <= j + 2; ++t)
+      if (row[t - 1] != 0.0) v = __dadd_rn(v, __dmul_rn(row[t - 1], S.buf(b, c_node_slot[t])[idx]));
+    if (i == jj && row[0] != 0.0) v = __dadd_rn(v, row[0]);
+    S.buf(b, dk)[idx] = v;
+  }
+}
+
+// L = -2^s z (scale_i / scale_j) with z = out row of scheme k_b over P1..P_{k+2}
+__global__ void poly_final_kernel(Slots S, DList L, const CallDesc* d, const MDev* ms, const double* scale, int* nonfinite,
+                                  int unit_mult) {
+  const int n = S.n;
+  const LgmParams& P = d->P;
+  double* Lout = d->L;
+  const long long ld = d->ld;
+  LIST_LOOP(L, (size_t)n * n)
+    const int k = ms[b].k;
+    const double* row = lgm_out(P, k);
+    const int i = idx / n, j = idx - (size_t)i * n;
+    double v = 0.0;
+    for (int t = 2; t <= k + 2; ++t)
+      if (row[t - 1] != 0.0) v = __dadd_rn(v, __dmul_rn(row[t - 1], S.buf(b, c_node_slot[t])[idx]));
+    if (i == j && row[0] != 0.0) v = __dadd_rn(v, row[0]);
+    if (!unit_mult) {
+      v = -ldexp(1.0, ms[b].s) * v;
+      if (P.balance) v = v * (scale[(size_t)b * n + i] / scale[(size_t)b * n + j]);
+    }
+    Lout[(size_t)b * n * ld + (size_t)i * ld + j] = v;
+    if (nonfinite && !isfinite(v)) nonfinite[b] = 1;
+  }
+}
+
+// products of the polynomial, non-finite results (estimator overflow upstream), failures
+__global__ void __launch_bounds__(CT) decide_final_kernel(Ctl c) {
+  __shared__ int s_w[33];
   {
-    std::vector<int> failed;
-    for (int b = 0; b < batch; ++b)
-      if (ms[b].status && !ms[b].post_fail) failed.push_back(b);
-    if (!failed.empty()) {
-      if (G.upload_ids(failed)) return LGM_ERR_CUDA;
-      lgm_count_launch(), nan_fill_kernel<<<G.ew_grid((int)failed.size()), 256, 0, st>>>(G.d_ids, n, L, ld);
-      CK(cudaGetLastError());
+    FOR_LIST(c, LS_SEL)
+      if (b >= 0) {
+        MDev& M = c.ms[b];
+        M.products += M.k - 1;
+        if (c.flag[b]) { M.status = LGM_NONFINITE; M.post_fail = 1; }
+      }
     }
   }
-  // reports
-  std::vector<lgm_report> R(batch);
-  for (int b = 0; b < batch; ++b) {
-    MState& M = ms[b];
-    lgm_report& r = R[b];
-    std::memset(&r, 0, sizeof(r));
+  __syncthreads();
+  {
+    int off = 0;
+    FOR_LIST(c, LS_ALL)
+      const bool f = b >= 0 && c.ms[b].status && !c.ms[b].post_fail;
+      const int pos = blk_append(f, s_w, off);
+      if (f) c.ids(LS_FAILED)[pos] = b;
+    }
+    if (threadIdx.x == 0) c.cnt[LS_FAILED] = off;
+  }
+}
+
+// L of a failed matrix: all NaN (a caller ignoring the status never reads stale data)
+__global__ void nan_fill_kernel(Slots S, DList L, const CallDesc* d) {
+  const int n = S.n;
+  double* out = d->L;
+  const long long ld = d->ld;
+  LIST_LOOP(L, (size_t)n * n)
+    const int i = idx / n, j = idx - (size_t)i * n;
+    out[(size_t)b * n * ld + (size_t)i * ld + j] = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+__global__ void report_kernel(Ctl c, int nodes) {
+  const CallDesc& D = *c.desc;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c.batch; b += gridDim.x * blockDim.x) {
+    const MDev& M = c.ms[b];
+    lgm_report r;
+    memset(&r, 0, sizeof(r));
+    const bool keep = !M.status || M.post_fail;
     r.status = M.status;
     r.s = M.s;
-    const bool keep = !M.status || M.post_fail;
     r.k = keep ? M.k : 0;
     r.db_iters = M.db_iters;
     r.products = keep ? M.products : 0;
     r.divisions = 2 * M.db_iters;
     r.estimation_passes = M.passes;
     r.norm_estimations = M.nest;
-    r.balanced = P.balance;
+    r.balanced = D.P.balance;
     r.balance_sweeps = M.sweeps;
     r.db_plateau = M.plateau;
     r.alpha_used = keep ? M.cert : 0.0;
     r.min_margin = M.mm;
+    D.rep[b] = r;
   }
-  CK(cudaMemcpyAsync(rep, R.data(), batch * sizeof(lgm_report), cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
-  return 0;
+  if (blockIdx.x == 0) count_nodes(nodes);
 }
 
-// ============================================================================ building blocks (n > 64)
-// These entry points take no workspace argument; for n > 64 they use stream-ordered scratch
-// (cudaMallocAsync) released before returning.
+// ------------------------------------------------------------------ building-block epilogues
+__global__ void store_kernel(Slots S, DList L, const CallDesc* d, int k) {
+  const int n = S.n;
+  double* out = d->L;
+  const long long ld = d->ld;
+  LIST_LOOP(L, (size_t)n * n)
+    const int i = idx / n, j = idx - (size_t)i * n;
+    out[(size_t)b * n * ld + (size_t)i * ld + j] = S.buf(b, k)[idx];
+  }
+}
 
-namespace {
-struct Scratch {
-  void* p = nullptr;
-  cudaStream_t st;
-  explicit Scratch(cudaStream_t s) : st(s) {}
-  ~Scratch() { if (p) cudaFreeAsync(p, st); }
-};
+__global__ void block_out_kernel(Ctl c, int kind, int nodes) {
+  const CallDesc& D = *c.desc;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c.batch; b += gridDim.x * blockDim.x) {
+    const MDev& M = c.ms[b];
+    if (kind == 0) {         // sqrt_db: iterations, status
+      D.iout[b] = M.status ? 0 : M.dbit;
+      D.iout2[b] = M.status ? M.status : M.dbst;
+    } else if (kind == 1) {  // estimate: value, passes (one job per matrix, table order = b)
+      D.dout[b] = c.est[b].est;
+      D.iout[b] = c.est[b].passes;
+    } else if (kind == 2) {  // balance: sweeps, scales
+      D.iout[b] = c.sweeps[b];
+      for (int i = 0; i < c.n; ++i) D.dout[(size_t)b * c.n + i] = c.scale[(size_t)b * c.n + i];
+    } else {                 // degopt: products
+      D.iout[b] = M.products;
+    }
+  }
+  if (blockIdx.x == 0) count_nodes(nodes);
+}
+
+// est building block: one job per matrix, M1 in G_B, M2 (optional) in G_AM
+__global__ void __launch_bounds__(CT) est_block_jobs_kernel(Ctl c, int has_m2) {
+  const CallDesc& D = *c.desc;
+  for (int b = threadIdx.x; b < c.batch; b += CT)
+    est_slot(c, b, b, c.S.buf(b, G_B), D.p1, has_m2 ? c.S.buf(b, G_AM) : nullptr, D.zero_shortcut, 0);
+}
+
+// degopt building block: every matrix uses scheme kblk; first_product given or one product
+__global__ void __launch_bounds__(CT) degopt_block_init_kernel(Ctl c, int have_fp) {
+  const int k = c.desc->kblk;
+  for (int b = threadIdx.x; b < c.batch; b += CT) {
+    MDev& M = c.ms[b];
+    M.k = k;
+    M.s = 0;
+    M.products = have_fp ? 0 : 1;
+    c.ids(LS_SEL)[b] = b;
+  }
+  if (threadIdx.x == 0) c.cnt[LS_SEL] = c.batch;
+}
+
 }  // namespace
 
-int lgm_grid_sqrt_db(const double* A, double* X, int64_t n64, int64_t batch64, int64_t ld, double tol, int maxiter,
-                     int* iters, int* status, cudaStream_t st) {
-  const int n = (int)n64, batch = (int)batch64;
-  Scratch sc(st);
-  CK(cudaMallocAsync(&sc.p, Grid::bytes(n, batch), st));
-  Grid G;
-  G.st = st;
-  G.carve(sc.p, n, batch);
-  std::vector<int> all(batch);
-  for (int b = 0; b < batch; ++b) all[b] = b;
-  CK(cudaMemsetAsync(G.d_iflag, 0, batch * 4, st));
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
-  std::vector<int> bad(batch);
-  CK(cudaMemcpyAsync(bad.data(), G.d_iflag, batch * 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  std::vector<int> live, dst(batch, 0), dit(batch, 0), plat(batch, 0);
-  std::vector<double> mm(batch, INFINITY);
-  for (int b = 0; b < batch; ++b) {
-    if (bad[b]) dst[b] = LGM_NONFINITE;
-    else live.push_back(b);
+// ==========================================================================================
+// Graph construction (stream capture) and the per-workspace graph cache
+#include <mutex>
+
+namespace {
+
+thread_local int t_cap_nodes = 0;  // kernel launches recorded by the current capture
+// LGM_GRAPH_DEBUG=1: trace the capture steps on stderr (diagnostics only)
+bool graph_debug() {
+  static const bool on = std::getenv("LGM_GRAPH_DEBUG") != nullptr;
+  return on;
+}
+#define GDBG(...) do { if (graph_debug()) { std::fprintf(stderr, "[lgm graph] " __VA_ARGS__); std::fputc('\n', stderr); std::fflush(stderr); } } while (0)
+inline int cap_launch() { ++t_cap_nodes; return 0; }
+#define GL cap_launch(),
+
+double host_pairwise_abs_ramp(int n) {
+  // numpy pairwise sum of |(-1)^i (1 + i/max(1, n-1))| (matcore.py:270-271)
+  auto get = [n](int i) { return std::fabs(((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))); };
+  return lgm_pairwise_sum(get, n);
+}
+
+struct Cap {
+  Ctl c;
+  int n, batch;
+  cudaStream_t s[4];  // capture streams by nesting depth (s[0] top level)
+  cudaStream_t sB[4]; // G2 look-ahead stream of each capture sequence (a side stream joins one
+                      // sequence until it ends, so every sequence forks its own)
+  cudaStream_t side(cudaStream_t st) const {
+    for (int i = 0; i < 4; ++i)
+      if (s[i] == st) return sB[i];
+    return sB[0];
   }
-  if (G.sqrt_db(live, tol, maxiter, dst, dit, mm, plat)) return LGM_ERR_CUDA;
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, X, ld);
-  CK(cudaMemcpyAsync(iters, dit.data(), batch * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(status, dst.data(), batch * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
+  cudaEvent_t evN, evP;
+  int itmax;
+};
+
+dim3 ew_blocks() { return dim3(EW_BLOCKS); }
+
+// WHILE node whose handle is set by a kernel upstream of it (captured before this call)
+int cap_while_after(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaGraph_t g;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  *body = p.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
   return 0;
 }
 
-int lgm_grid_est(const double* M1, int p1, const double* M2, int64_t n64, int64_t batch64, int64_t ld, int itmax,
-                 int zero_shortcut, double* est, int* passes, cudaStream_t st) {
-  const int n = (int)n64, batch = (int)batch64;
-  Scratch sc(st);
-  CK(cudaMallocAsync(&sc.p, Grid::bytes(n, batch), st));
-  Grid G;
-  G.st = st;
-  G.carve(sc.p, n, batch);
-  std::vector<int> all(batch);
-  for (int b = 0; b < batch; ++b) all[b] = b;
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M1, ld, G.S, G.d_ids, G.d_iflag);
-  if (M2) {  // second operand into slot G_AM via the B slot
-    G.ew(all, 1, G_AP, G_B, G_B);
-    lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(M2, ld, G.S, G.d_ids, G.d_iflag);
-    G.ew(all, 1, G_AM, G_B, G_B);
-    G.ew(all, 1, G_B, G_AP, G_AP);
+
+
+int new_handle(cudaStream_t st, cudaGraphConditionalHandle* h) {
+  cudaStreamCaptureStatus cs;
+  unsigned long long id = 0;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamGetCaptureInfo(st, &cs, &id, &g, &deps, &nd));
+  if (cs != cudaStreamCaptureStatusActive || !g) {
+    std::fprintf(stderr, "logmpoly_b200 grid: stream not capturing (%d)\n", (int)cs);
+    return LGM_ERR_CUDA;
   }
-  std::vector<int> nz;
-  if (zero_shortcut) {
-    if (G.any_nonzero(all, G_B, nz)) return LGM_ERR_CUDA;
-  } else {
-    nz.assign(batch, 1);
-  }
-  std::vector<const double*> m1, m2;
-  std::vector<int> pp, zero;
-  for (int b = 0; b < batch; ++b) {
-    m1.push_back(G.S.buf(b, G_B));
-    m2.push_back(M2 ? G.S.buf(b, G_AM) : nullptr);
-    pp.push_back(p1);
-    zero.push_back(nz[b] ? 0 : 1);
-  }
-  std::vector<double> e, mm;
-  std::vector<int> ps;
-  if (G.estimate(m1, pp, m2, zero, itmax, e, ps, mm)) return LGM_ERR_CUDA;
-  CK(cudaMemcpyAsync(est, e.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(passes, ps.data(), batch * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
+  CK(cudaGraphConditionalHandleCreate(h, g, 0, 0));
   return 0;
 }
 
-int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n64, int64_t batch64, int64_t ld,
-                     int max_sweeps, int* sweeps, cudaStream_t st) {
-  const int n = (int)n64, batch = (int)batch64;
-  Scratch sc(st);
-  CK(cudaMallocAsync(&sc.p, Grid::bytes(n, batch), st));
-  Grid G;
-  G.st = st;
-  G.carve(sc.p, n, batch);
-  std::vector<int> all(batch);
-  for (int b = 0; b < batch; ++b) all[b] = b;
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(A, ld, G.S, G.d_ids, G.d_iflag);
-  std::vector<double> mm0(batch, INFINITY);
-  CK(cudaMemcpyAsync(G.d_margin, mm0.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  lgm_count_launch(), balance_kernel_g<<<batch, bal_threads(n), bal_smem(n), st>>>(G.S, G.d_ids, scale, sweeps, max_sweeps, G.d_margin);
-  lgm_count_launch(), store_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, G_B, B, ld);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(st));
+int cap_ew(Cap& C, cudaStream_t st, int lst, int op, int dk, int sk, int s2k) {
+  GL ew_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(lst), op, dk, sk, s2k);
   return 0;
 }
 
-int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n64, int64_t batch64, int64_t ld, int k,
-                    int* products, const LgmParams& P, cudaStream_t st) {
-  const int n = (int)n64, batch = (int)batch64;
-  Scratch sc(st);
-  CK(cudaMallocAsync(&sc.p, Grid::bytes(n, batch), st));
-  Grid G;
-  G.st = st;
-  G.carve(sc.p, n, batch);
-  std::vector<int> all(batch);
-  for (int b = 0; b < batch; ++b) all[b] = b;
-  if (G.upload_ids(all)) return LGM_ERR_CUDA;
-  lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(X, ld, G.S, G.d_ids, G.d_iflag);
-  int prods = 0;
+int cap_norm(Cap& C, cudaStream_t st, int lst, int slot, double* out) {
+  CK(cudaMemsetAsync(out, 0, C.batch * 8, st));
+  GL onenorm_kernel<<<ew_blocks(), 128, 0, st>>>(C.c.S, C.c.list(lst), slot, out);
+  return 0;
+}
+
+// one estimate per live entry of the EstJob table (batched; maxq >= every job's p1 + [M2])
+int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
+  const int n = C.n, nj = C.batch;
+  const double rsum = host_pairwise_abs_ramp(n);
+  GL est_nz_kernel<<<dim3(std::max(1, std::min(32, n * n / 4096)), nj), 256, 0, st>>>(C.c.est, n);
+  if (n <= EST_FUSED_MAXN && est_fused_on()) {
+    const int sm = n * n * 8;
+    GL est_fused_kernel<<<nj, 256, sm, st>>>(C.c.est, n, rsum, C.itmax);
+    return 0;
+  }
+  GL est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, rsum);
+  for (int sweep = 0; sweep < C.itmax; ++sweep) {
+    for (int q = 0; q < maxq; ++q)
+      GL est_fwd_kernel<<<dim3((n + 8 * EST_FWD_R - 1) / (8 * EST_FWD_R), nj), 256, 0, st>>>(C.c.est, n, q);
+    GL est_after_fwd_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+    for (int q = 0; q < maxq; ++q) {
+      if ((n & 1) == 0) GL est_adj2_kernel<<<dim3((n + 255) / 256, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q);
+      else GL est_adj_kernel<<<dim3((n + 127) / 128, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q);
+      GL est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, q, C.c.splits);
+    }
+    GL est_after_adj_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+  }
+  return 0;
+}
+
+// alpha (A.2) for the matrices of list `lst` (request m / th already in the state)
+int cap_alpha(Cap& C, cudaStream_t st, int lst, int maxq) {
+  GL alpha_a_kernel<<<1, CT, 0, st>>>(C.c, lst);
+  if (cap_estimate(C, st, maxq)) return LGM_ERR_CUDA;
+  GL alpha_b_kernel<<<1, CT, 0, st>>>(C.c, lst);
+  if (cap_estimate(C, st, maxq)) return LGM_ERR_CUDA;
+  GL alpha_c_kernel<<<1, CT, 0, st>>>(C.c, lst);
+  return 0;
+}
+
+// ---- batched Gauss-Jordan inversion of the job table (capacity nj jobs)
+template <int NT>
+int launch_g1(Cap& C, cudaStream_t st, int nj) {
+  const size_t sm = G1Smem<NT>::bytes;
+  GL gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(C.c.jobs, C.n);
+  return 0;
+}
+
+int cap_invert(Cap& C, cudaStream_t st, int nj) {
+  const int n = C.n;
+  const InvJob* d_jobs = C.c.jobs;
+  if (use_g1(n)) {  // G1: one CTA per inversion, no per-panel launches
+    if (n <= 128) return launch_g1<128>(C, st, nj);
+    if (n <= 256) return launch_g1<256>(C, st, nj);
+    return launch_g1<512>(C, st, nj);
+  }
+  cudaStream_t sB = C.side(st);
+  cudaEvent_t evN = C.evN, evP = C.evP;
+  GL gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
   const int tiles = (n + TM - 1) / TM;
-  if (FP) {
-    G.ew(all, 1, G_Y, G_B, G_B);
-    lgm_count_launch(), load_kernel<<<G.ew_grid(batch), 256, 0, st>>>(FP, ld, G.S, G.d_ids, G.d_iflag);
-    G.ew(all, 1, G_AP, G_B, G_B);
-    G.ew(all, 1, G_B, G_Y, G_Y);
-  } else {
-    CombSpec cs{};
-    cs.nterm = 1;
-    cs.node[0] = G_B;
-    cs.coef[0] = 1.0;
-    lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, cs, G_B, G_AP);
-    prods++;
-  }
-  const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
-  const double* base = P.coef + P.coef_off[k - 1];
-  auto spec = [&](const double* row, int nn) {
-    CombSpec cs{};
-    cs.c0 = row[0];
-    for (int t = 2; t <= nn; ++t)
-      if (row[t - 1] != 0.0) { cs.node[cs.nterm] = node_slot[t]; cs.coef[cs.nterm] = row[t - 1]; cs.nterm++; }
-    return cs;
+  const bool cta_panel = n <= 512;  // one CTA per panel (writes A1 itself: no gj_copy_a1_kernel)
+  auto panel = [&](int k0, cudaStream_t s, int a1_kind = -1, int s1_a1kind = -1) {
+    const int nb = std::min(NB, n - k0);
+    if (n <= 128) {
+      GL gj_panel_cta_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+    } else if (n <= 256) {
+      GL gj_panel_cta_kernel<256><<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+    } else if (n <= 512) {
+      GL gj_panel_cta_kernel<512><<<nj, 512, 16 * 32 * 33 * 8, s>>>(d_jobs, n, k0, nb, a1_kind, s1_a1kind);
+    } else if (n <= CL * 512) {  // G2 panel: one 8-CTA cluster per inversion
+      GL gj_panel_cluster_kernel<<<nj * CL, 512, 0, s>>>(d_jobs, n, k0, nb);
+    } else {
+      GL gj_panel_kernel<<<nj, 512, 0, s>>>(d_jobs, n, k0, nb, 0);
+    }
   };
-  int nn = 3;
-  for (int j = 1; j < k; ++j) {
-    const double* lrow = base + j * (j + 3) / 2;
-    const double* rrow = base + k * (k + 3) / 2 + j * (j + 3) / 2;
-    CombSpec rs = spec(rrow, nn);
-    lgm_count_launch(), combine_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, rs, G_Y);
-    CombSpec ls = spec(lrow, nn);
-    lgm_count_launch(), gemm_comb_kernel<<<dim3(tiles, tiles, batch), 128, 0, st>>>(G.S, G.d_ids, ls, G_Y, node_slot[nn + 1]);
-    nn++;
-    prods++;
+  auto snapshot = [&](int k0, int kind, int jlo = 0, int jhi = -1, cudaStream_t s = nullptr) {
+    const int nb = std::min(NB, n - k0);
+    if (jhi < 0) jhi = n;
+    GL gj_snapshot_kernel<<<dim3((nb * (jhi - jlo) + 255) / 256, nj), 256, 0, s ? s : st>>>(d_jobs, n, k0, nb, kind, jlo,
+                                                                                            jhi);
+  };
+  static const bool rank64 = [] {  // LGM_G2_RANK64=0 falls back to rank-32 passes (A/B switch)
+    const char* e = std::getenv("LGM_G2_RANK64");
+    return !(e && e[0] == '0');
+  }();
+  // rank-64 vs rank-32 passes round differently: the choice depends on n only, so a
+  // matrix's arithmetic never depends on its batch-mates or on how many have converged
+  const bool use64 = rank64 && n % (2 * NB) == 0;
+  panel(0, st, use64 && cta_panel ? 2 : -1);
+  if (use64) {
+    // rank-64 delayed update with both panels of the next pair factored on sB during the
+    // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
+    // rows), A1 (copy of P1's multipliers), stage-1 update of P2's columns, factor P2, W2.
+    auto prepare_pair = [&](int k0, int q, cudaStream_t s, bool full_snapshot) {
+      // P1 = [k0, k0+NB) already factored; everything except the full-width W1 / W2
+      if (cta_panel) {  // stage-1 update fused into P2's panel kernel
+        panel(k0 + NB, s, -1, 3 * q + 2);
+        return;
+      }
+      if (full_snapshot) snapshot(k0, 3 * q, 0, n, s);
+      else snapshot(k0, 3 * q, k0 + NB, k0 + 2 * NB, s);  // P2's columns only (for stage 1)
+      GL gj_copy_a1_kernel<<<dim3((n * NB + 255) / 256, nj), 256, 0, s>>>(d_jobs, n, k0, 3 * q + 2);
+      GL gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, s>>>(d_jobs, n, k0, NB, k0 + NB, k0 + NB, k0 + 2 * NB, 0, 0,
+                                                             3 * q);
+      panel(k0 + NB, s);
+    };
+    prepare_pair(0, 0, st, !cta_panel);
+    if (cta_panel) GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
+    else GL gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, 0);
+    for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
+      const int kn = k0 + 2 * NB;
+      const bool next = kn < n;
+      if (next) {  // finish the next pair's columns, then factor both of its panels on sB
+        GL gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0, kn, kn, kn + 2 * NB,
+                                                                                 0, 0, q);
+        CK(cudaEventRecord(evN, st));
+        CK(cudaStreamWaitEvent(sB, evN, 0));
+        panel(kn, sB, cta_panel ? 3 * (q ^ 1) + 2 : -1);
+        prepare_pair(kn, q ^ 1, sB, false);
+        CK(cudaEventRecord(evP, sB));
+      }
+      GL gj_update2_kernel<G2_RT><<<dim3(tiles, n / G2_RT, nj), 2 * G2_RT, up2_smem<G2_RT>(), st>>>(
+          d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
+      if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
+        CK(cudaStreamWaitEvent(st, evP, 0));
+        if (cta_panel) {
+          GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
+        } else {
+          snapshot(kn, 3 * (q ^ 1));
+          GL gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, 0);
+        }
+      }
+    }
+    return 0;
   }
-  CombSpec os = spec(base + k * (k + 3), nn);
-  std::vector<double> mult(batch, 1.0);
-  CK(cudaMemcpyAsync(G.d_scal, mult.data(), batch * 8, cudaMemcpyHostToDevice, st));
-  lgm_count_launch(), final_kernel<<<G.ew_grid(batch), 256, 0, st>>>(G.S, G.d_ids, os, G.d_scal, G.d_scale, 0, Z, ld,
-                                                                      nullptr);
-  CK(cudaGetLastError());
-  std::vector<int> pr(batch, prods);
-  CK(cudaMemcpyAsync(products, pr.data(), batch * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));
+  snapshot(0, 0);
+  for (int k0 = 0, par = 0; k0 < n; k0 += NB, par ^= 1) {
+    const int nb = std::min(NB, n - k0);
+    const int kn = k0 + NB, nbn = kn < n ? std::min(NB, n - kn) : 0;
+    if (kn < n) {
+      GL gj_update_kernel<<<dim3(1, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, kn, kn, kn + nbn, 0, 0, par);
+      CK(cudaEventRecord(evN, st));
+      CK(cudaStreamWaitEvent(sB, evN, 0));
+      panel(kn, sB);
+      CK(cudaEventRecord(evP, sB));
+    }
+    GL gj_update_kernel<<<dim3(tiles, tiles, nj), 128, 0, st>>>(d_jobs, n, k0, nb, 0, 0, n, kn, kn + nbn, par);
+    if (kn < n) {
+      CK(cudaStreamWaitEvent(st, evP, 0));
+      snapshot(kn, par ^ 1);
+    }
+  }
   return 0;
+}
+
+// one DB iteration over LS_DB (first: X only, Y = I), ending in decide_db_kernel(h)
+int cap_db_iter(Cap& C, cudaStream_t st, bool first, cudaGraphConditionalHandle h, int block_mode) {
+  const int n = C.n;
+  const int n0 = t_cap_nodes;
+  const bool oop = use_g1(n);
+  GL build_jobs_kernel<<<1, CT, 0, st>>>(C.c, first ? 1 : 0, oop ? 1 : 0);
+  if (!oop) {  // G2 inverts in place: copies first
+    if (cap_ew(C, st, LS_DB, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
+    if (!first && cap_ew(C, st, LS_DB, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
+  }
+  if (cap_invert(C, st, first ? C.batch : 2 * C.batch)) return LGM_ERR_CUDA;
+  DbArgs a;
+  a.S = C.c.S;
+  a.L = C.c.list(LS_DB);
+  a.xpiv = C.c.piv;
+  a.xstep = C.c.step;
+  a.ypiv = C.c.piv + (size_t)C.batch * n;
+  a.ystep = C.c.step + (size_t)C.batch * n;
+  a.xlog = C.c.logdet;
+  a.ylog = C.c.logdet + C.batch;
+  a.scaling = C.c.scaling;
+  a.first = first ? 1 : 0;
+  a.change = C.c.change;
+  a.size = C.c.size;
+  a.istat = C.c.istat;
+  a.batch = C.batch;
+  GL db_update_kernel<<<dim3((n + 127) / 128, C.batch), 128, 0, st>>>(a);
+  const int nodes = t_cap_nodes - n0 + 1;
+  GL decide_db_kernel<<<1, CT, 0, st>>>(C.c, h, first ? 0 : nodes, first ? 1 : 0, block_mode);
+  return 0;
+}
+
+// the square roots of LS_DB (already = roots): Y = I, iteration 1, WHILE(more iterations)
+int cap_sqrt_db(Cap& C, int depth, int block_mode) {
+  cudaStream_t st = C.s[depth];
+  if (cap_ew(C, st, LS_DB, 2, G_Y, G_Y, G_Y)) return LGM_ERR_CUDA;  // Y = I
+  cudaGraphConditionalHandle h;
+  cudaGraph_t body;
+  // handle created first so that iteration 1's decide kernel can set it
+  if (new_handle(st, &h)) return LGM_ERR_CUDA;
+  GDBG("sqrt_db: handle created (depth %d)", depth);
+  if (cap_db_iter(C, st, true, h, block_mode)) return LGM_ERR_CUDA;
+  GDBG("sqrt_db: first iteration captured");
+  if (cap_while_after(st, h, &body)) return LGM_ERR_CUDA;
+  GDBG("sqrt_db: while node added");
+  cudaStream_t sb = C.s[depth + 1];
+  const int saved = t_cap_nodes;  // the body's kernels are counted by its decide kernel
+  CK(cudaStreamBeginCaptureToGraph(sb, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  if (cap_db_iter(C, sb, false, h, block_mode)) return LGM_ERR_CUDA;
+  cudaGraph_t tmp;
+  CK(cudaStreamEndCapture(sb, &tmp));
+  t_cap_nodes = saved;
+  GDBG("sqrt_db: body captured");
+  return 0;
+}
+
+// one scaling-loop iteration (A.1 step 5) at depth d, ending in decide_post_kernel(h)
+int cap_scal_iter(Cap& C, int depth, int maxq, cudaGraphConditionalHandle h, bool in_loop) {
+  cudaStream_t st = C.s[depth];
+  const int n0 = t_cap_nodes;
+  GL decide_act_kernel<<<1, CT, 0, st>>>(C.c);
+  if (cap_ew(C, st, LS_ACT, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;  // A - I
+  if (cap_norm(C, st, LS_ACT, G_AM, C.c.nrm)) return LGM_ERR_CUDA;
+  if (cap_norm(C, st, LS_ACTAI2, G_AP, C.c.nrm2)) return LGM_ERR_CUDA;
+  GL scal_req_kernel<<<1, CT, 0, st>>>(C.c);
+  if (cap_alpha(C, st, LS_ACT, maxq)) return LGM_ERR_CUDA;
+  GL decide_roots_kernel<<<1, CT, 0, st>>>(C.c);
+  if (cap_ew(C, st, LS_ROOTS, 1, G_AP, G_B, G_B)) return LGM_ERR_CUDA;  // A_prev = B
+  if (cap_sqrt_db(C, depth, 0)) return LGM_ERR_CUDA;
+  const int nodes = t_cap_nodes - n0 + 2;
+  GL decide_post_kernel<<<1, CT, 0, st>>>(C.c, h, in_loop ? nodes : 0);
+  if (cap_ew(C, st, LS_OK, 3, G_AP, G_AP, G_B)) return LGM_ERR_CUDA;  // A_I2 = A_prev - 2B + I
+  return 0;
+}
+
+// ------------------------------------------------------------------ whole programs
+enum { PROG_LOGM = 0, PROG_SQRTDB, PROG_EST, PROG_BALANCE, PROG_DEGOPT };
+
+int cap_load(Cap& C, cudaStream_t st, const double* const* src, int slot) {
+  // load_kernel writes slot G_B; other slots by a copy
+  GL load_kernel<<<ew_blocks(), 256, 0, st>>>(src, &C.c.desc->ld, C.c.S, C.c.list(LS_ALL), C.c.flag);
+  if (slot != G_B && cap_ew(C, st, LS_ALL, 1, slot, G_B, G_B)) return LGM_ERR_CUDA;
+  return 0;
+}
+
+int cap_logm(Cap& C) {
+  cudaStream_t st = C.s[0];
+  const int n = C.n;
+  GL ctl_init_kernel<<<1, CT, 0, st>>>(C.c);
+  GL fill_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.scale, (size_t)C.batch * n, 1.0);
+  if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+  GL decide_live_kernel<<<1, CT, 0, st>>>(C.c);
+  // balance (matcore.py:180-215); the kernel returns at once when the call disables it
+  GL balance_kernel_g<<<C.batch, bal_threads(n), bal_smem(n), st>>>(C.c.S, C.c.list(LS_LIVE), C.c.scale, C.c.sweeps,
+                                                                    100, C.c.margin, &C.c.desc->P.balance, nullptr);
+  if (cap_ew(C, st, LS_LIVE, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
+  if (cap_norm(C, st, LS_LIVE, G_AM, C.c.nrm)) return LGM_ERR_CUDA;
+  GL decide_start_kernel<<<1, CT, 0, st>>>(C.c);
+  // scaling loop: iteration 1 peeled (s = 0: estimates of (A - I)^{m_K}, (A - I)^{m_K + 1}),
+  // then WHILE(some matrix still scaling) with s >= 1 (A_I2-based estimates: <= m_K/2 + 1)
+  cudaGraphConditionalHandle hs;
+  if (new_handle(st, &hs)) return LGM_ERR_CUDA;
+  const int mk = LGM_ORDER_DEFAULT[LGM_K_MAX - 1];
+  if (cap_scal_iter(C, 0, mk + 1, hs, false)) return LGM_ERR_CUDA;
+  cudaGraph_t body;
+  if (cap_while_after(st, hs, &body)) return LGM_ERR_CUDA;
+  int saved = t_cap_nodes;
+  CK(cudaStreamBeginCaptureToGraph(C.s[1], body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  if (cap_scal_iter(C, 1, mk / 2 + 1, hs, true)) return LGM_ERR_CUDA;
+  {
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(C.s[1], &tmp));
+  }
+  t_cap_nodes = saved;
+  // select_order
+  GL decide_sel_kernel<<<1, CT, 0, st>>>(C.c);
+  if (cap_ew(C, st, LS_SEL, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
+  if (cap_norm(C, st, LS_SEL, G_AM, C.c.nrm)) return LGM_ERR_CUDA;
+  {  // s = 0: A_I2 = (B - I)(B - I), one product
+    const int tiles = (n + TM - 1) / TM;
+    if ((n & 1) == 0) {
+      const size_t sm = 2 * (size_t)(GP_A + GP_B) * 8;
+      GL gemm_plain_kernel<<<dim3(tiles, tiles, C.batch), 128, sm, st>>>(C.c.S, C.c.list(LS_NEEDAI2), G_AM, G_AM, G_AP);
+    } else {
+      CombSpec cs{};
+      cs.nterm = 1;
+      cs.node[0] = G_AM;
+      cs.coef[0] = 1.0;
+      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, C.c.list(LS_NEEDAI2), cs, G_AM, G_AP);
+    }
+  }
+  if (cap_norm(C, st, LS_SEL, G_AP, C.c.nrm2)) return LGM_ERR_CUDA;
+  cudaGraphConditionalHandle hsel;
+  if (new_handle(st, &hsel)) return LGM_ERR_CUDA;
+  GL select_init_kernel<<<1, CT, 0, st>>>(C.c, hsel);
+  if (cap_while_after(st, hsel, &body)) return LGM_ERR_CUDA;
+  saved = t_cap_nodes;
+  CK(cudaStreamBeginCaptureToGraph(C.s[1], body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  {
+    const int n0 = t_cap_nodes;
+    if (cap_alpha(C, C.s[1], LS_CUR, mk / 2 + 1)) return LGM_ERR_CUDA;
+    GL select_step_kernel<<<1, CT, 0, C.s[1]>>>(C.c, hsel, t_cap_nodes - n0 + 1);
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(C.s[1], &tmp));
+  }
+  t_cap_nodes = saved;
+  // polynomial
+  GL decide_poly_kernel<<<1, CT, 0, st>>>(C.c);
+  if (cap_ew(C, st, LS_SEL, 4, G_B, G_B, G_B)) return LGM_ERR_CUDA;  // P2 = I - B
+  CK(cudaMemsetAsync(C.c.flag, 0, C.batch * 4, st));
+  const int tiles = (n + TM - 1) / TM;
+  const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+  const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
+  for (int j = 1; j < LGM_K_MAX; ++j) {
+    const DList Lj = C.c.list(LS_POLY0 + j);
+    GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 1, G_Y);
+    GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 0, G_AM);
+    if ((n & 1) == 0) {
+      GL gemm_plain_kernel<<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(C.c.S, Lj, G_AM, G_Y, node_slot[j + 3]);
+    } else {
+      CombSpec cs{};
+      cs.nterm = 1;
+      cs.node[0] = G_AM;
+      cs.coef[0] = 1.0;
+      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, Lj, cs, G_Y, node_slot[j + 3]);
+    }
+  }
+  GL poly_final_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_SEL), C.c.desc, C.c.ms, C.c.scale, C.c.flag, 0);
+  GL decide_final_kernel<<<1, CT, 0, st>>>(C.c);
+  GL nan_fill_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_FAILED), C.c.desc);
+  GL report_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, t_cap_nodes + 1);
+  return 0;
+}
+
+int cap_block(Cap& C, int prog, int has2, int p1) {
+  cudaStream_t st = C.s[0];
+  const int n = C.n;
+  GL ctl_init_kernel<<<1, CT, 0, st>>>(C.c);
+  GL fill_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.scale, (size_t)C.batch * n, 1.0);
+  if (prog == PROG_SQRTDB) {
+    if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+    GL decide_live_kernel<<<1, CT, 0, st>>>(C.c);
+    GL decide_db_start_kernel<<<1, CT, 0, st>>>(C.c);
+    if (cap_sqrt_db(C, 0, 1)) return LGM_ERR_CUDA;
+    GL store_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.desc, G_B);
+    GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 0, t_cap_nodes + 1);
+  } else if (prog == PROG_EST) {
+    if (has2) {  // M2 -> G_AM (via G_B), then M1 -> G_B
+      if (cap_load(C, st, &C.c.desc->A2, G_AM)) return LGM_ERR_CUDA;
+    }
+    if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+    GL est_block_jobs_kernel<<<1, CT, 0, st>>>(C.c, has2);
+    if (cap_estimate(C, st, p1 + (has2 ? 1 : 0))) return LGM_ERR_CUDA;
+    GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 1, t_cap_nodes + 1);
+  } else if (prog == PROG_BALANCE) {
+    if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+    GL balance_kernel_g<<<C.batch, bal_threads(n), bal_smem(n), st>>>(C.c.S, C.c.list(LS_ALL), C.c.scale, C.c.sweeps,
+                                                                      0, C.c.margin, nullptr, &C.c.desc->max_sweeps);
+    GL store_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.desc, G_B);
+    GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 2, t_cap_nodes + 1);
+  } else {  // PROG_DEGOPT: X -> P2 slot G_B, first product -> G_AP (given, or one GEMM)
+    if (has2 && cap_load(C, st, &C.c.desc->A2, G_AP)) return LGM_ERR_CUDA;
+    if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+    GL degopt_block_init_kernel<<<1, CT, 0, st>>>(C.c, has2);
+    const int tiles = (n + TM - 1) / TM;
+    if (!has2) {
+      CombSpec cs{};
+      cs.nterm = 1;
+      cs.node[0] = G_B;
+      cs.coef[0] = 1.0;
+      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, C.c.list(LS_ALL), cs, G_B, G_AP);
+    }
+    GL decide_poly_kernel<<<1, CT, 0, st>>>(C.c);
+    for (int j = 1; j < LGM_K_MAX; ++j) {
+      const DList Lj = C.c.list(LS_POLY0 + j);
+      const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+      GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 1, G_Y);
+      CombSpec ls{};
+      GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 0, G_AM);
+      ls.nterm = 1;
+      ls.node[0] = G_AM;
+      ls.coef[0] = 1.0;
+      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, Lj, ls, G_Y, node_slot[j + 3]);
+    }
+    GL poly_final_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_SEL), C.c.desc, C.c.ms, C.c.scale, nullptr, 1);
+    GL decide_final_kernel<<<1, CT, 0, st>>>(C.c);
+    GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 3, t_cap_nodes + 1);
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ cache
+struct GraphKey {
+  int dev, prog, n, batch, itmax, has2, p1;
+  const void* ws;
+  bool operator==(const GraphKey& o) const {
+    return dev == o.dev && prog == o.prog && n == o.n && batch == o.batch && itmax == o.itmax && has2 == o.has2 &&
+           p1 == o.p1 && ws == o.ws;
+  }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long used = 0;
+};
+std::mutex g_cache_mu;
+std::vector<GraphEntry> g_cache;  // small LRU of instantiated programs
+unsigned long long g_cache_tick = 0;
+constexpr size_t CACHE_MAX = 24;
+
+struct CapStreams {
+  cudaStream_t s[8] = {};
+  cudaEvent_t evN = nullptr, evP = nullptr;
+  ~CapStreams() {
+    for (auto x : s)
+      if (x) cudaStreamDestroy(x);
+    if (evN) cudaEventDestroy(evN);
+    if (evP) cudaEventDestroy(evP);
+  }
+};
+
+// dynamic shared-memory limits are per device: set before every capture (no process-wide flag)
+int set_attrs(int n) {
+  const cudaFuncAttribute mx = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  CK(cudaFuncSetAttribute(est_fused_kernel, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
+  CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128>, mx, (int)G1Smem<128>::bytes));
+  CK(cudaFuncSetAttribute(gj_inv_cta_kernel<256>, mx, (int)G1Smem<256>::bytes));
+  CK(cudaFuncSetAttribute(gj_inv_cta_kernel<512>, mx, (int)G1Smem<512>::bytes));
+  CK(cudaFuncSetAttribute(gj_panel_cta_kernel<128>, mx, 4 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_cta_kernel<256>, mx, 8 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_cta_kernel<512>, mx, 16 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
+  CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
+  CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
+  return 0;
+}
+
+int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
+  if (set_attrs(k.n)) return LGM_ERR_CUDA;
+  CapStreams cs;
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (int i = 0; i < 4; ++i) CK(cudaStreamCreateWithFlags(&cs.s[i], cudaStreamNonBlocking));
+  for (int i = 4; i < 8; ++i) CK(cudaStreamCreateWithPriority(&cs.s[i], cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&cs.evN, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&cs.evP, cudaEventDisableTiming));
+  Cap C;
+  C.n = k.n;
+  C.batch = k.batch;
+  C.c = ctl_carve(ws, k.n, k.batch);
+  for (int i = 0; i < 4; ++i) {
+    C.s[i] = cs.s[i];
+    C.sB[i] = cs.s[4 + i];
+  }
+  C.evN = cs.evN;
+  C.evP = cs.evP;
+  C.itmax = k.itmax;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  GDBG("capture prog %d n %d batch %d", k.prog, k.n, k.batch);
+  CK(cudaStreamBeginCaptureToGraph(C.s[0], g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  t_cap_nodes = 0;
+  int rc = k.prog == PROG_LOGM ? cap_logm(C) : cap_block(C, k.prog, k.has2, k.p1);
+  GDBG("capture body done rc %d nodes %d", rc, t_cap_nodes);
+  for (int i = 3; i >= 1; --i) {  // a failed capture may leave a body sequence open
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(C.s[i], &st);
+    if (st != cudaStreamCaptureStatusNone) {
+      cudaGraph_t t2 = nullptr;
+      cudaStreamEndCapture(C.s[i], &t2);
+    }
+  }
+  cudaGraph_t tmp;
+  cudaError_t e = cudaStreamEndCapture(C.s[0], &tmp);
+  GDBG("end capture: %s", cudaGetErrorString(e));
+  if (rc || e != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky capture error
+    cudaGraphDestroy(g);
+    std::fprintf(stderr, "logmpoly_b200 grid: graph capture failed (%s)\n", cudaGetErrorString(e));
+    return LGM_ERR_CUDA;
+  }
+  e = cudaGraphInstantiate(out, g, 0);
+  GDBG("instantiate: %s", cudaGetErrorString(e));
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "logmpoly_b200 grid: graph instantiate failed (%s)\n", cudaGetErrorString(e));
+    return LGM_ERR_CUDA;
+  }
+  return 0;
+}
+
+// launch the program for key k on stream st with this call's descriptor
+int run_prog(const GraphKey& k0, void* ws, const CallDesc& d, cudaStream_t st) {
+  GraphKey k = k0;
+  CK(cudaGetDevice(&k.dev));
+  k.ws = ws;
+  const Ctl c = ctl_carve(ws, k.n, k.batch);
+  lgm_count_launch(), setup_kernel<<<1, 1, 0, st>>>(c.desc, d);
+  CK(cudaGetLastError());
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  GraphEntry* ent = nullptr;
+  for (auto& e : g_cache)
+    if (e.key == k) ent = &e;
+  if (!ent) {
+    cudaGraphExec_t ex = nullptr;
+    if (build_exec(k, ws, &ex)) return LGM_ERR_CUDA;
+    if (g_cache.size() >= CACHE_MAX) {
+      auto old = std::min_element(g_cache.begin(), g_cache.end(),
+                                  [](const GraphEntry& a, const GraphEntry& b) { return a.used < b.used; });
+      cudaGraphExecDestroy(old->exec);  // freed asynchronously if still in flight
+      g_cache.erase(old);
+    }
+    g_cache.push_back(GraphEntry{k, ex, 0});
+    ent = &g_cache.back();
+  }
+  ent->used = ++g_cache_tick;
+  CK(cudaGraphLaunch(ent->exec, st));
+  return 0;
+}
+
+CallDesc desc_base(const LgmParams& P) {
+  CallDesc d;
+  std::memset(&d, 0, sizeof(d));
+  d.P = P;
+  return d;
+}
+
+}  // namespace
+
+// ============================================================================ entry points (n > 64)
+
+size_t lgm_grid_workspace_bytes(int64_t n, int64_t batch) { return ctl_bytes(n, batch); }
+
+int lgm_grid_logm(const double* A, double* L, int64_t n, int64_t batch, int64_t ld, const LgmParams& P,
+                  lgm_report* rep, void* ws, cudaStream_t st) {
+  CallDesc d = desc_base(P);
+  d.A = A;
+  d.L = L;
+  d.ld = ld;
+  d.rep = rep;
+  GraphKey k{0, PROG_LOGM, (int)n, (int)batch, P.est_itmax, 0, 0, nullptr};
+  return run_prog(k, ws, d, st);
+}
+
+int lgm_grid_sqrt_db(const double* A, double* X, int64_t n, int64_t batch, int64_t ld, double tol, int maxiter,
+                     int* iters, int* status, void* ws, cudaStream_t st) {
+  LgmParams P{};
+  CallDesc d = desc_base(P);
+  d.A = A;
+  d.L = X;
+  d.ld = ld;
+  d.iout = iters;
+  d.iout2 = status;
+  d.tol = tol;
+  d.maxiter = maxiter;
+  GraphKey k{0, PROG_SQRTDB, (int)n, (int)batch, 0, 0, 0, nullptr};
+  return run_prog(k, ws, d, st);
+}
+
+int lgm_grid_est(const double* M1, int p1, const double* M2, int64_t n, int64_t batch, int64_t ld, int itmax,
+                 int zero_shortcut, double* est, int* passes, void* ws, cudaStream_t st) {
+  LgmParams P{};
+  CallDesc d = desc_base(P);
+  d.A = M1;
+  d.A2 = M2;
+  d.ld = ld;
+  d.p1 = p1;
+  d.zero_shortcut = zero_shortcut;
+  d.dout = est;
+  d.iout = passes;
+  GraphKey k{0, PROG_EST, (int)n, (int)batch, itmax, M2 ? 1 : 0, p1, nullptr};
+  return run_prog(k, ws, d, st);
+}
+
+int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n, int64_t batch, int64_t ld,
+                     int max_sweeps, int* sweeps, void* ws, cudaStream_t st) {
+  LgmParams P{};
+  CallDesc d = desc_base(P);
+  d.A = A;
+  d.L = B;
+  d.ld = ld;
+  d.dout = scale;
+  d.iout = sweeps;
+  d.max_sweeps = max_sweeps;
+  GraphKey k{0, PROG_BALANCE, (int)n, (int)batch, 0, 0, 0, nullptr};
+  return run_prog(k, ws, d, st);
+}
+
+int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int k,
+                    int* products, const LgmParams& P, void* ws, cudaStream_t st) {
+  CallDesc d = desc_base(P);
+  d.A = X;
+  d.A2 = FP;
+  d.L = Z;
+  d.ld = ld;
+  d.kblk = k;
+  d.iout = products;
+  GraphKey key{0, PROG_DEGOPT, (int)n, (int)batch, 0, FP ? 1 : 0, 0, nullptr};
+  return run_prog(key, ws, d, st);
+}
+
+// kernels executed inside graphs on the current device (read back synchronously: stats only)
+unsigned long long lgm_grid_exec_nodes() {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_exec_nodes, sizeof(v)) != cudaSuccess) return 0;
+  return v;
 }
 
 extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
@@ -3053,12 +3559,4 @@ extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
   (void)out;
   return 0;
 #endif
-}
-
-extern "C" int lgm_debug_grid_phase_ms(double* out, int reset) {
-  for (int i = 0; i < PH_N; ++i) {
-    out[i] = g_phase_ms[i];
-    if (reset) g_phase_ms[i] = 0.0;
-  }
-  return PH_N;
 }

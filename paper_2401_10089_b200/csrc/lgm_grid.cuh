@@ -1,4 +1,6 @@
-// Engine G (n > 64): host-orchestrated batched kernels.  Declarations used by lgm_api.cu.
+// Engine G (n > 64): device-driven batched kernels captured into a CUDA graph.  Declarations
+// used by lgm_api.cu.  Every entry point is stream-ordered (no host synchronisation) and uses
+// only the caller's workspace (lgm_grid_workspace_bytes).
 #pragma once
 #include "lgm_common.cuh"
 
@@ -6,10 +8,12 @@ size_t lgm_grid_workspace_bytes(int64_t n, int64_t batch);
 int lgm_grid_logm(const double* A, double* L, int64_t n, int64_t batch, int64_t ld, const LgmParams& P,
                   lgm_report* rep, void* ws, cudaStream_t s);
 int lgm_grid_sqrt_db(const double* A, double* X, int64_t n, int64_t batch, int64_t ld, double tol, int maxiter,
-                     int* iters, int* status, cudaStream_t s);
+                     int* iters, int* status, void* ws, cudaStream_t s);
 int lgm_grid_est(const double* M1, int p1, const double* M2, int64_t n, int64_t batch, int64_t ld, int itmax,
-                 int zero_shortcut, double* est, int* passes, cudaStream_t s);
+                 int zero_shortcut, double* est, int* passes, void* ws, cudaStream_t s);
 int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n, int64_t batch, int64_t ld,
-                     int max_sweeps, int* sweeps, cudaStream_t s);
+                     int max_sweeps, int* sweeps, void* ws, cudaStream_t s);
 int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int k,
-                    int* products, const LgmParams& P, cudaStream_t s);
+                    int* products, const LgmParams& P, void* ws, cudaStream_t s);
+// kernels executed inside Engine G graphs on the current device (synchronous read; stats only)
+unsigned long long lgm_grid_exec_nodes();

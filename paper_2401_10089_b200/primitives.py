@@ -57,6 +57,15 @@ def _stream(dev):
     return ctypes.c_void_p(_torch().cuda.current_stream(dev).cuda_stream)
 
 
+def _block_ws(n, B, dev):
+    """Caller-owned scratch of the building blocks (lgm_block_workspace_bytes; the library
+    allocates nothing).  Returns (tensor keeping it alive, pointer, bytes)."""
+    nb = ctypes.c_size_t(0)
+    _lib.check(_lib.load().lgm_block_workspace_bytes(n, B, ctypes.byref(nb)), "lgm_block_workspace_bytes")
+    ws = _torch().empty(max(int(nb.value), 1), dtype=_torch().uint8, device=dev)
+    return ws, ws.data_ptr(), nb.value
+
+
 def sqrt_db_batched(A, tol=None, maxiter=50):
     """Returns (X, iterations[int32], status[int32])."""
     torch = _torch()
@@ -65,8 +74,10 @@ def sqrt_db_batched(A, tol=None, maxiter=50):
     X = torch.empty_like(Ad)
     it = torch.zeros(B, dtype=torch.int32, device=Ad.device)
     st = torch.zeros(B, dtype=torch.int32, device=Ad.device)
+    ws, wp, wb = _block_ws(n, B, Ad.device)
     _lib.check(_lib.load().lgm_sqrt_db_f64(Ad.data_ptr(), X.data_ptr(), n, B, n, float(tol or 0.0), int(maxiter),
-                                           it.data_ptr(), st.data_ptr(), _stream(Ad.device)), "lgm_sqrt_db_f64")
+                                           it.data_ptr(), st.data_ptr(), wp, wb, _stream(Ad.device)),
+               "lgm_sqrt_db_f64")
     return _out(X, was_numpy, squeeze), it.cpu().numpy(), st.cpu().numpy()
 
 
@@ -92,15 +103,17 @@ def _est(M1, p1, M2, itmax, zero_shortcut):
     est = torch.zeros(B, dtype=torch.float64, device=Ad.device)
     passes = torch.zeros(B, dtype=torch.int32, device=Ad.device)
     lib = _lib.load()
+    ws, wp, wb = _block_ws(n, B, Ad.device)
     if M2 is None and zero_shortcut:
         rc = lib.lgm_est_power_norm_f64(Ad.data_ptr(), n, B, n, int(p1), int(itmax), est.data_ptr(),
-                                        passes.data_ptr(), _stream(Ad.device))
+                                        passes.data_ptr(), wp, wb, _stream(Ad.device))
     else:
         M2d = None
         if M2 is not None:
             M2d, _, _ = _dev(M2)
         rc = lib.lgm_est_product_norm_f64(Ad.data_ptr(), int(p1), M2d.data_ptr() if M2d is not None else None, n, B,
-                                          n, int(itmax), est.data_ptr(), passes.data_ptr(), _stream(Ad.device))
+                                          n, int(itmax), est.data_ptr(), passes.data_ptr(), wp, wb,
+                                          _stream(Ad.device))
     _lib.check(rc, "lgm_est_*_norm_f64")
     e, p = est.cpu().numpy(), passes.cpu().numpy()
     return (float(e[0]), int(p[0])) if squeeze else (e, p)
@@ -135,8 +148,9 @@ def balance_batched(A, max_sweeps=100):
     Bo = torch.empty_like(Ad)
     sc = torch.empty((B, n), dtype=torch.float64, device=Ad.device)
     sw = torch.zeros(B, dtype=torch.int32, device=Ad.device)
+    ws, wp, wb = _block_ws(n, B, Ad.device)
     _lib.check(_lib.load().lgm_balance_f64(Ad.data_ptr(), Bo.data_ptr(), sc.data_ptr(), n, B, n, int(max_sweeps),
-                                           sw.data_ptr(), _stream(Ad.device)), "lgm_balance_f64")
+                                           sw.data_ptr(), wp, wb, _stream(Ad.device)), "lgm_balance_f64")
     return _out(Bo, was_numpy, squeeze), sc.cpu().numpy(), sw.cpu().numpy()
 
 
@@ -157,8 +171,9 @@ def eval_degopt(k, A, counter=None, first_product=None):
         FP, _, _ = _dev(first_product)
     Z = torch.empty_like(Ad)
     pr = torch.zeros(B, dtype=torch.int32, device=Ad.device)
+    ws, wp, wb = _block_ws(n, B, Ad.device)
     _lib.check(_lib.load().lgm_eval_degopt_f64(Ad.data_ptr(), FP.data_ptr() if FP is not None else None,
-                                               Z.data_ptr(), n, B, n, k, pr.data_ptr(), _stream(Ad.device)),
+                                               Z.data_ptr(), n, B, n, k, pr.data_ptr(), wp, wb, _stream(Ad.device)),
                "lgm_eval_degopt_f64")
     if counter is not None:
         counter.products += int(pr.cpu().numpy().sum())
