@@ -2878,7 +2878,11 @@ bool graph_debug() {
   static const bool on = std::getenv("LGM_GRAPH_DEBUG") != nullptr;
   return on;
 }
-#define GDBG(...) do { if (graph_debug()) { std::fprintf(stderr, "[lgm graph] " __VA_ARGS__); std::fputc('\n', stderr); std::fflush(stderr); } } while (0)
+double gdbg_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+#define GDBG(...) do { if (graph_debug()) { std::fprintf(stderr, "[lgm graph %9.3f ms] ", gdbg_ms()); std::fprintf(stderr, __VA_ARGS__); std::fputc('\n', stderr); std::fflush(stderr); } } while (0)
 inline int cap_launch() { ++t_cap_nodes; return 0; }
 #define GL cap_launch(),
 
@@ -3381,7 +3385,9 @@ int set_attrs(int n) {
 }
 
 int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
+  GDBG("build_exec start");
   if (set_attrs(k.n)) return LGM_ERR_CUDA;
+  GDBG("attrs set");
   CapStreams cs;
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -3389,6 +3395,7 @@ int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
   for (int i = 4; i < 8; ++i) CK(cudaStreamCreateWithPriority(&cs.s[i], cudaStreamNonBlocking, hi));
   CK(cudaEventCreateWithFlags(&cs.evN, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&cs.evP, cudaEventDisableTiming));
+  GDBG("streams created");
   Cap C;
   C.n = k.n;
   C.batch = k.batch;
@@ -3427,6 +3434,7 @@ int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
   e = cudaGraphInstantiate(out, g, 0);
   GDBG("instantiate: %s", cudaGetErrorString(e));
   cudaGraphDestroy(g);
+  GDBG("graph destroyed");
   if (e != cudaSuccess) {
     std::fprintf(stderr, "logmpoly_b200 grid: graph instantiate failed (%s)\n", cudaGetErrorString(e));
     return LGM_ERR_CUDA;
@@ -3449,6 +3457,7 @@ int run_prog(const GraphKey& k0, void* ws, const CallDesc& d, cudaStream_t st) {
   if (!ent) {
     cudaGraphExec_t ex = nullptr;
     if (build_exec(k, ws, &ex)) return LGM_ERR_CUDA;
+    GDBG("build_exec done (streams destroyed)");
     if (g_cache.size() >= CACHE_MAX) {
       auto old = std::min_element(g_cache.begin(), g_cache.end(),
                                   [](const GraphEntry& a, const GraphEntry& b) { return a.used < b.used; });
@@ -3459,7 +3468,9 @@ int run_prog(const GraphKey& k0, void* ws, const CallDesc& d, cudaStream_t st) {
     ent = &g_cache.back();
   }
   ent->used = ++g_cache_tick;
+  GDBG("launch");
   CK(cudaGraphLaunch(ent->exec, st));
+  GDBG("launched");
   return 0;
 }
 

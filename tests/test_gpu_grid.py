@@ -262,3 +262,50 @@ def test_sqrt_db_g2_small_failures():
     assert its[1] == 0 and its[2] == 50
     Xo, ito = P.sqrt_db(good)
     assert its[0] == ito and rel_err(X[0], Xo) <= 1e-12
+
+
+def test_grid_call_is_stream_ordered_and_nonblocking():
+    """lgm_logm_f64 for n > 64 is one CUDA-graph launch with device-side loops: the host
+    call returns while the stream is still busy (no cudaStreamSynchronize anywhere), and the
+    result equals the synchronous run bit for bit."""
+    import time
+    from paper_2401_10089_b200 import _lib, driver
+    A = torch.from_numpy(synth.config(4, batch=4, n=256)).cuda()
+    opts = lp.LogmOptions(raise_on_error=False)
+    s = torch.cuda.current_stream()
+    L0, r0, _ = driver.run_device(A, opts, s)                 # capture + instantiate (cached per
+    torch.cuda.synchronize()                                  # workspace; the driver reuses it)
+    n0 = _lib.launch_count()
+    torch.cuda._sleep(3_000_000_000)                          # ~1.5 s of GPU spin ahead of the call
+    t0 = time.perf_counter()
+    L1, r1, _ = driver.run_device(A, opts, s)
+    dt = time.perf_counter() - t0
+    assert not s.query()                                      # still queued behind the spin
+    torch.cuda.synchronize()
+    assert dt < 0.5, dt
+    assert torch.equal(L0, L1) and torch.equal(r0, r1)
+    assert _lib.launch_count() - n0 > 100                     # kernels executed inside the graph
+
+
+def test_sharding_bitwise_large_n():
+    """a matrix's arithmetic must not depend on its batch-mates (rank-64 / rank-32
+    passes chosen by n only).  n = 576 (G2 cluster panels): batch of 3 vs each matrix alone."""
+    A = synth.config("5b", batch=3, n=576)
+    L3, r3 = lp.logm_batched(A)
+    for b in range(3):
+        L1, r1 = lp.logm_batched(A[b:b + 1])
+        assert np.array_equal(L1[0], L3[b]) and r1.tobytes() == r3[b:b + 1].tobytes()
+
+
+def test_graph_cache_distinct_workspaces_and_shapes():
+    """The per-(workspace, n, batch) graph cache: interleaved calls of different shapes and
+    workspaces reproduce their own first results exactly."""
+    outs = {}
+    for rep in range(2):
+        for n, B in ((80, 3), (96, 5), (80, 2)):
+            A = synth.config("3b", batch=B, n=n)
+            L, r = lp.logm_batched(A, lp.LogmOptions(raise_on_error=False))
+            if rep == 0:
+                outs[(n, B)] = (L, r)
+            else:
+                assert np.array_equal(outs[(n, B)][0], L) and outs[(n, B)][1].tobytes() == r.tobytes()

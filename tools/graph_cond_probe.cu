@@ -2,6 +2,7 @@
 // two-stream fork/join inside the inner body (the pattern Engine G's device-driven
 // Algorithm 1 relies on).  Prints the counters and the per-launch time of the graph.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -o tools/graph_cond_probe tools/graph_cond_probe.cu
+#include <chrono>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -15,6 +16,7 @@ __global__ void set_outer(cudaGraphConditionalHandle h, int* c) {
   if (threadIdx.x == 0) { c[6]++; cudaGraphSetConditional(h, c[6] < 3); }
 }
 __global__ void empty_exit(const int* flag) { if (*flag) return; }
+__global__ void spin(long long cycles) { long long t0 = clock64(); while (clock64() - t0 < cycles) { } }
 
 static int add_while(cudaStream_t st, cudaGraphConditionalHandle* h, cudaGraph_t* body, unsigned init) {
   cudaStreamCaptureStatus cs;
@@ -86,6 +88,15 @@ int main() {
   printf("counters: start %d outer %d inner %d fork %d join %d innerflag %d outerflag %d end %d\n", h[0], h[1], h[2],
          h[3], h[4], h[5], h[6], h[7]);
   printf("expect:   start 1 outer 3 inner 12 fork 12 join 12 innerflag 12 outerflag 3 end 1\n");
+  {  // does launching a graph with conditional nodes block the host behind earlier stream work?
+    spin<<<1, 1, 0, s0>>>(2000000000LL);
+    auto h0 = std::chrono::steady_clock::now();
+    CK(cudaGraphLaunch(ex, s0));
+    auto h1 = std::chrono::steady_clock::now();
+    printf("host time of cudaGraphLaunch behind a ~1 s spin: %.3f ms (query %d)\n",
+           std::chrono::duration<double, std::milli>(h1 - h0).count(), (int)cudaStreamQuery(s0));
+    CK(cudaStreamSynchronize(s0));
+  }
   // timing: empty-exit launches (capture 200 in a graph)
   int* flag;
   CK(cudaMalloc(&flag, 4));
