@@ -55,6 +55,11 @@ bool use_g1(int n) {
   return n <= 256 || (n <= 512 && n % 64 != 0);
 }
 
+// Out-of-place inversion (the job reads its matrix from Src, no copy pass): G1, and G2 with
+// single-CTA panels and rank-64 passes (n <= 512, n % 64 == 0) whose first pair reads the
+// columns not yet written from Src.
+bool inv_oop(int n) { return use_g1(n) || (n <= 512 && n % 64 == 0 && !(std::getenv("LGM_G2_RANK64") && std::getenv("LGM_G2_RANK64")[0] == '0')); }
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -563,6 +568,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   bool used = tid < n ? (J.rowstep[tid] >= 0) : true;
   double r[32];
   double* M = J.M;
+  // out-of-place first pair: columns not yet written in M are read from Src
+  const double* Mi = (J.Src && k0 < 2 * NB) ? J.Src : M;
   // full panels move through a per-warp 32 x 33 shared tile: the warp reads / writes its 32
   // rows' 256-byte segments coalesced (one row per instruction) instead of one strided
   // 256-byte segment per lane
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   if (tiled) {
     if (warp * 32 < n) {
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) r[rr] = M[(size_t)(warp * 32 + rr) * n + k0 + lane];  // all in flight
+      for (int rr = 0; rr < 32; ++rr) r[rr] = Mi[(size_t)(warp * 32 + rr) * n + k0 + lane];  // all in flight
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = r[rr];
       __syncwarp();
@@ -586,12 +593,12 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
 #pragma unroll
     for (int c = 0; c < 32; c += 2) {
       if (tid < n && c + 1 < nb && (n & 1) == 0) {
-        const double2 v = *reinterpret_cast<const double2*>(&M[(size_t)tid * n + k0 + c]);
+        const double2 v = *reinterpret_cast<const double2*>(&Mi[(size_t)tid * n + k0 + c]);
         r[c] = v.x;
         r[c + 1] = v.y;
       } else {
-        r[c] = (tid < n && c < nb) ? M[(size_t)tid * n + k0 + c] : 0.0;
-        r[c + 1] = (tid < n && c + 1 < nb) ? M[(size_t)tid * n + k0 + c + 1] : 0.0;
+        r[c] = (tid < n && c < nb) ? Mi[(size_t)tid * n + k0 + c] : 0.0;
+        r[c + 1] = (tid < n && c + 1 < nb) ? Mi[(size_t)tid * n + k0 + c + 1] : 0.0;
       }
     }
   }
@@ -603,7 +610,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
     const int p1 = k0 - NB;
     for (int idx = tid; idx < 32 * 32; idx += NT) {
       const int c1 = idx >> 5, c = idx & 31;
-      w1s[c1][c] = M[(size_t)J.piv[p1 + c1] * n + k0 + c];
+      w1s[c1][c] = Mi[(size_t)J.piv[p1 + c1] * n + k0 + c];
     }
     __syncthreads();
     if (tid < n) {
@@ -1022,7 +1029,8 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
   for (int idx = tid; idx < NB * 32; idx += 128) {  // W1 rows, 16-byte chunks
     const int cc = idx >> 5, jj = (idx & 31) * 2;
     const int j = j0 + jj;
-    double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)p1s[cc] * n + j]);
+    const double* Ms = (J.Src && k0 == 0 && j >= 2 * NB) ? J.Src : J.M;  // out-of-place first pair
+    double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)p1s[cc] * n + j]);
     if (j >= k0 && j < k0 + NB) v = make_double2(0.0, 0.0);
     *reinterpret_cast<double2*>(&w1s[cc][jj]) = v;
     *reinterpret_cast<double2*>(&W1[(size_t)cc * n + j]) = v;
@@ -1034,7 +1042,9 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
-      const double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)p2s[mi * 8 + g8] * n + j0 + wc + ni * 8 + 2 * t4]);
+      const int jc = j0 + wc + ni * 8 + 2 * t4;
+      const double* Ms = (J.Src && k0 == 0 && jc >= 2 * NB) ? J.Src : J.M;
+      const double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)p2s[mi * 8 + g8] * n + jc]);
       acc[mi][ni][0] = v.x;
       acc[mi][ni][1] = v.y;
     }
@@ -1107,6 +1117,8 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
   // C fragments while the tiles land; z1 / z2 masks per row
   double acc[4][4][2];
   bool z2r[4];
+  // out-of-place first pair: columns beyond the pair are still only in Src
+  const double* Cs = (J.Src && k0 == 0 && c0 >= 2 * NB) ? J.Src : J.M;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
     const int i = r0 + mi * 8 + g;
@@ -1117,7 +1129,7 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
     for (int ni = 0; ni < 4; ++ni) {
       const int j = c0 + ni * 8 + 2 * t;  // j, j+1 on the same side of every 32-aligned boundary
       const bool keep = (j >= p1lo && j < p2lo) ? z2 : (z1 && z2);
-      const double2 v = *reinterpret_cast<const double2*>(&J.M[(size_t)i * n + j]);
+      const double2 v = *reinterpret_cast<const double2*>(&Cs[(size_t)i * n + j]);
       acc[mi][ni][0] = keep ? v.x : 0.0;
       acc[mi][ni][1] = keep ? v.y : 0.0;
     }
@@ -2228,10 +2240,26 @@ __device__ __forceinline__ void count_nodes(int nodes) {
   if (threadIdx.x == 0) atomicAdd(&g_exec_nodes, (unsigned long long)nodes);
 }
 
+// Device-side phase timer (diagnostics: lgm_debug_grid_phase_ns): every decide kernel charges
+// the globaltimer interval since the previous mark to the phase that just ended.  One stream
+// at a time (a process-wide accumulator).
+enum { PH_LOAD = 0, PH_BALANCE, PH_ALPHA, PH_DB, PH_SELPREP, PH_SELECT, PH_POLY, PH_OTHER, PH_N };
+__device__ unsigned long long g_phase_ns[PH_N];
+__device__ unsigned long long g_phase_last;
+__device__ __forceinline__ void phase_mark(int ph, bool start = false) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (!start) g_phase_ns[ph] += now - g_phase_last;
+    g_phase_last = now;
+  }
+}
+
 // ------------------------------------------------------------------ setup / init / load
 __global__ void setup_kernel(CallDesc* d, CallDesc v) { *d = v; }
 
 __global__ void __launch_bounds__(CT) ctl_init_kernel(Ctl c) {
+  phase_mark(PH_OTHER, true);
   for (int b = threadIdx.x; b < c.batch; b += CT) {
     MDev& M = c.ms[b];
     memset(&M, 0, sizeof(MDev));
@@ -2256,6 +2284,7 @@ __global__ void fill_kernel(double* p, size_t count, double v) {
 // as_square (matcore.py:64-65): non-finite input -> NONFINITE; the rest is the live list
 __global__ void __launch_bounds__(CT) decide_live_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_LOAD);
   int off = 0;
   FOR_LIST(c, LS_ALL)
     const bool bad = b >= 0 && c.flag[b];
@@ -2268,6 +2297,7 @@ __global__ void __launch_bounds__(CT) decide_live_kernel(Ctl c) {
 
 // finish = ||B - I||_1 <= Theta_K, after balancing
 __global__ void __launch_bounds__(CT) decide_start_kernel(Ctl c) {
+  phase_mark(PH_BALANCE);
   const LgmParams& P = c.desc->P;
   const double thK = P.theta[P.max_k - 1];
   FOR_LIST(c, LS_LIVE)
@@ -2288,6 +2318,7 @@ __device__ __forceinline__ bool scal_active(const MDev& M, const LgmParams& P) {
 // scaling-loop head: act = live matrices still scaling; act_ai2 = those with A_I2
 __global__ void __launch_bounds__(CT) decide_act_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_OTHER);
   const LgmParams& P = c.desc->P;
   int off = 0, off2 = 0;
   FOR_LIST(c, LS_LIVE)
@@ -2437,6 +2468,7 @@ __global__ void __launch_bounds__(CT) scal_req_kernel(Ctl c) {
 // finish = alpha <= Theta_K; roots = matrices taking another square root
 __global__ void __launch_bounds__(CT) decide_roots_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_ALPHA);
   const LgmParams& P = c.desc->P;
   const double thK = P.theta[P.max_k - 1];
   int off = 0;
@@ -2462,6 +2494,7 @@ __global__ void __launch_bounds__(CT) decide_roots_kernel(Ctl c) {
 __global__ void __launch_bounds__(CT) decide_post_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes) {
   __shared__ int s_w[33];
   __shared__ int s_any;
+  phase_mark(PH_DB);
   const LgmParams& P = c.desc->P;
   if (threadIdx.x == 0) s_any = 0;
   int off = 0;
@@ -2546,6 +2579,7 @@ __global__ void __launch_bounds__(CT) decide_db_start_kernel(Ctl c) {
 __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes, int first,
                                                         int block_mode) {
   __shared__ int s_w[33];
+  phase_mark(PH_DB);
   const CallDesc& D = *c.desc;
   const int n = c.n;
   const double tol_in = block_mode ? D.tol : D.P.db_tol;
@@ -2592,6 +2626,7 @@ __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphCondition
 // ------------------------------------------------------------------ select_order (A.3)
 __global__ void __launch_bounds__(CT) decide_sel_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_OTHER);
   int off = 0, off2 = 0;
   FOR_LIST(c, LS_LIVE)
     bool sel = false, need = false;
@@ -2618,6 +2653,7 @@ __device__ int first_index(MDev& M, double x, const LgmParams& P) {
 // min_im (Eqs. 29-31 + tabmin_im), max_in (Eqs. 32-34); immediate choice or the sweep list
 __global__ void __launch_bounds__(CT) select_init_kernel(Ctl c, cudaGraphConditionalHandle h) {
   __shared__ int s_w[33];
+  phase_mark(PH_SELPREP);
   const LgmParams& P = c.desc->P;
   const int K = P.max_k;
   const int mK = P.order[K - 1];
@@ -2672,6 +2708,7 @@ __global__ void __launch_bounds__(CT) select_init_kernel(Ctl c, cudaGraphConditi
 
 __global__ void __launch_bounds__(CT) select_step_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes) {
   __shared__ int s_w[33];
+  phase_mark(PH_SELECT);
   const LgmParams& P = c.desc->P;
   int off = 0;
   FOR_LIST(c, LS_CUR)
@@ -2701,6 +2738,7 @@ __constant__ int c_node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
 
 __global__ void __launch_bounds__(CT) decide_poly_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_SELECT);
   for (int j = 1; j < LGM_K_MAX; ++j) {
     int off = 0;
     FOR_LIST(c, LS_SEL)
@@ -2756,6 +2794,7 @@ __global__ void poly_final_kernel(Slots S, DList L, const CallDesc* d, const MDe
 // products of the polynomial, non-finite results (estimator overflow upstream), failures
 __global__ void __launch_bounds__(CT) decide_final_kernel(Ctl c) {
   __shared__ int s_w[33];
+  phase_mark(PH_POLY);
   {
     FOR_LIST(c, LS_SEL)
       if (b >= 0) {
@@ -2790,6 +2829,7 @@ __global__ void nan_fill_kernel(Slots S, DList L, const CallDesc* d) {
 
 __global__ void report_kernel(Ctl c, int nodes) {
   const CallDesc& D = *c.desc;
+  phase_mark(PH_OTHER);
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < c.batch; b += gridDim.x * blockDim.x) {
     const MDev& M = c.ms[b];
     lgm_report r;
@@ -3110,7 +3150,7 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
 int cap_db_iter(Cap& C, cudaStream_t st, bool first, cudaGraphConditionalHandle h, int block_mode) {
   const int n = C.n;
   const int n0 = t_cap_nodes;
-  const bool oop = use_g1(n);
+  const bool oop = inv_oop(n);
   GL build_jobs_kernel<<<1, CT, 0, st>>>(C.c, first ? 1 : 0, oop ? 1 : 0);
   if (!oop) {  // G2 inverts in place: copies first
     if (cap_ew(C, st, LS_DB, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
@@ -3570,4 +3610,60 @@ extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
   (void)out;
   return 0;
 #endif
+}
+
+// Engine G phase times (ns, accumulated on the current device; diagnostics): load, balance,
+// alpha (scaling-loop estimates), DB (inversions + updates), select prep, select, poly, other.
+extern "C" int lgm_debug_grid_phase_ns(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_phase_ns, sizeof(unsigned long long) * PH_N) != cudaSuccess) return -2;
+  if (reset) {
+    unsigned long long z[PH_N] = {};
+    cudaMemcpyToSymbol(g_phase_ns, z, sizeof(z));
+  }
+  return PH_N;
+}
+
+// Inversion micro-benchmark (diagnostics; tools/inv_bench.py): the batched Gauss-Jordan of
+// Engine G on 2*batch jobs (X and Y slots loaded from A), launched directly on `stream`
+// (no graph, so ncu sees every kernel).  Each rep re-copies the inputs into the job slots.
+extern "C" int lgm_debug_invert_f64(const double* A, int64_t n64, int64_t batch64, int reps, void* ws,
+                                    cudaStream_t st) {
+  const int n = (int)n64, batch = (int)batch64;
+  if (n <= 64 || !ws) return LGM_ERR_ARG;
+  if (set_attrs(n)) return LGM_ERR_CUDA;
+  CapStreams cs;
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&cs.s[4], cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&cs.evN, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&cs.evP, cudaEventDisableTiming));
+  Cap C;
+  C.n = n;
+  C.batch = batch;
+  C.c = ctl_carve(ws, n, batch);
+  for (int i = 0; i < 4; ++i) { C.s[i] = st; C.sB[i] = cs.s[4]; }
+  C.evN = cs.evN;
+  C.evP = cs.evP;
+  C.itmax = 5;
+  CallDesc d = desc_base(LgmParams{});
+  d.A = A;
+  d.ld = n;
+  setup_kernel<<<1, 1, 0, st>>>(C.c.desc, d);
+  ctl_init_kernel<<<1, CT, 0, st>>>(C.c);
+  load_kernel<<<ew_blocks(), 256, 0, st>>>(&C.c.desc->A, &C.c.desc->ld, C.c.S, C.c.list(LS_ALL), C.c.flag);
+  ew_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), 1, G_Y, G_B, G_B);
+  decide_live_kernel<<<1, CT, 0, st>>>(C.c);
+  decide_db_start_kernel<<<1, CT, 0, st>>>(C.c);
+  const bool oop = inv_oop(n);
+  for (int r = 0; r < reps; ++r) {
+    build_jobs_kernel<<<1, CT, 0, st>>>(C.c, 0, oop ? 1 : 0);
+    if (!oop) {
+      ew_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_DB), 1, G_XI, G_B, G_B);
+      ew_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_DB), 1, G_YI, G_Y, G_Y);
+    }
+    if (cap_invert(C, st, 2 * batch)) return LGM_ERR_CUDA;
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return 0;
 }
