@@ -21,6 +21,8 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "lgm_grid.cuh"
 
@@ -548,20 +550,27 @@ __device__ unsigned long long g_panel_cyc[6];  // load, stage-1, factor, store, 
 // of the 32-column panel in registers, the pivot rule and shift-in-FMA frame of G1
 // (gj_inv_cta_kernel).  No cluster: with hundreds of jobs the 8-CTA cluster panel's
 // per-step cluster barriers serialise into many waves.
-template <int NT>
 // s1_a1kind >= 0 (P2 of a rank-64 pair): the stage-1 update of P2's columns by P1 is applied
 // to the loaded rows first (r <- z1 r + A1 W1[:, P2], FMA chain in c' order), replacing the
 // narrow gj_update_kernel launch and its snapshot.
-__global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob* jobs, int n, int k0, int nb, int a1_kind,
-                                                                   int s1_a1kind) {
+struct PanelSmem {
+  double prow[2][40];
+  unsigned wkey32[2][16];
+  double wval[2][16];
+  double red[16];
+  int piv_s[32];
+  double w1s[32][34];
+};
+// Returns false when the panel hit an exact zero pivot (status set).
+template <int NT>
+__device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int nb, int a1_kind, int s1_a1kind,
+                                           PanelSmem& ps, double* ptile) {
   constexpr int NW = NT / 32;
-  __shared__ __align__(16) double prow[2][40];
-  __shared__ unsigned wkey32[2][16];
-  __shared__ double wval[2][16];
-  __shared__ double red[16];
-  __shared__ int piv_s[32];
-  const InvJob J = jobs[blockIdx.x];
-  if (*J.status) return;  // uniform per CTA
+  auto& prow = ps.prow;
+  auto& wkey32 = ps.wkey32;
+  auto& wval = ps.wval;
+  auto& red = ps.red;
+  auto& piv_s = ps.piv_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < 80) (&prow[0][0])[tid] = 0.0;  // pure-rotation steps read it with g = 0
   PP_T(t0);
@@ -573,7 +582,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   // full panels move through a per-warp 32 x 33 shared tile: the warp reads / writes its 32
   // rows' 256-byte segments coalesced (one row per instruction) instead of one strided
   // 256-byte segment per lane
-  extern __shared__ __align__(16) double ptile[];
   double* T = ptile + warp * 32 * 33;
   const bool tiled = nb == 32 && (n & 31) == 0;
   if (tiled) {
@@ -606,7 +614,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   PP_T(t1);
   PP_ADD(0, t1 - t0);
   if (s1_a1kind >= 0) {
-    __shared__ __align__(16) double w1s[32][34];
+    auto& w1s = ps.w1s;
     const int p1 = k0 - NB;
     for (int idx = tid; idx < 32 * 32; idx += NT) {
       const int c1 = idx >> 5, c = idx & 31;
@@ -660,7 +668,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
       const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par][lane] : 0u);
       if (bk == 0u) {  // exact zero pivot (matcore.py:124-125)
         if (tid == 0) *J.status = 1;
-        return;
+        return false;
       }
       const int p = 1023 - (int)(bk & 0x3ffu);
       const double rp = lgm_rcp(wval[par][p >> 5]);
@@ -740,6 +748,33 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob
   PP_T(t4);
   PP_ADD(3, t4 - t3);
   PP_ADD(4, 1);
+  return true;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) gj_panel_cta_kernel(const InvJob* jobs, int n, int k0, int nb, int a1_kind,
+                                                                   int s1_a1kind) {
+  __shared__ __align__(16) PanelSmem ps;
+  extern __shared__ __align__(16) double ptile[];
+  const InvJob J = jobs[blockIdx.x];
+  if (*J.status) return;  // uniform per CTA
+  panel_body<NT>(J, n, k0, nb, a1_kind, s1_a1kind, ps, ptile);
+}
+
+// Both panels of a rank-64 pair in one launch (one CTA per job): P1 [k0, k0+NB) writing its
+// multiplier copy A1 (kind a1_kind), then P2 [k0+NB, k0+2NB) with P1's stage-1 update fused
+// (the same CTA wrote everything P2 reads: a block-scope fence orders it).  One wave tail and
+// one launch per pair instead of two.
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) gj_panel_pair_kernel(const InvJob* jobs, int n, int k0, int a1_kind) {
+  __shared__ __align__(16) PanelSmem ps;
+  extern __shared__ __align__(16) double ptile[];
+  const InvJob J = jobs[blockIdx.x];
+  if (*J.status) return;
+  if (!panel_body<NT>(J, n, k0, NB, a1_kind, -1, ps, ptile)) return;
+  __threadfence_block();
+  __syncthreads();
+  panel_body<NT>(J, n, k0 + NB, NB, -1, a1_kind, ps, ptile);
 }
 
 __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n, int k0, int nb, int in_smem) {
@@ -1008,7 +1043,8 @@ __global__ void __launch_bounds__(128) gj_w2_kernel(const InvJob* jobs, int n, i
 // W2[c][j] = M[p2_c][j] + sum_cc A1[p2_c][cc] W1[cc][j] as a 32 x 64 x 32 product (warp w:
 // all 32 rows c, columns 16w..16w+15), W1[cc][j] = M[p1_cc][j] read once (not snapshotted
 // beforehand).  P1 columns: W1 = 0, W2 = A1[p2_c][j - k0]; P2 columns: W2 = 0.
-__global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int n, int k0, int q) {
+// wt = 1: W1 / W2 stored transposed (n x NB per kind) for gj_update2_tma_kernel's TMA tiles
+__global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int n, int k0, int q, int wt) {
   __shared__ __align__(16) double a1s[NB][NB + 4];
   __shared__ __align__(16) double w1s[NB][64 + 4];
   __shared__ int p1s[NB], p2s[NB];
@@ -1033,9 +1069,15 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
     double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)p1s[cc] * n + j]);
     if (j >= k0 && j < k0 + NB) v = make_double2(0.0, 0.0);
     *reinterpret_cast<double2*>(&w1s[cc][jj]) = v;
-    *reinterpret_cast<double2*>(&W1[(size_t)cc * n + j]) = v;
+    if (!wt) *reinterpret_cast<double2*>(&W1[(size_t)cc * n + j]) = v;
   }
   __syncthreads();
+  if (wt) {  // transposed: the 64 x NB block W1T[j0 .. j0+64) is contiguous
+    for (int idx = tid; idx < 64 * NB; idx += 128) {
+      const int jj = idx >> 5, cc = idx & 31;
+      W1[(size_t)(j0 + jj) * NB + cc] = w1s[cc][jj];
+    }
+  }
   const int g8 = lane >> 2, t4 = lane & 3, wc = warp * 16;
   double acc[4][2][2];
 #pragma unroll
@@ -1060,6 +1102,7 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
   }
+  if (wt) __syncthreads();  // every warp is done reading w1s before it stages W2
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
     const int c = mi * 8 + g8;
@@ -1069,7 +1112,19 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
       double2 v = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
       if (j >= k0 && j < k0 + NB) v = make_double2(a1s[c][j - k0], a1s[c][j + 1 - k0]);
       else if (j >= k0 + NB && j < k0 + 2 * NB) v = make_double2(0.0, 0.0);
-      *reinterpret_cast<double2*>(&W2[(size_t)c * n + j]) = v;
+      if (wt) {  // staged (w1s is free now) for a contiguous transposed store
+        w1s[c][j - j0] = v.x;
+        w1s[c][j + 1 - j0] = v.y;
+      } else {
+        *reinterpret_cast<double2*>(&W2[(size_t)c * n + j]) = v;
+      }
+    }
+  }
+  if (wt) {
+    __syncthreads();
+    for (int idx = tid; idx < 64 * NB; idx += 128) {
+      const int jj = idx >> 5, cc = idx & 31;
+      W2[(size_t)(j0 + jj) * NB + cc] = w1s[cc][jj];
     }
   }
 }
@@ -1174,6 +1229,231 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
       const bool in = j >= col_lo && j < col_hi && !(j >= p2lo && j < p2hi) && !(j >= ex_lo && j < ex_hi);
       if (in) *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA-pipelined combined rank-64 pass (n <= 512 with single-CTA panels, n % 64 == 0).
+// One CTA owns a 64-row block of one job and walks its column tiles: the A operands (A1 and
+// P2's multipliers) are staged once, the W1 / W2 column tiles stream through a 2-stage ring
+// filled by TMA (cp.async.bulk.tensor, 128-byte swizzle, mbarrier complete_tx) from a producer
+// warp, and each tile's C fragments are prefetched into registers one tile ahead.  W1 / W2 are
+// stored transposed (n x NB per kind, written by gj_w2_mma_kernel) so the swizzled B-fragment
+// reads are bank-conflict free.
+#ifndef UT_STAGES_DEF
+#define UT_STAGES_DEF 3
+#endif
+#ifndef UT_NWR
+#define UT_NWR 2
+#endif
+constexpr int UT_STAGES = UT_STAGES_DEF;
+constexpr int UT_ROWS = 64 * UT_NWR;                  // rows per CTA (4 compute warps per 64)
+constexpr int UT_THREADS = 128 * UT_NWR;              // thread 0 also issues the TMA loads
+constexpr int UT_BOX = 64 * 16 * 8;                 // one TMA box: 64 W rows (columns of M) x 16 k
+constexpr int UT_STAGE_BYTES = 4 * UT_BOX;           // W1 (2 boxes) + W2 (2 boxes)
+constexpr size_t ut_smem() { return 1024 + (size_t)UT_STAGES * UT_STAGE_BYTES + (size_t)(2 * UT_ROWS * LDA_S + 32) * 8 + 64; }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c_inner, int c_row, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c_inner), "r"(c_row), "r"(smem_u32(bar))
+      : "memory");
+}
+// element (row r, k) of a 64 x 16 box stored with the 128-byte swizzle
+__device__ __forceinline__ int swz(int r, int k) { return r * 16 + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
+
+#ifndef UT_MINB
+#define UT_MINB 1
+#endif
+__global__ void __launch_bounds__(UT_THREADS, UT_MINB) gj_update2_tma_kernel(const InvJob* jobs, int n, int k0, int col_base,
+                                                                 int col_lo, int col_hi, int ex_lo, int ex_hi, int q,
+                                                                 const double* Wbase,
+                                                                 const __grid_constant__ CUtensorMap wmap) {
+  extern __shared__ __align__(16) unsigned char utsm_raw[];
+  // 1024-byte aligned ring (128-byte swizzle), then A1 / A2 tiles, the zero row, barriers
+  unsigned char* base = (unsigned char*)(((uintptr_t)utsm_raw + 1023) & ~(uintptr_t)1023);
+  double* ring = reinterpret_cast<double*>(base);
+  double* As1 = ring + UT_STAGES * UT_STAGE_BYTES / 8;
+  double* As2 = As1 + UT_ROWS * LDA_S;
+  double* Zs = As2 + UT_ROWS * LDA_S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Zs + 32);
+  uint64_t* empty = full + UT_STAGES;
+  const InvJob J = jobs[blockIdx.y];
+  if (*J.status) return;  // uniform per CTA (unused table slots read the always-1 status)
+  const int row0 = blockIdx.x * UT_ROWS;
+  const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NCW = 4 * UT_NWR;  // compute warps
+  // the column tiles this CTA writes, in order
+  const int ntile_all = (col_hi - col_base + 63) / 64;
+  auto tile_ok = [&](int t) {
+    const int c0 = col_base + t * 64;
+    if (c0 >= col_hi || c0 + 64 <= col_lo) return false;
+    if (c0 >= p2lo && c0 + 64 <= p2hi) return false;
+    if (c0 >= ex_lo && c0 + 64 <= ex_hi) return false;
+    return true;
+  };
+  // W row index of (kind, column j): rows of the transposed W region, NB doubles each
+  const long long w1row = (long long)(wkind(J, 3 * q) - Wbase) / NB;
+  const long long w2row = (long long)(wkind(J, 3 * q + 1) - Wbase) / NB;
+  if (tid == 0) {
+    for (int s = 0; s < UT_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // A1 rows and P2's multipliers (M columns [p2lo, p2hi)) of this row block, once
+  {
+    const double* A1 = wkind(J, 3 * q + 2);
+    for (int idx = tid; idx < UT_ROWS * (NB / 2); idx += UT_THREADS) {
+      const int r = idx / (NB / 2), c = (idx - r * (NB / 2)) * 2;
+      if (row0 + r >= n) break;  // last row block of n % UT_ROWS != 0 (n % 64 == 0)
+      cp_async16(&As1[r * LDA_S + c], &A1[(size_t)(row0 + r) * NB + c]);
+      cp_async16(&As2[r * LDA_S + c], &J.M[(size_t)(row0 + r) * n + p2lo + c]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (tid < 32) Zs[tid] = 0.0;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  // consumers: warp w owns rows (w/2)*32.., columns (w%2)*32.. of each UT_ROWS x 64 tile
+  const int g = lane >> 2, t4 = lane & 3;
+  const int lr0 = (warp >> 1) * 32, lc0 = (warp & 1) * 32;
+  const int r0 = row0 + lr0;
+  const bool rows_ok = r0 < n;  // (a warp's 32 rows are all in range or all out: n % 64 == 0)
+  bool z1r[4], z2r[4];
+  int aoff[4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int rs = rows_ok ? J.rowstep[r0 + mi * 8 + g] : -1;
+    z1r[mi] = !(rs >= p1lo && rs < p2lo);
+    z2r[mi] = !(rs >= p2lo && rs < p2hi);
+    aoff[mi] = z2r[mi] ? (lr0 + mi * 8 + g) * LDA_S : (int)(Zs - As1);
+  }
+  auto load_c = [&](int c0, double (&cv)[4][4][2]) {
+    if (!rows_ok) return;
+    const double* Cs = (J.Src && k0 == 0 && c0 + lc0 >= 2 * NB) ? J.Src : J.M;  // out-of-place first pair
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const double2 v = *reinterpret_cast<const double2*>(&Cs[(size_t)(r0 + mi * 8 + g) * n + c0 + lc0 + ni * 8 + 2 * t4]);
+        cv[mi][ni][0] = v.x;
+        cv[mi][ni][1] = v.y;
+      }
+  };
+  // TMA issue (thread 0): the ring runs UT_STAGES tiles ahead of the consumers
+  int tiss = 0, sis = 0;
+  unsigned phis = 0;
+  auto issue_next = [&]() {
+    while (tiss < ntile_all && !tile_ok(tiss)) ++tiss;
+    if (tiss >= ntile_all) return;
+    const int c0 = col_base + tiss * 64;
+    mbar_wait(&empty[sis], phis ^ 1u);
+    mbar_expect_tx(&full[sis], UT_STAGE_BYTES);
+    double* st = ring + (size_t)sis * (UT_STAGE_BYTES / 8);
+    tma_load_2d(st, &wmap, 0, (int)(w1row + c0), &full[sis]);
+    tma_load_2d(st + UT_BOX / 8, &wmap, 16, (int)(w1row + c0), &full[sis]);
+    tma_load_2d(st + 2 * UT_BOX / 8, &wmap, 0, (int)(w2row + c0), &full[sis]);
+    tma_load_2d(st + 3 * UT_BOX / 8, &wmap, 16, (int)(w2row + c0), &full[sis]);
+    ++tiss;
+    if (++sis == UT_STAGES) { sis = 0; phis ^= 1u; }
+  };
+  if (tid == 0)
+    for (int s0 = 0; s0 < UT_STAGES; ++s0) issue_next();
+  int tcur = 0;
+  while (tcur < ntile_all && !tile_ok(tcur)) ++tcur;
+  if (tcur >= ntile_all) return;
+  double acc[4][4][2] = {};
+  load_c(col_base + tcur * 64, acc);
+  int stage = 0;
+  unsigned ph = 0;
+  while (tcur < ntile_all) {
+    int tnext = tcur + 1;
+    while (tnext < ntile_all && !tile_ok(tnext)) ++tnext;
+    const int c0 = col_base + tcur * 64;
+    double cn[4][4][2] = {};
+    if (tnext < ntile_all) load_c(col_base + tnext * 64, cn);  // in flight during this tile's MMAs
+    // masks: P1 columns keep z2; other columns keep z1 && z2 (the applied panels' pivot rows)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int j = c0 + lc0 + ni * 8 + 2 * t4;
+        const bool keep = (j >= p1lo && j < p2lo) ? z2r[mi] : (z1r[mi] && z2r[mi]);
+        if (!keep) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+    mbar_wait(&full[stage], ph);
+    const double* st = ring + (size_t)stage * (UT_STAGE_BYTES / 8);
+#pragma unroll
+    for (int k = 0; k < NB; k += 4) {  // + z2 A1 W1
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = As1[aoff[mi] + k + t4];
+      const double* bx = st + ((k >> 4) * UT_BOX / 8);
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = bx[swz(lc0 + ni * 8 + g, (k & 15) + t4)];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+#pragma unroll
+    for (int k = 0; k < NB; k += 4) {  // + A2 W2
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = As2[(lr0 + mi * 8 + g) * LDA_S + k + t4];
+      const double* bx = st + ((2 + (k >> 4)) * UT_BOX / 8);
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = bx[swz(lc0 + ni * 8 + g, (k & 15) + t4)];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == UT_STAGES) { stage = 0; ph ^= 1u; }
+    if (tid == 0) issue_next();  // refill the slot just released (waits for every warp)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i = r0 + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int j = c0 + lc0 + ni * 8 + 2 * t4;
+        const bool in = rows_ok && j >= col_lo && j < col_hi && !(j >= p2lo && j < p2hi) && !(j >= ex_lo && j < ex_hi);
+        if (in) *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      }
+    }
+    if (tnext < ntile_all) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          acc[mi][ni][0] = cn[mi][ni][0];
+          acc[mi][ni][1] = cn[mi][ni][1];
+        }
+    }
+    tcur = tnext;
   }
 }
 
@@ -2945,7 +3225,46 @@ struct Cap {
   }
   cudaEvent_t evN, evP;
   int itmax;
+  bool tma = false;     // rank-64 passes by gj_update2_tma_kernel (W stored transposed)
+  CUtensorMap wmap;     // the W region as (12 batch n) rows x NB doubles, 64 x 16 boxes
 };
+
+// LGM_G2_TMA=1: rank-64 passes by gj_update2_tma_kernel (TMA ring; measured 9.04 vs 8.48 ms
+// per 512-job n = 512 inversion step against the one-tile-per-CTA cp.async kernel, so off
+// by default -- DESIGN.md section 4)
+bool g2_tma_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_G2_TMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// TMA descriptor of the W region (driver entry point; no libcuda link dependency)
+int make_wmap(Cap& C) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode) return LGM_ERR_CUDA;
+  const cuuint64_t rows = (cuuint64_t)12 * C.batch * C.n;
+  cuuint64_t gdim[2] = {(cuuint64_t)NB, rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)NB * 8};
+  cuuint32_t box[2] = {16, 64};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(&C.wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)C.c.W, gdim, gstride, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::fprintf(stderr, "logmpoly_b200 grid: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+    return LGM_ERR_CUDA;
+  }
+  return 0;
+}
 
 dim3 ew_blocks() { return dim3(EW_BLOCKS); }
 
@@ -3079,7 +3398,11 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
   // rank-64 vs rank-32 passes round differently: the choice depends on n only, so a
   // matrix's arithmetic never depends on its batch-mates or on how many have converged
   const bool use64 = rank64 && n % (2 * NB) == 0;
-  panel(0, st, use64 && cta_panel ? 2 : -1);
+  const bool pair0 = use64 && cta_panel && [] {
+    const char* e = std::getenv("LGM_G2_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (!pair0) panel(0, st, use64 && cta_panel ? 2 : -1);
   if (use64) {
     // rank-64 delayed update with both panels of the next pair factored on sB during the
     // current combined pass.  Per pair (P1, P2) in buffer set q: W1 (snapshot of P1's pivot
@@ -3097,27 +3420,53 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
                                                              3 * q);
       panel(k0 + NB, s);
     };
-    prepare_pair(0, 0, st, !cta_panel);
-    if (cta_panel) GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, 0, 0);
+    const bool tma = cta_panel && C.tma;
+    static const bool pair_on = [] {  // LGM_G2_PAIR=0: the two panels as separate launches (A/B)
+      const char* e = std::getenv("LGM_G2_PAIR");
+      return !(e && e[0] == '0');
+    }();
+    const bool pairk = cta_panel && pair_on;
+    auto panel_pair = [&](int k0p, cudaStream_t s, int a1k) {  // both panels of a pair, one launch
+      if (n <= 128) GL gj_panel_pair_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
+      else if (n <= 256) GL gj_panel_pair_kernel<256><<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
+      else GL gj_panel_pair_kernel<512><<<nj, 512, 16 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
+    };
+    auto pass = [&](int k0p, int cb, int clo, int chi, int exlo, int exhi, int qq, bool narrow) {
+      if (tma) {
+        GL gj_update2_tma_kernel<<<dim3((n + UT_ROWS - 1) / UT_ROWS, nj), UT_THREADS, ut_smem(), st>>>(d_jobs, n, k0p, cb, clo, chi, exlo,
+                                                                                      exhi, qq, C.c.W, C.wmap);
+      } else if (narrow) {
+        GL gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0p, cb, clo, chi, exlo,
+                                                                                 exhi, qq);
+      } else {
+        GL gj_update2_kernel<G2_RT><<<dim3(tiles, n / G2_RT, nj), 2 * G2_RT, up2_smem<G2_RT>(), st>>>(
+            d_jobs, n, k0p, cb, clo, chi, exlo, exhi, qq);
+      }
+    };
+    if (pairk) panel_pair(0, st, 2);
+    else prepare_pair(0, 0, st, !cta_panel);
+    if (cta_panel) GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, 0, 0, tma ? 1 : 0);
     else GL gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, 0, 0, 0);
     for (int k0 = 0, q = 0; k0 < n; k0 += 2 * NB, q ^= 1) {
       const int kn = k0 + 2 * NB;
       const bool next = kn < n;
       if (next) {  // finish the next pair's columns, then factor both of its panels on sB
-        GL gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0, kn, kn, kn + 2 * NB,
-                                                                                 0, 0, q);
+        pass(k0, kn, kn, kn + 2 * NB, 0, 0, q, true);
         CK(cudaEventRecord(evN, st));
         CK(cudaStreamWaitEvent(sB, evN, 0));
-        panel(kn, sB, cta_panel ? 3 * (q ^ 1) + 2 : -1);
-        prepare_pair(kn, q ^ 1, sB, false);
+        if (pairk) {
+          panel_pair(kn, sB, 3 * (q ^ 1) + 2);
+        } else {
+          panel(kn, sB, cta_panel ? 3 * (q ^ 1) + 2 : -1);
+          prepare_pair(kn, q ^ 1, sB, false);
+        }
         CK(cudaEventRecord(evP, sB));
       }
-      GL gj_update2_kernel<G2_RT><<<dim3(tiles, n / G2_RT, nj), 2 * G2_RT, up2_smem<G2_RT>(), st>>>(
-          d_jobs, n, k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q);
+      pass(k0, 0, 0, n, next ? kn : 0, next ? kn + 2 * NB : 0, q, false);
       if (next) {  // full-width W1 / W2 of the next pair need this pass's rows
         CK(cudaStreamWaitEvent(st, evP, 0));
         if (cta_panel) {
-          GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1);
+          GL gj_w2_mma_kernel<<<dim3(n / 64, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, tma ? 1 : 0);
         } else {
           snapshot(kn, 3 * (q ^ 1));
           GL gj_w2_kernel<<<dim3((n + 127) / 128, nj), 128, 0, st>>>(d_jobs, n, kn, q ^ 1, 0);
@@ -3417,9 +3766,13 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_panel_cta_kernel<128>, mx, 4 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_panel_cta_kernel<256>, mx, 8 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_panel_cta_kernel<512>, mx, 16 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_pair_kernel<128>, mx, 4 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_pair_kernel<256>, mx, 8 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_pair_kernel<512>, mx, 16 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
   CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(gj_update2_tma_kernel, mx, (int)ut_smem()));
   CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
   return 0;
 }
@@ -3447,6 +3800,8 @@ int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
   C.evN = cs.evN;
   C.evP = cs.evP;
   C.itmax = k.itmax;
+  C.tma = g2_tma_on() && k.n <= 512 && k.n % (2 * NB) == 0 && !use_g1(k.n);
+  if (C.tma && make_wmap(C)) return LGM_ERR_CUDA;
   cudaGraph_t g;
   CK(cudaGraphCreate(&g, 0));
   GDBG("capture prog %d n %d batch %d", k.prog, k.n, k.batch);
@@ -3645,6 +4000,8 @@ extern "C" int lgm_debug_invert_f64(const double* A, int64_t n64, int64_t batch6
   C.evN = cs.evN;
   C.evP = cs.evP;
   C.itmax = 5;
+  C.tma = g2_tma_on() && n <= 512 && n % (2 * NB) == 0 && !use_g1(n);
+  if (C.tma && make_wmap(C)) return LGM_ERR_CUDA;
   CallDesc d = desc_base(LgmParams{});
   d.A = A;
   d.ld = n;

@@ -20,7 +20,7 @@ from paper_2401_10089_b200 import _lib, synth  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-lib = _lib.load()
+lib = _lib.load(os.environ.get("LGM_LIB", _lib.LIB_PATH))  # LGM_LIB: A/B variant builds (make gvariant)
 lib.lgm_debug_invert_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
                                      ctypes.c_void_p]
 A = torch.from_numpy(synth.config(4, batch=B, n=n)).cuda()
