@@ -27,6 +27,7 @@ from paper_2401_10089_b200 import constants as _C  # frozen data only (no produc
 from . import primitives as P
 
 K_MAX = _C.K_MAX
+K_DEFAULT = getattr(_C, "K_DEFAULT", _C.K_MAX)  # reference default (shipped schemes k <= 5)
 THETA = _C.THETA
 ORDER = _C.ORDER
 TABMIN_IM = _C.TABMIN_IM
@@ -202,7 +203,7 @@ def _report(st, status, k=0, balanced=True, sweeps=0, msg=""):
     }
 
 
-def logm_status(A, prims, theta=THETA, order=ORDER, max_k=K_MAX, maxiter=40, do_balance=True):
+def logm_status(A, prims, theta=THETA, order=ORDER, max_k=K_DEFAULT, maxiter=40, do_balance=True):
     """Algorithm 1 (A.1).  Returns (L or None, report dict); never raises for numerical
     failures -- the status code carries them (mirrors the GPU report)."""
     st = _State(prims, theta, order, max_k)

@@ -118,7 +118,7 @@ def build_parser():
     p.add_argument("-o", "--output")
     p.add_argument("--ref", help="reference logarithm file: print Er")
     p.add_argument("--no-balance", action="store_true")
-    p.add_argument("--max-k", type=int, default=C.K_MAX)
+    p.add_argument("--max-k", type=int, default=getattr(C, "K_DEFAULT", C.K_MAX))
     p.add_argument("--check-spectrum", action="store_true", help="eig_small pre-check (n <= 512)")
     p.set_defaults(fn=cmd_logm)
     p = sub.add_parser("gen", help="write a synthetic matrix family")

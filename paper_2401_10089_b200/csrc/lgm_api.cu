@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? LGM_F32_MINB : 1) 
   Ctx<NMAX, FULL> c;
   c.init(smem, n, &P);
   const long long b = blockIdx.x;
-  logm_one<NMAX, FULL>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * 4 * n * n);
+  logm_one<NMAX, FULL>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * LGM_FUSED_WS * n * n);
 }
 
 template <int NMAX>
@@ -176,7 +176,7 @@ extern "C" {
 
 void lgm_default_opts(lgm_opts* o) {
   if (!o) return;
-  o->max_k = LGM_K_MAX;
+  o->max_k = LGM_K_DEFAULT;
   o->maxiter_s = 40;
   o->db_maxiter = 50;
   o->est_itmax = 5;
@@ -227,22 +227,27 @@ static int64_t grid_chunk() {
 
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
-  // n <= 64: one 4 n^2 slot per matrix: polynomial nodes P4..P6 and A_prev / A_I2 (L2 resident)
-  *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * 4 * n * n * sizeof(double)
+  // n <= 64: LGM_FUSED_WS n^2 doubles per matrix: polynomial nodes P4..P10 and A_prev / A_I2
+  // (only P4..P6 and A_I2 are touched with the shipped k <= 5 schemes: L2 resident)
+  *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * LGM_FUSED_WS * n * n * sizeof(double)
                    : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
 }
 
 int lgm_block_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
-  *bytes = n <= LGM_FUSED_MAX ? 0 : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
+  // n <= 64 needs it only for eval_degopt with k > 5 (graph path); sized for every case
+  *bytes = lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
 }
 
-static bool block_ws_ok(int64_t n, int64_t batch, const void* ws, size_t ws_bytes) {
+// n <= 64 building blocks run in one fused kernel without scratch (eval_degopt with k > 5
+// excepted); everything else takes the caller's workspace
+static bool block_ws_ok(int64_t n, int64_t batch, const void* ws, size_t ws_bytes, bool fused = true) {
+  if (n <= LGM_FUSED_MAX && fused) return true;
   size_t need = 0;
   lgm_block_workspace_bytes(n, batch, &need);
-  return need == 0 || (ws && ws_bytes >= need);
+  return ws && ws_bytes >= need;
 }
 
 const char* lgm_status_string(int code) {
@@ -382,17 +387,18 @@ int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_
 int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
                         int32_t* products, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(X, n, batch, ld) || !Z || !products || k < 1 || k > LGM_K_MAX) return LGM_ERR_ARG;
-  if (!block_ws_ok(n, batch, ws, ws_bytes)) return LGM_ERR_WORKSPACE;
+  const bool fused = n <= LGM_FUSED_MAX && k <= 5;  // node storage of the fused kernel: P4..P6
+  if (!block_ws_ok(n, batch, ws, ws_bytes, fused)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
-  if (n <= 32) {
+  if (fused && n <= 32) {
     if (prep<32>(degopt_kernel<32>, Cfg<32>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
     lgm_count_launch(), degopt_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
                                                                                                   k, products, P);
     return check_launch();
   }
-  if (n <= 64) {
+  if (fused) {
     if (prep<64>(degopt_kernel<64>, Cfg<64>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
     lgm_count_launch(), degopt_kernel<64><<<(unsigned)batch, Cfg<64>::NT, Cfg<64>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
                                                                                                   k, products, P);

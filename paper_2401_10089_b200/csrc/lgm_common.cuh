@@ -13,6 +13,7 @@ int lgm_count_launch();
 #define LGM_SCALING_SWITCH 1e-2                   // sqrtm.py:21
 #define LGM_MU_MIN 1e-8                           // sqrtm.py:24
 #define LGM_MU_MAX 1e8
+#define LGM_FUSED_WS 8                            // Engine F workspace: n^2 slots per matrix
 
 // Everything the driver needs besides the matrices; passed by value as a kernel parameter.
 struct LgmParams {

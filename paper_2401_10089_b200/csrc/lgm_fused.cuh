@@ -814,7 +814,9 @@ struct Ctx {
     }
     __device__ __forceinline__ int ld(int t) const { return t == 2 ? C::LDM : (t == 3 ? p3_ld : ext_ld); }
   };
-  static constexpr int TMAX = 7;  // nodes P2..P7
+  // nodes P2..P_{TM}: TM = 7 for the shipped schemes k <= 5, LGM_K_MAX + 2 for k = 6..9 (a
+  // separate instantiation so the k <= 5 path keeps its register allocation)
+  static constexpr int TM5 = 7, TM9 = LGM_K_MAX + 2;
 
   // Polynomial GEMMs on the FP64 tensor cores (mma.sync m8n8k4 -> DMMA): warp w owns output
   // rows 16w .. 16w+15 (two 8-row tiles) x all NMAX/8 column tiles, so every left-operand
@@ -830,6 +832,7 @@ struct Ctx {
   // acc = L * R with L = sum_{t=2..nn} crow[t-1] * P_t + crow[0] * I formed on the fly with
   // numpy's _combine rounding (schemes.py:91-101: sequential over t, zero coefficients
   // skipped, products and sums rounded separately).  R: swizzled (rswz) or row stride LDM.
+  template <int TMAX>
   __device__ void gemm_comb(const Nodes& nd, int nn, const double* crow, const double* R, bool rswz,
                             double (&acc)[NMAX / 2]) {
 #pragma unroll
@@ -869,6 +872,7 @@ struct Ctx {
   }
 
   // D (swizzled) = sum_{t=2..nn} crow[t-1] P_t + crow[0] I (schemes.py:91-101 order)
+  template <int TMAX>
   __device__ void combine_rhs(double* D, const Nodes& nd, int nn, const double* crow) {
     double cf[TMAX - 1];
 #pragma unroll
@@ -905,8 +909,10 @@ struct Ctx {
                                       int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
                                       int& products) {
     Ctx s = *this;
-    s.degopt_impl(k, bX, b3, have_fp, bR, ext, ext_ld, ext_stride, mult, unbal, Lg, ldg, products);
+    if (k <= 5) s.degopt_impl<TM5>(k, bX, b3, have_fp, bR, ext, ext_ld, ext_stride, mult, unbal, Lg, ldg, products);
+    else s.degopt_impl<TM9>(k, bX, b3, have_fp, bR, ext, ext_ld, ext_stride, mult, unbal, Lg, ldg, products);
   }
+  template <int TMAX>
   __device__ __forceinline__ void degopt_impl(int k, int bX, MRef b3, bool have_fp, int bR, double* ext, int ext_ld,
                                               int ext_stride, double mult, bool unbal, double* Lg, long long ldg,
                                               int& products) {
@@ -915,7 +921,7 @@ struct Ctx {
     double acc[NMAX / 2];
     if (!have_fp) {  // P3 = P2 * P2
       const double one[2] = {0.0, 1.0};
-      gemm_comb(nd, 2, one, buf(bX), false, acc);
+      gemm_comb<TMAX>(nd, 2, one, buf(bX), false, acc);
       products++;
       __syncthreads();
       store_frag(b3.p, b3.ld, acc);
@@ -924,9 +930,9 @@ struct Ctx {
     int nn = 3;  // nodes P1..P3 available
     bool last_in_regs = false;
     for (int j = 1; j < k; ++j) {
-      combine_rhs(R, nd, nn, lgm_rhs(*P, k, j));
+      combine_rhs<TMAX>(R, nd, nn, lgm_rhs(*P, k, j));
       __syncthreads();
-      gemm_comb(nd, nn, lgm_lhs(*P, k, j), R, true, acc);
+      gemm_comb<TMAX>(nd, nn, lgm_lhs(*P, k, j), R, true, acc);
       products++;
       nn++;
       __syncthreads();
@@ -1017,7 +1023,7 @@ struct Ctx {
   // ---- Algorithm 1 (oracle/driver.py logm_status) ----------------------------------------
   // bB: A - I (shared), bAI2: A_I2 (global workspace slot), nI2 = ||A_I2||_1 (cached per root)
   __device__ __noinline__ double alpha(MRef bB, bool have_ai2, MRef bAI2, double nA, double nI2, int m, double theta,
-                          double (&cache)[16], unsigned& cvalid, int& nest, int& passes) {
+                          double (&cache)[32], unsigned& cvalid, int& nest, int& passes) {
     const int itmax = P->est_itmax;
     double t1, Pm;
     if (have_ai2) {
@@ -1075,7 +1081,7 @@ struct Ctx {
   }
 
   // returns k; cert = alpha certifying k
-  __device__ __noinline__ int select(MRef bB, MRef bAI2, double nA, double nI2, double alpha_loop, double (&cache)[16],
+  __device__ __noinline__ int select(MRef bB, MRef bAI2, double nA, double nI2, double alpha_loop, double (&cache)[32],
                         unsigned& cvalid, int& nest, int& passes, double& cert) {
     const int K = P->max_k;
     const double* th = P->theta;
@@ -1092,7 +1098,7 @@ struct Ctx {
     } else {
       min_im = first_index(r2, K);
     }
-    const int tabmin[5] = {1, 2, 3, 4, 4};
+    const int tabmin[LGM_K_MAX] = LGM_TABMIN_IM;
     min_im = tabmin[min_im - 1];
     note(r2, th[0]);
     min_im = (r2 > th[0]) ? (min_im > 2 ? min_im : 2) : 1;
@@ -1151,12 +1157,12 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
   const double thK = P.theta[K - 1];
   const int mK = P.order[K - 1];
   const double tol = P.db_tol > 0.0 ? P.db_tol : 10.0 * n * LGM_UNIT_ROUNDOFF;
-  double cache[16];
+  double cache[32];  // estimates by power m (<= m_K + 1 = 29 with k = 9)
   unsigned cvalid = 0u;
   int nest = 0, passes = 0, s = 0, db_iters = 0, products = 0;
   bool have_ai2 = false;
   // A_prev / A_I2 in this matrix's workspace slot 3 (row stride n)
-  const typename Ctx<NMAX, FULL>::MRef AI2{ws + 3 * n * n, n};
+  const typename Ctx<NMAX, FULL>::MRef AI2{ws + (LGM_FUSED_WS - 1) * n * n, n};
   double nI2 = 0.0;
   double alpha_loop = c.onenorm(BUF_B, 1.0);
   bool finish = c.le(alpha_loop, thK);
@@ -1236,7 +1242,7 @@ __device__ void logm_one(Ctx<NMAX, FULL>& c, const double* Ag, double* Lg, long 
     typename Ctx<NMAX, FULL>::Nodes nd{c.buf(BUF_Y), c.buf(BUF_Y), Cfg<NMAX>::LDM, nullptr, 0, 0};  // P2 := A - I
     const double one[2] = {0.0, 1.0};
     double acc[NMAX / 2];
-    c.gemm_comb(nd, 2, one, c.buf(BUF_Y), false, acc);
+    c.template gemm_comb<Ctx<NMAX, FULL>::TM5>(nd, 2, one, c.buf(BUF_Y), false, acc);
     products++;
     c.store_frag(AI2.p, AI2.ld, acc);
     __syncthreads();

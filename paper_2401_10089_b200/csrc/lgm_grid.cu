@@ -32,8 +32,9 @@ constexpr int NB = 32;      // Gauss-Jordan panel width
 #ifndef G2_RT
 #define G2_RT 64            // rows per tile of the rank-64 combined pass (64: 4 warps; 128 measured equal)
 #endif
-constexpr int NBUF = 8;     // n x n slots per matrix
-enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7 };
+constexpr int NBUF = 12;    // n x n slots per matrix (P8..P11: schemes k = 6..9)
+static_assert(LGM_K_MAX <= 9, "node slots P2..P11 cover k <= 9");
+enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11 };
 
 #define CK(x)                                                                       \
   do {                                                                              \
@@ -2346,6 +2347,7 @@ enum {
 };
 
 // per-matrix Algorithm-1 state (oracle/driver.py _State + the running root / request)
+static_assert(2 * 14 + 2 <= 32, "estimate cache covers powers up to m_K + 1");
 struct MDev {
   int status, s, db_iters, nest, passes, products, k, plateau, sweeps;
   int finish, have_ai2, post_fail;
@@ -2356,7 +2358,7 @@ struct MDev {
   double dbmm;                      // running root's margin
   double th, t1, Pm, t2, aout;      // alpha request threshold and terms
   double alpha_loop, mm, nA, nI2, cert, cert_max;
-  double cache[20];
+  double cache[32];  // estimates by power m (<= m_K + 1 = 29 with k = 9)
   __device__ void note(double x, double thr) {
     const double d = fabs(thr);
     mm = fmin(mm, d > 0 ? fabs(x - thr) / d : fabs(x - thr));
@@ -2953,7 +2955,7 @@ __global__ void __launch_bounds__(CT) select_init_kernel(Ctl c, cudaGraphConditi
       } else {
         mi = first_index(M, r2, P);
       }
-      const int tabmin[LGM_K_MAX] = {1, 2, 3, 4, 4};
+      const int tabmin[LGM_K_MAX] = LGM_TABMIN_IM;
       mi = tabmin[mi - 1];
       M.note(r2, P.theta[0]);
       mi = (r2 > P.theta[0]) ? max(mi, 2) : 1;
@@ -3012,9 +3014,10 @@ __global__ void __launch_bounds__(CT) select_step_kernel(Ctl c, cudaGraphConditi
 }
 
 // ------------------------------------------------------------------ polynomial (schemes.py:91-126)
-// node slots: P2 = I - B (G_B), P3 = A_I2 (G_AP), P4.. (G_XI, G_YI, G_P6, G_P7); R temp G_Y,
+// node slots: P2 = I - B (G_B), P3 = A_I2 (G_AP), P4.. (G_XI, G_YI, G_P6 .. G_P11); R temp G_Y,
 // L temp G_AM.  Scheme k_b's coefficient rows come from the call's parameter block.
-__constant__ int c_node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+__constant__ int c_node_slot[12] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11};
+constexpr int h_node_slot[12] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11};
 
 __global__ void __launch_bounds__(CT) decide_poly_kernel(Ctl c) {
   __shared__ int s_w[33];
@@ -3225,6 +3228,7 @@ struct Cap {
   }
   cudaEvent_t evN, evP;
   int itmax;
+  int mk = 14;          // m_K: estimator thin products <= m_K + 1 (s = 0) / m_K / 2 + 1
   bool tma = false;     // rank-64 passes by gj_update2_tma_kernel (W stored transposed)
   CUtensorMap wmap;     // the W region as (12 batch n) rows x NB doubles, 64 x 16 boxes
 };
@@ -3597,7 +3601,7 @@ int cap_logm(Cap& C) {
   // then WHILE(some matrix still scaling) with s >= 1 (A_I2-based estimates: <= m_K/2 + 1)
   cudaGraphConditionalHandle hs;
   if (new_handle(st, &hs)) return LGM_ERR_CUDA;
-  const int mk = LGM_ORDER_DEFAULT[LGM_K_MAX - 1];
+  const int mk = C.mk;
   if (cap_scal_iter(C, 0, mk + 1, hs, false)) return LGM_ERR_CUDA;
   cudaGraph_t body;
   if (cap_while_after(st, hs, &body)) return LGM_ERR_CUDA;
@@ -3646,7 +3650,7 @@ int cap_logm(Cap& C) {
   if (cap_ew(C, st, LS_SEL, 4, G_B, G_B, G_B)) return LGM_ERR_CUDA;  // P2 = I - B
   CK(cudaMemsetAsync(C.c.flag, 0, C.batch * 4, st));
   const int tiles = (n + TM - 1) / TM;
-  const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+  const int* node_slot = h_node_slot;
   const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
   for (int j = 1; j < LGM_K_MAX; ++j) {
     const DList Lj = C.c.list(LS_POLY0 + j);
@@ -3710,7 +3714,7 @@ int cap_block(Cap& C, int prog, int has2, int p1) {
     GL decide_poly_kernel<<<1, CT, 0, st>>>(C.c);
     for (int j = 1; j < LGM_K_MAX; ++j) {
       const DList Lj = C.c.list(LS_POLY0 + j);
-      const int node_slot[8] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7};
+      const int* node_slot = h_node_slot;
       GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 1, G_Y);
       CombSpec ls{};
       GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 0, G_AM);
@@ -3730,9 +3734,10 @@ int cap_block(Cap& C, int prog, int has2, int p1) {
 struct GraphKey {
   int dev, prog, n, batch, itmax, has2, p1;
   const void* ws;
+  int mk;  // m_K of the call's max_k (bounds the estimator's thin-product count)
   bool operator==(const GraphKey& o) const {
     return dev == o.dev && prog == o.prog && n == o.n && batch == o.batch && itmax == o.itmax && has2 == o.has2 &&
-           p1 == o.p1 && ws == o.ws;
+           p1 == o.p1 && ws == o.ws && mk == o.mk;
   }
 };
 struct GraphEntry {
@@ -3800,6 +3805,7 @@ int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
   C.evN = cs.evN;
   C.evP = cs.evP;
   C.itmax = k.itmax;
+  C.mk = k.mk > 0 ? k.mk : LGM_ORDER_DEFAULT[LGM_K_DEFAULT - 1];
   C.tma = g2_tma_on() && k.n <= 512 && k.n % (2 * NB) == 0 && !use_g1(k.n);
   if (C.tma && make_wmap(C)) return LGM_ERR_CUDA;
   cudaGraph_t g;
@@ -3889,7 +3895,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n, int64_t batch, int64_t 
   d.L = L;
   d.ld = ld;
   d.rep = rep;
-  GraphKey k{0, PROG_LOGM, (int)n, (int)batch, P.est_itmax, 0, 0, nullptr};
+  GraphKey k{0, PROG_LOGM, (int)n, (int)batch, P.est_itmax, 0, 0, nullptr, P.order[P.max_k - 1]};
   return run_prog(k, ws, d, st);
 }
 
@@ -3904,7 +3910,7 @@ int lgm_grid_sqrt_db(const double* A, double* X, int64_t n, int64_t batch, int64
   d.iout2 = status;
   d.tol = tol;
   d.maxiter = maxiter;
-  GraphKey k{0, PROG_SQRTDB, (int)n, (int)batch, 0, 0, 0, nullptr};
+  GraphKey k{0, PROG_SQRTDB, (int)n, (int)batch, 0, 0, 0, nullptr, 0};
   return run_prog(k, ws, d, st);
 }
 
@@ -3919,7 +3925,7 @@ int lgm_grid_est(const double* M1, int p1, const double* M2, int64_t n, int64_t 
   d.zero_shortcut = zero_shortcut;
   d.dout = est;
   d.iout = passes;
-  GraphKey k{0, PROG_EST, (int)n, (int)batch, itmax, M2 ? 1 : 0, p1, nullptr};
+  GraphKey k{0, PROG_EST, (int)n, (int)batch, itmax, M2 ? 1 : 0, p1, nullptr, 0};
   return run_prog(k, ws, d, st);
 }
 
@@ -3933,7 +3939,7 @@ int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n, int64
   d.dout = scale;
   d.iout = sweeps;
   d.max_sweeps = max_sweeps;
-  GraphKey k{0, PROG_BALANCE, (int)n, (int)batch, 0, 0, 0, nullptr};
+  GraphKey k{0, PROG_BALANCE, (int)n, (int)batch, 0, 0, 0, nullptr, 0};
   return run_prog(k, ws, d, st);
 }
 
@@ -3946,7 +3952,7 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n, int
   d.ld = ld;
   d.kblk = k;
   d.iout = products;
-  GraphKey key{0, PROG_DEGOPT, (int)n, (int)batch, 0, FP ? 1 : 0, 0, nullptr};
+  GraphKey key{0, PROG_DEGOPT, (int)n, (int)batch, 0, FP ? 1 : 0, 0, nullptr, 0};
   return run_prog(key, ws, d, st);
 }
 

@@ -88,9 +88,10 @@ def _oracle_init(threads):
         sys.path.insert(0, root)
 
 
-def _oracle_one(A):
+def _oracle_one(A, max_k=None):
     from oracle import driver as D
-    L, rep = D.logm_status(A, D.default_prims())
+    kw = {} if max_k is None else {"max_k": max_k}
+    L, rep = D.logm_status(A, D.default_prims(), **kw)
     rep = {k: v for k, v in rep.items() if k != "message"}
     return L, rep
 
@@ -98,20 +99,20 @@ def _oracle_one(A):
 def _oracle_check_one(args):
     """Worker: oracle on one matrix, then the accuracy check against the GPU result (so the
     n x n L never travels back to the parent)."""
-    A, Lg, grec = args
-    Lr, rr = _oracle_one(A)
+    A, Lg, max_k = args
+    Lr, rr = _oracle_one(A, max_k)
     err = tol = None
     if Lr is not None and Lg is not None:
         err, tol = rel_err(Lg, Lr), tolerance(A, Lr)
     return rr, err, tol
 
 
-def oracle_reports(As, Ls, reps, procs=None):
+def oracle_reports(As, Ls, reps, procs=None, max_k=None):
     """Run the oracle on every matrix of As (process pool, one BLAS thread per worker; a
     single matrix runs in-process with all-core BLAS) and return, per matrix, (oracle report,
     rel error of the GPU L, tolerance)."""
     B = As.shape[0]
-    items = [(As[b], None if Ls is None else np.asarray(Ls[b]), None) for b in range(B)]
+    items = [(As[b], None if Ls is None else np.asarray(Ls[b]), max_k) for b in range(B)]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     procs = procs or min(cores, B)
     if B == 1 or procs == 1:
@@ -121,13 +122,13 @@ def oracle_reports(As, Ls, reps, procs=None):
         return pool.map(_oracle_check_one, items, chunksize=max(1, B // (4 * procs)))
 
 
-def check_batch(As, L, reps, allow_mismatch=0, procs=None, verbose=True, allow_stall=0):
+def check_batch(As, L, reps, allow_mismatch=0, procs=None, verbose=True, allow_stall=0, max_k=None):
     """Compare GPU (L, reports) with the oracle per matrix.  match / db_plateau records with
     status OK on both sides must meet the L tolerance; mismatches are counted (<= allowed).
     An exempt record with equal (status, s, k) is held to the L tolerance as well."""
     counts = {"match": 0, "exempt": 0, "db_plateau": 0, "db_stall": 0, "mismatch": 0}
     worst = 0.0
-    res = oracle_reports(As, L, reps, procs)
+    res = oracle_reports(As, L, reps, procs, max_k)
     for b, (rr, err, tol) in enumerate(res):
         cls, g, o = classify(reps[b], rr)
         counts[cls] += 1

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2401_10089_b200 import _lib
+from paper_2401_10089_b200 import constants as C
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -29,14 +30,14 @@ def test_default_opts_and_workspace():
     lib = _lib.load()
     o = _lib.Opts()
     lib.lgm_default_opts(ctypes.byref(o))
-    assert (o.max_k, o.maxiter_s, o.db_maxiter, o.est_itmax, o.balance) == (5, 40, 50, 5, 1)
+    assert (o.max_k, o.maxiter_s, o.db_maxiter, o.est_itmax, o.balance) == (C.K_DEFAULT, 40, 50, 5, 1)
     assert o.db_tol == 0.0 and not o.theta
     ws = ctypes.c_size_t(123)
-    # fused engine: 3 n^2 doubles per matrix (polynomial nodes P4..P6 in L2)
-    assert lib.lgm_workspace_bytes(32, 4096, ctypes.byref(ws)) == 0 and ws.value == 4096 * 4 * 32 * 32 * 8
-    assert lib.lgm_workspace_bytes(512, 2, ctypes.byref(ws)) == 0 and ws.value >= 2 * 8 * 512 * 512 * 8
+    # fused engine: 8 n^2 doubles per matrix (polynomial nodes P4..P10 and A_I2)
+    assert lib.lgm_workspace_bytes(32, 4096, ctypes.byref(ws)) == 0 and ws.value == 4096 * 8 * 32 * 32 * 8
+    assert lib.lgm_workspace_bytes(512, 2, ctypes.byref(ws)) == 0 and ws.value >= 2 * 12 * 512 * 512 * 8
     assert lib.lgm_launch_count() >= 0
-    assert lib.lgm_block_workspace_bytes(32, 8, ctypes.byref(ws)) == 0 and ws.value == 0
+    assert lib.lgm_block_workspace_bytes(32, 8, ctypes.byref(ws)) == 0 and ws.value > 0
     assert lib.lgm_block_workspace_bytes(100, 8, ctypes.byref(ws)) == 0 and ws.value >= 8 * 8 * 100 * 100 * 8
     assert lib.lgm_workspace_bytes(0, 1, ctypes.byref(ws)) == _lib.ERR_ARG
     assert lib.lgm_max_fused_n() == 64

@@ -28,7 +28,7 @@ def test_c_opts_mapping():
     assert [o.theta[i] for i in range(C.K_MAX)] == list(C.THETA)
     th = (1e-9, 1e-5, 1e-3, 0.05, 0.2)
     o, keep = driver._c_opts(driver.LogmOptions(theta_table=th))
-    assert [o.theta[i] for i in range(C.K_MAX)] == list(th)
+    assert [o.theta[i] for i in range(C.K_MAX)] == list(th) + list(C.THETA[len(th):])
 
 
 def test_report_decoding_and_exception_mapping():
@@ -61,7 +61,7 @@ def test_host_chunking():
 def test_workspace_sizes_through_the_abi():
     lib = _lib.load()
     ws = ctypes.c_size_t(0)
-    assert lib.lgm_workspace_bytes(32, 10, ctypes.byref(ws)) == 0 and ws.value == 10 * 4 * 32 * 32 * 8
+    assert lib.lgm_workspace_bytes(32, 10, ctypes.byref(ws)) == 0 and ws.value == 10 * 8 * 32 * 32 * 8
     assert lib.lgm_workspace_bytes(64, 0, ctypes.byref(ws)) == 0 and ws.value == 0
     small, big = ctypes.c_size_t(0), ctypes.c_size_t(0)
     assert lib.lgm_workspace_bytes(100, 16384, ctypes.byref(small)) == 0

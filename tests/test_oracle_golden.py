@@ -105,7 +105,10 @@ def test_theta_frozen_from_shipped_coefficients():
     table2 = (1.83e-8, 1.53e-4, 1.33e-2, 9.31e-2, 0.246)
     for t, p in zip(C.THETA, table2):
         assert abs(t - p) / p < 0.02
-    assert C.ORDER == (2, 4, 8, 14, 14)
+    assert C.ORDER[:5] == (2, 4, 8, 14, 14) and C.K_DEFAULT == 5
+    # k = 6..9 (generated, opt-in): Theta grows with k and every order is even (Algorithm 1's
+    # alpha / max_in formulas)
+    assert all(a < b for a, b in zip(C.THETA, C.THETA[1:])) and all(m % 2 == 0 for m in C.ORDER)
 
 
 def test_spec_onenorm_and_det():
