@@ -32,9 +32,9 @@ constexpr int NB = 32;      // Gauss-Jordan panel width
 #ifndef G2_RT
 #define G2_RT 64            // rows per tile of the rank-64 combined pass (64: 4 warps; 128 measured equal)
 #endif
-constexpr int NBUF = 12;    // n x n slots per matrix (P8..P11: schemes k = 6..9)
+constexpr int NBUF = 14;    // n x n slots per matrix (P8..P11: schemes k = 6..9; Q0/Q1: operand ping-pong)
 static_assert(LGM_K_MAX <= 9, "node slots P2..P11 cover k <= 9");
-enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11 };
+enum { G_B = 0, G_Y, G_XI, G_YI, G_AP, G_AM, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11, G_Q0, G_Q1 };
 
 #define CK(x)                                                                       \
   do {                                                                              \
@@ -3033,44 +3033,240 @@ __global__ void __launch_bounds__(CT) decide_poly_kernel(Ctl c) {
   }
 }
 
-// dst = sum_t c_t P_t + c0 I over the matrices of list `lst`, row `j` of side (0 lhs, 1 rhs)
-// of each matrix's own scheme (numpy _combine rounding: separate multiply and add)
-__global__ void poly_combine_kernel(Slots S, DList L, const CallDesc* d, const MDev* ms, int j, int side, int dk) {
-  const int n = S.n;
-  const LgmParams& P = d->P;
+// ---- fused polynomial chain (schemes.py:104-126 + PAPER.md:746-747) ---------------------
+// The combinations of the graph live in the producing kernels' epilogues: poly_start forms
+// P2 (= I - B for logm) and the first operand pair (L1, R1) elementwise; GEMM j multiplies
+// the pair (L_j, R_j) and its epilogue either stores P_{j+3} and forms the next pair
+// (L_{j+1}, R_{j+1}) from the nodes -- P_{j+3} straight from the accumulators -- or, for the
+// matrix's last product, forms z = sum out_t P_t + out_0 I, L = -2^s z, unbalanced, and
+// writes the output.  Operand pairs alternate between (G_AM, G_Y) and (G_Q0, G_Q1) so that
+// the epilogue never overwrites an operand other CTAs of the same GEMM still read.  Every
+// combination is numpy's _combine rounding (sequential over the nodes, zero coefficients
+// skipped, separate multiply / add, the identity term last).
+__device__ __forceinline__ int pair_l(int j) { return (j & 1) ? G_Q0 : G_AM; }
+__device__ __forceinline__ int pair_r(int j) { return (j & 1) ? G_Q1 : G_Y; }
+
+struct PolyArgs {
+  Slots S;
+  const CallDesc* d;
+  const MDev* ms;
+  const double* scale;
+  int* nonfinite;
+  int logm;  // 1: P2 = I - B, L = -2^s z unbalanced; 0 (eval_degopt block): P2 = X, L = z
+};
+
+// the value at (i, c) of sum_{t=2..nn} row[t-1] P_t + row[0] I, P_pn (if pn > 0) given
+__device__ __forceinline__ double comb_at(const Slots& S, int b, const double* row, int nn, size_t idx, bool diag,
+                                          int pn, double pv) {
+  double v = 0.0;
+  for (int t = 2; t <= nn; ++t)
+    if (row[t - 1] != 0.0) v = __dadd_rn(v, __dmul_rn(row[t - 1], t == pn ? pv : S.buf(b, c_node_slot[t])[idx]));
+  if (diag && row[0] != 0.0) v = __dadd_rn(v, row[0]);
+  return v;
+}
+
+__device__ __forceinline__ void poly_out(const PolyArgs& a, int b, int k, int i, int c, size_t idx, int pn, double pv) {
+  const int n = a.S.n;
+  const LgmParams& P = a.d->P;
+  double v = comb_at(a.S, b, lgm_out(P, k), k + 2, idx, i == c, pn, pv);
+  if (a.logm) {
+    v = -ldexp(1.0, a.ms[b].s) * v;
+    if (P.balance) v = v * (a.scale[(size_t)b * n + i] / a.scale[(size_t)b * n + c]);
+  }
+  a.d->L[(size_t)b * n * a.d->ld + (size_t)i * a.d->ld + c] = v;
+  if (a.nonfinite && !isfinite(v)) a.nonfinite[b] = 1;
+}
+
+// P2 (logm: I - B in place), then L1 / R1 into pair 1 -- or, for k = 1, the output
+__global__ void poly_start_kernel(PolyArgs a, DList L) {
+  const int n = a.S.n;
+  const LgmParams& P = a.d->P;
   LIST_LOOP(L, (size_t)n * n)
-    const int k = ms[b].k;
-    const double* row = side ? lgm_rhs(P, k, j) : lgm_lhs(P, k, j);
-    const int i = idx / n, jj = idx - (size_t)i * n;
-    double v = 0.0;
-    for (int t = 2; t <= j + 2; ++t)
-      if (row[t - 1] != 0.0) v = __dadd_rn(v, __dmul_rn(row[t - 1], S.buf(b, c_node_slot[t])[idx]));
-    if (i == jj && row[0] != 0.0) v = __dadd_rn(v, row[0]);
-    S.buf(b, dk)[idx] = v;
+    const int k = a.ms[b].k;
+    const int i = idx / n, c = idx - (size_t)i * n;
+    double* P2 = a.S.buf(b, G_B);
+    double p2 = P2[idx];
+    if (a.logm) {
+      p2 = (i == c) ? 1.0 - p2 : -p2;
+      P2[idx] = p2;
+    }
+    if (k == 1) {
+      poly_out(a, b, k, i, c, idx, 2, p2);
+    } else {
+      a.S.buf(b, pair_l(1))[idx] = comb_at(a.S, b, lgm_lhs(P, k, 1), 3, idx, i == c, 2, p2);
+      a.S.buf(b, pair_r(1))[idx] = comb_at(a.S, b, lgm_rhs(P, k, 1), 3, idx, i == c, 2, p2);
+    }
   }
 }
 
-// L = -2^s z (scale_i / scale_j) with z = out row of scheme k_b over P1..P_{k+2}
-__global__ void poly_final_kernel(Slots S, DList L, const CallDesc* d, const MDev* ms, const double* scale, int* nonfinite,
-                                  int unit_mult) {
+// GEMM j: P_{j+3} = L_j R_j (64 x 64 tiles, K in chunks of 32 staged by a two-stage cp.async
+// pipeline, DMMA core; scalar loads for odd n), fused epilogue as above
+template <bool EVEN>
+__global__ void __launch_bounds__(128) poly_gemm_kernel(PolyArgs a, DList L, int j) {
+  extern __shared__ __align__(16) double gsm[];
+  if (blockIdx.z >= *L.cnt) return;
+  const int b = L.ids[blockIdx.z];
+  const Slots& S = a.S;
   const int n = S.n;
-  const LgmParams& P = d->P;
-  double* Lout = d->L;
-  const long long ld = d->ld;
-  LIST_LOOP(L, (size_t)n * n)
-    const int k = ms[b].k;
-    const double* row = lgm_out(P, k);
-    const int i = idx / n, j = idx - (size_t)i * n;
-    double v = 0.0;
-    for (int t = 2; t <= k + 2; ++t)
-      if (row[t - 1] != 0.0) v = __dadd_rn(v, __dmul_rn(row[t - 1], S.buf(b, c_node_slot[t])[idx]));
-    if (i == j && row[0] != 0.0) v = __dadd_rn(v, row[0]);
-    if (!unit_mult) {
-      v = -ldexp(1.0, ms[b].s) * v;
-      if (P.balance) v = v * (scale[(size_t)b * n + i] / scale[(size_t)b * n + j]);
+  const int col0 = blockIdx.x * TN, row0 = blockIdx.y * TM;
+  const double* A = S.buf(b, pair_l(j));
+  const double* Bm = S.buf(b, pair_r(j));
+  const int tid = threadIdx.x;
+  auto ld2 = [&](double* dst, const double* src, bool ok2, bool ok1) {
+    if (EVEN && ok2) cp_async16(dst, src);
+    else { dst[0] = ok1 ? src[0] : 0.0; dst[1] = ok2 ? src[1] : 0.0; }
+  };
+  auto stage = [&](int k0, int buf) {
+    double* As = gsm + buf * (GP_A + GP_B);
+    double* Bs = As + GP_A;
+    for (int c = tid; c < 64 * 16; c += 128) {
+      const int r = c >> 4, q = (c & 15) * 2;
+      const int i = row0 + r, kk = k0 + q;
+      ld2(&As[r * LDA_S + q], &A[(size_t)i * n + kk], i < n && kk + 1 < n, i < n && kk < n);
     }
-    Lout[(size_t)b * n * ld + (size_t)i * ld + j] = v;
-    if (nonfinite && !isfinite(v)) nonfinite[b] = 1;
+    for (int c = tid; c < 32 * 32; c += 128) {
+      const int r = c >> 5, q = (c & 31) * 2;
+      const int kk = k0 + r, jc = col0 + q;
+      ld2(&Bs[r * LDB_S + q], &Bm[(size_t)kk * n + jc], kk < n && jc + 1 < n, kk < n && jc < n);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const int nk = (n + TK - 1) / TK;
+  stage(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      stage((kc + 1) * TK, (kc + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* As = gsm + (kc & 1) * (GP_A + GP_B);
+    tile_mma(As, As + GP_A, acc);
+    __syncthreads();
+  }
+  const int k = a.ms[b].k;
+  const LgmParams& P = a.d->P;
+  const int pn = j + 3;                 // this product is node P_{j+3}
+  const bool last = (j == k - 1);
+  const double* lrow = last ? nullptr : lgm_lhs(P, k, j + 1);
+  const double* rrow = last ? nullptr : lgm_rhs(P, k, j + 1);
+  double* Pn = S.buf(b, c_node_slot[pn]);
+  double* Ln = S.buf(b, pair_l(j + 1));
+  double* Rn = S.buf(b, pair_r(j + 1));
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
+  if (last) {  // z over P2..P_{k+2} (P_{k+2} from the accumulators), -2^s, unbalance, output
+    const double* orow = lgm_out(P, k);
+    double co[LGM_K_MAX + 2];
+#pragma unroll
+    for (int q = 0; q < LGM_K_MAX + 2; ++q) co[q] = (q + 2 <= pn) ? orow[q + 1] : 0.0;
+    const double mult = -ldexp(1.0, a.ms[b].s);
+    const bool unbal = a.logm && P.balance;
+    double* Lout = a.d->L;
+    const long long ldo = a.d->ld;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const int i = r0 + mi * 8 + g;
+      if (i >= n) continue;
+      const double si = unbal ? a.scale[(size_t)b * n + i] : 1.0;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int c = c0 + ni * 8 + 2 * t;
+        if (c >= n) continue;
+        const bool two = EVEN || c + 1 < n;
+        const size_t idx = (size_t)i * n + c;
+        double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+        for (int tt = 2; tt < LGM_K_MAX + 4 && tt < pn; ++tt) {
+          if (co[tt - 2] == 0.0) continue;
+          const double* src = S.buf(b, c_node_slot[tt]) + idx;
+          double v0, v1 = 0.0;
+          if (EVEN) {
+            const double2 v = *reinterpret_cast<const double2*>(src);
+            v0 = v.x;
+            v1 = v.y;
+          } else {
+            v0 = src[0];
+            if (two) v1 = src[1];
+          }
+          z0 = __dadd_rn(z0, __dmul_rn(co[tt - 2], v0));
+          z1 = __dadd_rn(z1, __dmul_rn(co[tt - 2], v1));
+        }
+        const double cp = co[pn - 2];
+        if (cp != 0.0) { z0 = __dadd_rn(z0, __dmul_rn(cp, acc[mi][ni][0])); z1 = __dadd_rn(z1, __dmul_rn(cp, acc[mi][ni][1])); }
+        if (orow[0] != 0.0) { if (i == c) z0 = __dadd_rn(z0, orow[0]); if (i == c + 1) z1 = __dadd_rn(z1, orow[0]); }
+        double zz[2] = {z0, z1};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (e == 1 && !two) break;
+          double v = zz[e];
+          if (a.logm) {
+            v = mult * v;
+            if (unbal) v = v * (si / a.scale[(size_t)b * n + c + e]);
+          }
+          Lout[(size_t)b * n * ldo + (size_t)i * ldo + c + e] = v;
+          if (a.nonfinite && !isfinite(v)) a.nonfinite[b] = 1;
+        }
+      }
+    }
+    return;
+  }
+  // P_{j+3} and the next operand pair in one pass over the nodes (each node element read
+  // once for both combinations; per element the _combine order over t is unchanged)
+  double cl[LGM_K_MAX + 2], cr[LGM_K_MAX + 2];
+#pragma unroll
+  for (int q = 0; q < LGM_K_MAX + 2; ++q) {
+    cl[q] = (q + 2 <= pn) ? lrow[q + 1] : 0.0;
+    cr[q] = (q + 2 <= pn) ? rrow[q + 1] : 0.0;
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+    if (i >= n) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int c = c0 + ni * 8 + 2 * t;
+      if (c >= n) continue;
+      const bool two = EVEN || c + 1 < n;  // (EVEN: c even, c + 1 < n)
+      const size_t idx = (size_t)i * n + c;
+      double l0 = 0.0, l1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+      for (int tt = 2; tt < LGM_K_MAX + 4 && tt < pn; ++tt) {
+        if (cl[tt - 2] == 0.0 && cr[tt - 2] == 0.0) continue;
+        const double* src = S.buf(b, c_node_slot[tt]) + idx;
+        double v0, v1 = 0.0;
+        if (EVEN) {
+          const double2 v = *reinterpret_cast<const double2*>(src);
+          v0 = v.x;
+          v1 = v.y;
+        } else {
+          v0 = src[0];
+          if (two) v1 = src[1];
+        }
+        if (cl[tt - 2] != 0.0) { l0 = __dadd_rn(l0, __dmul_rn(cl[tt - 2], v0)); l1 = __dadd_rn(l1, __dmul_rn(cl[tt - 2], v1)); }
+        if (cr[tt - 2] != 0.0) { q0 = __dadd_rn(q0, __dmul_rn(cr[tt - 2], v0)); q1 = __dadd_rn(q1, __dmul_rn(cr[tt - 2], v1)); }
+      }
+      const double p0 = acc[mi][ni][0], p1 = acc[mi][ni][1];
+      const double clp = cl[pn - 2], crp = cr[pn - 2];
+      if (clp != 0.0) { l0 = __dadd_rn(l0, __dmul_rn(clp, p0)); l1 = __dadd_rn(l1, __dmul_rn(clp, p1)); }
+      if (crp != 0.0) { q0 = __dadd_rn(q0, __dmul_rn(crp, p0)); q1 = __dadd_rn(q1, __dmul_rn(crp, p1)); }
+      if (lrow[0] != 0.0) { if (i == c) l0 = __dadd_rn(l0, lrow[0]); if (i == c + 1) l1 = __dadd_rn(l1, lrow[0]); }
+      if (rrow[0] != 0.0) { if (i == c) q0 = __dadd_rn(q0, rrow[0]); if (i == c + 1) q1 = __dadd_rn(q1, rrow[0]); }
+      if (EVEN) {
+        *reinterpret_cast<double2*>(Pn + idx) = make_double2(p0, p1);
+        *reinterpret_cast<double2*>(Ln + idx) = make_double2(l0, l1);
+        *reinterpret_cast<double2*>(Rn + idx) = make_double2(q0, q1);
+      } else {
+        Pn[idx] = p0; Ln[idx] = l0; Rn[idx] = q0;
+        if (two) { Pn[idx + 1] = p1; Ln[idx + 1] = l1; Rn[idx + 1] = q1; }
+      }
+    }
   }
 }
 
@@ -3584,6 +3780,26 @@ int cap_load(Cap& C, cudaStream_t st, const double* const* src, int slot) {
   return 0;
 }
 
+// the fused polynomial chain over LS_SEL (lists LS_POLY0 + j built by decide_poly_kernel)
+int cap_poly(Cap& C, cudaStream_t st, bool logm) {
+  const int n = C.n;
+  PolyArgs a;
+  a.S = C.c.S;
+  a.d = C.c.desc;
+  a.ms = C.c.ms;
+  a.scale = C.c.scale;
+  a.nonfinite = logm ? C.c.flag : nullptr;
+  a.logm = logm ? 1 : 0;
+  GL poly_start_kernel<<<ew_blocks(), 256, 0, st>>>(a, C.c.list(LS_SEL));
+  const int tiles = (n + TM - 1) / TM;
+  const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
+  for (int j = 1; j < LGM_K_MAX; ++j) {
+    if ((n & 1) == 0) GL poly_gemm_kernel<true><<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(a, C.c.list(LS_POLY0 + j), j);
+    else GL poly_gemm_kernel<false><<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(a, C.c.list(LS_POLY0 + j), j);
+  }
+  return 0;
+}
+
 int cap_logm(Cap& C) {
   cudaStream_t st = C.s[0];
   const int n = C.n;
@@ -3645,28 +3861,10 @@ int cap_logm(Cap& C) {
     CK(cudaStreamEndCapture(C.s[1], &tmp));
   }
   t_cap_nodes = saved;
-  // polynomial
+  // polynomial: one fused kernel per product (cap_poly)
   GL decide_poly_kernel<<<1, CT, 0, st>>>(C.c);
-  if (cap_ew(C, st, LS_SEL, 4, G_B, G_B, G_B)) return LGM_ERR_CUDA;  // P2 = I - B
   CK(cudaMemsetAsync(C.c.flag, 0, C.batch * 4, st));
-  const int tiles = (n + TM - 1) / TM;
-  const int* node_slot = h_node_slot;
-  const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
-  for (int j = 1; j < LGM_K_MAX; ++j) {
-    const DList Lj = C.c.list(LS_POLY0 + j);
-    GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 1, G_Y);
-    GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 0, G_AM);
-    if ((n & 1) == 0) {
-      GL gemm_plain_kernel<<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(C.c.S, Lj, G_AM, G_Y, node_slot[j + 3]);
-    } else {
-      CombSpec cs{};
-      cs.nterm = 1;
-      cs.node[0] = G_AM;
-      cs.coef[0] = 1.0;
-      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, Lj, cs, G_Y, node_slot[j + 3]);
-    }
-  }
-  GL poly_final_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_SEL), C.c.desc, C.c.ms, C.c.scale, C.c.flag, 0);
+  if (cap_poly(C, st, true)) return LGM_ERR_CUDA;
   GL decide_final_kernel<<<1, CT, 0, st>>>(C.c);
   GL nan_fill_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_FAILED), C.c.desc);
   GL report_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, t_cap_nodes + 1);
@@ -3712,18 +3910,7 @@ int cap_block(Cap& C, int prog, int has2, int p1) {
       GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, C.c.list(LS_ALL), cs, G_B, G_AP);
     }
     GL decide_poly_kernel<<<1, CT, 0, st>>>(C.c);
-    for (int j = 1; j < LGM_K_MAX; ++j) {
-      const DList Lj = C.c.list(LS_POLY0 + j);
-      const int* node_slot = h_node_slot;
-      GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 1, G_Y);
-      CombSpec ls{};
-      GL poly_combine_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, Lj, C.c.desc, C.c.ms, j, 0, G_AM);
-      ls.nterm = 1;
-      ls.node[0] = G_AM;
-      ls.coef[0] = 1.0;
-      GL gemm_comb_kernel<<<dim3(tiles, tiles, C.batch), 128, 0, st>>>(C.c.S, Lj, ls, G_Y, node_slot[j + 3]);
-    }
-    GL poly_final_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_SEL), C.c.desc, C.c.ms, C.c.scale, nullptr, 1);
+    if (cap_poly(C, st, false)) return LGM_ERR_CUDA;
     GL decide_final_kernel<<<1, CT, 0, st>>>(C.c);
     GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 3, t_cap_nodes + 1);
   }
@@ -3777,6 +3964,8 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
   CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(poly_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(poly_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(gj_update2_tma_kernel, mx, (int)ut_smem()));
   CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
   return 0;
