@@ -133,6 +133,12 @@ int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z,
                         int64_t batch, int64_t ld, int32_t k, int32_t* products_dev,
                         void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
+/* E = expm(A) by the reference's test-oracle recipe (matcore.py:318-336 expm_ref): scale to
+ * ||A||_1 <= 1/2, degree-20 Taylor in Horner form, square back.  Validation helper (round
+ * trips of logm results on the device); workspace from lgm_block_workspace_bytes. */
+int lgm_expm_ref_f64(const double* A, double* E, int64_t n, int64_t batch, int64_t ld,
+                     void* workspace, size_t workspace_bytes, lgm_stream_t stream);
+
 const char* lgm_status_string(int code);
 
 /* Number of CUDA kernels this library has launched so far (process-wide, monotonic):

@@ -250,6 +250,20 @@ static bool block_ws_ok(int64_t n, int64_t batch, const void* ws, size_t ws_byte
   return ws && ws_bytes >= need;
 }
 
+int lgm_expm_ref_f64(const double* A, double* E, int64_t n, int64_t batch, int64_t ld, void* ws, size_t ws_bytes,
+                     lgm_stream_t stream) {
+  if (!args_ok(A, n, batch, ld) || !E || (const void*)E == (const void*)A) return LGM_ERR_ARG;
+  if (batch == 0) return 0;
+  if (!block_ws_ok(n, batch, ws, ws_bytes, false)) return LGM_ERR_WORKSPACE;
+  note_grid_device();
+  for (int64_t b0 = 0, ch = grid_chunk(); b0 < batch; b0 += ch) {
+    const int64_t cnt = batch - b0 < ch ? batch - b0 : ch;
+    const int rc = lgm_grid_expm(A + b0 * n * ld, E + b0 * n * ld, n, cnt, ld, ws, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 const char* lgm_status_string(int code) {
   switch (code) {
     case LGM_OK: return "ok";

@@ -3270,6 +3270,122 @@ __global__ void __launch_bounds__(128) poly_gemm_kernel(PolyArgs a, DList L, int
   }
 }
 
+// ---- reference exponential (validation helper; matcore.py:318-336 expm_ref) --------------
+// s = 0 if ||A||_1 <= 1/2 else ceil(log2(||A||_1 / (1/2))) (exact, from the binary exponent),
+// X = A / 2^s (exact), T = I + X T / j for j = 20..1, then s squarings.
+__global__ void __launch_bounds__(CT) expm_prep_kernel(Ctl c) {
+  for (int b = threadIdx.x; b < c.batch; b += CT) {
+    const double x = c.nrm[b] / 0.5;
+    int e = 0;
+    const double m = frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
+    int s = 0;
+    if (c.nrm[b] > 0.5) s = (m == 0.5) ? e - 1 : e;
+    if (s < 0) s = 0;
+    c.ms[b].s = s;
+    c.ms[b].dbit = 0;  // squarings done
+    c.scale[b] = ldexp(1.0, -s);
+  }
+}
+__global__ void expm_scale_kernel(Slots S, DList L, const double* f) {
+  const int n = S.n;
+  LIST_LOOP(L, (size_t)n * n)
+    S.buf(b, G_B)[idx] = S.buf(b, G_B)[idx] * f[b];
+  }
+}
+// mode 0: C = I + (X T) / j (Horner step); mode 1: C = T T (squaring)
+template <bool EVEN>
+__global__ void __launch_bounds__(128) expm_gemm_kernel(Slots S, DList L, int as, int bs, int cs, int j, int mode) {
+  extern __shared__ __align__(16) double gsm[];
+  if (blockIdx.z >= *L.cnt) return;
+  const int b = L.ids[blockIdx.z];
+  const int n = S.n;
+  const int col0 = blockIdx.x * TN, row0 = blockIdx.y * TM;
+  const double* A = S.buf(b, as);
+  const double* Bm = S.buf(b, bs);
+  double* Cm = S.buf(b, cs);
+  const int tid = threadIdx.x;
+  auto ld2 = [&](double* dst, const double* src, bool ok2, bool ok1) {
+    if (EVEN && ok2) cp_async16(dst, src);
+    else { dst[0] = ok1 ? src[0] : 0.0; dst[1] = ok2 ? src[1] : 0.0; }
+  };
+  auto stage = [&](int k0, int buf) {
+    double* As = gsm + buf * (GP_A + GP_B);
+    double* Bs = As + GP_A;
+    for (int c = tid; c < 64 * 16; c += 128) {
+      const int r = c >> 4, q = (c & 15) * 2;
+      const int i = row0 + r, kk = k0 + q;
+      ld2(&As[r * LDA_S + q], &A[(size_t)i * n + kk], i < n && kk + 1 < n, i < n && kk < n);
+    }
+    for (int c = tid; c < 32 * 32; c += 128) {
+      const int r = c >> 5, q = (c & 31) * 2;
+      const int kk = k0 + r, jc = col0 + q;
+      ld2(&Bs[r * LDB_S + q], &Bm[(size_t)kk * n + jc], kk < n && jc + 1 < n, kk < n && jc < n);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[4][4][2] = {};
+  const int nk = (n + TK - 1) / TK;
+  stage(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      stage((kc + 1) * TK, (kc + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* As = gsm + (kc & 1) * (GP_A + GP_B);
+    tile_mma(As, As + GP_A, acc);
+    __syncthreads();
+  }
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+    if (i >= n) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + ni * 8 + 2 * t + e;
+        if (c >= n) continue;
+        double v = acc[mi][ni][e];
+        if (mode == 0) {
+          v = v / (double)j;
+          v = (i == c) ? 1.0 + v : 0.0 + v;
+        }
+        Cm[(size_t)i * n + c] = v;
+      }
+  }
+}
+// squaring sweep: matrices with squarings left; sets the graph's WHILE condition when h != 0
+__global__ void __launch_bounds__(CT) expm_sq_decide_kernel(Ctl c, cudaGraphConditionalHandle h, int set, int nodes) {
+  __shared__ int s_w[33];
+  int off = 0;
+  FOR_LIST(c, LS_ALL)
+    const bool more = b >= 0 && c.ms[b].dbit < c.ms[b].s;
+    if (more) c.ms[b].dbit++;
+    const int pos = blk_append(more, s_w, off);
+    if (more) c.ids(LS_CUR)[pos] = b;
+  }
+  if (threadIdx.x == 0) {
+    c.cnt[LS_CUR] = off;
+    if (set) cudaGraphSetConditional(h, off > 0 ? 1u : 0u);
+  }
+  if (nodes) count_nodes(nodes);
+}
+// E: the result sits in slot G_Y after an even number of squarings, G_XI after an odd one
+__global__ void expm_store_kernel(Slots S, DList L, const CallDesc* d, const MDev* ms) {
+  const int n = S.n;
+  double* out = d->L;
+  const long long ld = d->ld;
+  LIST_LOOP(L, (size_t)n * n)
+    const int i = idx / n, j = idx - (size_t)i * n;
+    out[(size_t)b * n * ld + (size_t)i * ld + j] = S.buf(b, (ms[b].s & 1) ? G_XI : G_Y)[idx];
+  }
+}
+
 // products of the polynomial, non-finite results (estimator overflow upstream), failures
 __global__ void __launch_bounds__(CT) decide_final_kernel(Ctl c) {
   __shared__ int s_w[33];
@@ -3356,7 +3472,7 @@ __global__ void block_out_kernel(Ctl c, int kind, int nodes) {
     } else if (kind == 2) {  // balance: sweeps, scales
       D.iout[b] = c.sweeps[b];
       for (int i = 0; i < c.n; ++i) D.dout[(size_t)b * c.n + i] = c.scale[(size_t)b * c.n + i];
-    } else {                 // degopt: products
+    } else if (kind == 3) {  // degopt: products
       D.iout[b] = M.products;
     }
   }
@@ -3771,7 +3887,7 @@ int cap_scal_iter(Cap& C, int depth, int maxq, cudaGraphConditionalHandle h, boo
 }
 
 // ------------------------------------------------------------------ whole programs
-enum { PROG_LOGM = 0, PROG_SQRTDB, PROG_EST, PROG_BALANCE, PROG_DEGOPT };
+enum { PROG_LOGM = 0, PROG_SQRTDB, PROG_EST, PROG_BALANCE, PROG_DEGOPT, PROG_EXPM };
 
 int cap_load(Cap& C, cudaStream_t st, const double* const* src, int slot) {
   // load_kernel writes slot G_B; other slots by a copy
@@ -3897,6 +4013,42 @@ int cap_block(Cap& C, int prog, int has2, int p1) {
                                                                       0, C.c.margin, nullptr, &C.c.desc->max_sweeps);
     GL store_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.desc, G_B);
     GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 2, t_cap_nodes + 1);
+  } else if (prog == PROG_EXPM) {
+    if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
+    if (cap_norm(C, st, LS_ALL, G_B, C.c.nrm)) return LGM_ERR_CUDA;
+    GL expm_prep_kernel<<<1, CT, 0, st>>>(C.c);
+    GL expm_scale_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.scale);
+    if (cap_ew(C, st, LS_ALL, 2, G_Y, G_Y, G_Y)) return LGM_ERR_CUDA;  // T = I
+    const int tiles = (n + TM - 1) / TM;
+    const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
+    auto gemm = [&](cudaStream_t s, DList L, int as, int bs, int cs, int j, int mode) {
+      if ((n & 1) == 0) GL expm_gemm_kernel<true><<<dim3(tiles, tiles, C.batch), 128, gsm, s>>>(C.c.S, L, as, bs, cs, j, mode);
+      else GL expm_gemm_kernel<false><<<dim3(tiles, tiles, C.batch), 128, gsm, s>>>(C.c.S, L, as, bs, cs, j, mode);
+    };
+    for (int j = 20; j >= 1; --j) {  // Horner: 20 steps, T ends in G_Y (even count)
+      const bool fromY = (j % 2 == 0);
+      gemm(st, C.c.list(LS_ALL), G_B, fromY ? G_Y : G_XI, fromY ? G_XI : G_Y, j, 0);
+    }
+    // squarings: WHILE(some matrix has squarings left), two per body (slot parity)
+    cudaGraphConditionalHandle h;
+    if (new_handle(st, &h)) return LGM_ERR_CUDA;
+    GL expm_sq_decide_kernel<<<1, CT, 0, st>>>(C.c, h, 1, 0);
+    cudaGraph_t body;
+    if (cap_while_after(st, h, &body)) return LGM_ERR_CUDA;
+    const int saved = t_cap_nodes;
+    CK(cudaStreamBeginCaptureToGraph(C.s[1], body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    {
+      const int n0 = t_cap_nodes;
+      gemm(C.s[1], C.c.list(LS_CUR), G_Y, G_Y, G_XI, 0, 1);
+      GL expm_sq_decide_kernel<<<1, CT, 0, C.s[1]>>>(C.c, h, 0, 0);
+      gemm(C.s[1], C.c.list(LS_CUR), G_XI, G_XI, G_Y, 0, 1);
+      GL expm_sq_decide_kernel<<<1, CT, 0, C.s[1]>>>(C.c, h, 1, t_cap_nodes - n0 + 1);
+      cudaGraph_t tmp;
+      CK(cudaStreamEndCapture(C.s[1], &tmp));
+    }
+    t_cap_nodes = saved;
+    GL expm_store_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.desc, C.c.ms);
+    GL block_out_kernel<<<1, 32, 0, st>>>(C.c, 4, t_cap_nodes + 1);
   } else {  // PROG_DEGOPT: X -> P2 slot G_B, first product -> G_AP (given, or one GEMM)
     if (has2 && cap_load(C, st, &C.c.desc->A2, G_AP)) return LGM_ERR_CUDA;
     if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
@@ -3965,6 +4117,8 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
   CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(expm_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
+  CK(cudaFuncSetAttribute(expm_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(gj_update2_tma_kernel, mx, (int)ut_smem()));
   CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
@@ -4143,6 +4297,16 @@ int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n, int
   d.iout = products;
   GraphKey key{0, PROG_DEGOPT, (int)n, (int)batch, 0, FP ? 1 : 0, 0, nullptr, 0};
   return run_prog(key, ws, d, st);
+}
+
+int lgm_grid_expm(const double* A, double* E, int64_t n, int64_t batch, int64_t ld, void* ws, cudaStream_t st) {
+  LgmParams P{};
+  CallDesc d = desc_base(P);
+  d.A = A;
+  d.L = E;
+  d.ld = ld;
+  GraphKey k{0, PROG_EXPM, (int)n, (int)batch, 0, 0, 0, nullptr, 0};
+  return run_prog(k, ws, d, st);
 }
 
 // kernels executed inside graphs on the current device (read back synchronously: stats only)

@@ -1,11 +1,11 @@
 """On-device validation helpers: batched reference exponential and the
-spectrum pre-check.  Both are torch plumbing on the GPU (cuBLAS / cuSOLVER), not the product
-path; they exist to validate it.
+spectrum pre-check.
 
-* ``expm_ref_batched(A)`` restates the reference's test-oracle exponential
-  (``logmpoly/matcore.py:316-334``): scale by 2^-s so that ||A||_1 <= 1/2, degree-20 Taylor
-  polynomial in Horner form T = I + X T / j (j = 20..1), then s squarings -- per matrix s,
-  batched.
+* ``expm_ref_batched(A)`` runs the reference's test-oracle exponential
+  (``logmpoly/matcore.py:318-336``) as the library's own kernels (``lgm_expm_ref_f64``:
+  device-side scaling exponent from the 1-norm, 20 Horner DMMA GEMMs T = I + X T / j with the
+  division and identity fused into the epilogue, squarings in a device-driven CUDA-graph loop,
+  per matrix s) -- no cuBLAS, no host round trip.
 * ``spectrum_violations(A, cap=512)`` is the principal-logarithm precondition check of
   ``eig_small`` (``matcore.py:343-355``): True where a matrix has an
   eigenvalue on the closed negative real axis.  Matrices above ``cap`` are not checked (the
@@ -22,22 +22,25 @@ def _torch():
 
 
 def expm_ref_batched(A):
-    """exp of each (n, n) block of a (B, n, n) float64 CUDA tensor (matcore.py:316-334)."""
+    """exp of each (n, n) block of a (B, n, n) float64 CUDA tensor (matcore.py:318-336), on the
+    library's kernels (lgm_expm_ref_f64)."""
+    import ctypes
+    from . import _lib
     torch = _torch()
-    A = A.to(torch.float64)
+    A = A.to(torch.float64).contiguous()
+    if A.dim() == 2:
+        A = A.unsqueeze(0)
     B, n, _ = A.shape
-    nrm = A.abs().sum(dim=-2).amax(dim=-1).cpu().numpy()          # ||A||_1 per matrix
-    s = np.array([0 if v <= 0.5 else max(0, int(math.ceil(math.log2(v / 0.5)))) for v in nrm])
-    scale = torch.from_numpy(np.ldexp(1.0, -s)).to(A.device)
-    X = A * scale[:, None, None]
-    eye = torch.eye(n, dtype=A.dtype, device=A.device).expand(B, n, n)
-    T = eye.clone()
-    for j in range(20, 0, -1):
-        T = eye + (X @ T) / j
-    for i in range(int(s.max()) if B else 0):
-        sq = torch.from_numpy(s > i).to(A.device)
-        T = torch.where(sq[:, None, None], T @ T, T)
-    return T
+    E = torch.empty_like(A)
+    lib = _lib.load()
+    nb = ctypes.c_size_t(0)
+    _lib.check(lib.lgm_block_workspace_bytes(n, B, ctypes.byref(nb)), "lgm_block_workspace_bytes")
+    stream = torch.cuda.current_stream(A.device)
+    with torch.cuda.stream(stream):
+        ws = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=A.device)
+    _lib.check(lib.lgm_expm_ref_f64(A.data_ptr(), E.data_ptr(), n, B, n, ws.data_ptr(), nb.value,
+                                    ctypes.c_void_p(stream.cuda_stream)), "lgm_expm_ref_f64")
+    return E
 
 
 def spectrum_violations(A, cap=512):

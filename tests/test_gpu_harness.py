@@ -105,3 +105,32 @@ def test_spectrum_precheck(tmp_path, capsys):
     matio.write_matrix(str(tmp_path / "N.txt"), N)
     assert cli.main(["logm", str(tmp_path / "N.txt"), "--check-spectrum"]) == 3
     assert "spectrum" in capsys.readouterr().err
+
+
+def _expm_ref_np(A):
+    """numpy restatement of the reference's expm_ref (matcore.py:318-336) -- test oracle."""
+    import math
+    nrm = np.abs(A).sum(axis=0).max()
+    s = 0 if nrm <= 0.5 else max(0, int(math.ceil(math.log2(nrm / 0.5))))
+    X = A / (2.0 ** s)
+    E = np.eye(A.shape[0])
+    T = E.copy()
+    for j in range(20, 0, -1):
+        T = E + (X @ T) / j
+    for _ in range(s):
+        T = T @ T
+    return T
+
+
+@pytest.mark.parametrize("n,scale", [(20, 3.0), (71, 0.2), (130, 1.5), (64, 0.0)])
+def test_expm_ref_kernels_vs_reference_recipe(n, scale):
+    """lgm_expm_ref_f64 (the library's kernels) against the reference recipe in numpy: same
+    scaling exponent per matrix (s from 0 to ~8 here), 1e-13 relative agreement."""
+    from paper_2401_10089_b200.validate import expm_ref_batched
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((3, n, n)) * scale / np.sqrt(n)
+    X[1] *= 10.0
+    got = expm_ref_batched(torch.from_numpy(X).cuda()).cpu().numpy()
+    for b in range(3):
+        ref = _expm_ref_np(X[b])
+        assert np.linalg.norm(got[b] - ref) / np.linalg.norm(ref) <= 1e-13, b

@@ -33,7 +33,7 @@ REF_SRC = "/root/reference/pkg/src/logmpoly"
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 DATA = os.path.join(ROOT, "paper_2401_10089_b200", "data")
-SCRATCH = "/tmp/fit"
+SCRATCH = os.environ.get("LGM_FIT_SCRATCH", "/tmp/fit")
 U = 2.0 ** -53
 
 
@@ -65,8 +65,9 @@ def matched_order(an, scheme, tol=2.0 * U):
 def do_fit(k, radius, restarts, m):
     fit, an, sc = load_reference()
     t0 = time.time()
-    res = fit.fit_minmax(fit.FitProblem(k=k, radius=radius), opts=fit.FitOptions(restarts=restarts))
-    info = {"k": k, "radius": radius, "restarts": restarts, "seed": 0, "max_error": float(res.achieved_max_error),
+    seed = int(os.environ.get("LGM_FIT_SEED", "0"))
+    res = fit.fit_minmax(fit.FitProblem(k=k, radius=radius), opts=fit.FitOptions(restarts=restarts, seed=seed))
+    info = {"k": k, "radius": radius, "restarts": restarts, "seed": seed, "max_error": float(res.achieved_max_error),
             "converged": bool(res.converged), "iterations": int(res.iterations), "fit_seconds": time.time() - t0}
     os.makedirs(SCRATCH, exist_ok=True)
     src = os.path.join(SCRATCH, f"minmax_k{k}.pkl")
@@ -78,9 +79,12 @@ def do_fit(k, radius, restarts, m):
 
 def do_match(k, m, src):
     fit, an, sc = load_reference()
-    with open(src, "rb") as fh:
-        obj = pickle.load(fh)
-    seed, info = obj if isinstance(obj, tuple) else (obj, {"k": k})
+    if src == "taylor":  # the reference's Taylor-embedding seed instead of a min-max solution
+        seed, info = fit.taylor_seed_scheme(k), {"k": k, "seed_scheme": "taylor_seed_scheme"}
+    else:
+        with open(src, "rb") as fh:
+            obj = pickle.load(fh)
+        seed, info = obj if isinstance(obj, tuple) else (obj, {"k": k})
     hard = list(range(1, m + 1))
     got = fit._match_orders(fit.params_from_scheme(seed), k, hard, iters=200)
     if got is None or got[1] > 64.0 * U:
@@ -113,7 +117,7 @@ def freeze(ks):
         stab_max = float(stab.max_error) / U
         comment = (f"k={k} min-max graph coefficients for -log(1-x), generated by the reference's\n"
                    f"fit_minmax (logmpoly/fit.py:496-553) via tools/gen_schemes.py: radius {info.get('radius')}\n"
-                   f"(PAPER.md Table 2 Theta_{k}), restarts {info.get('restarts')}, seed 0; achieved max error "
+                   f"(PAPER.md Table 2 Theta_{k}), restarts {info.get('restarts')}, seed {info.get('seed', 0)}; achieved max error "
                    f"{info.get('max_error')}\non the radius circle; matched Taylor order {m_match}, used as m = {m} "
                    f"(even; |b_i - 1/i| i <= u for i <= m); Theta recomputed\nwith theta_for_scheme (300 digits): "
                    f"{float(th.theta)!r}; tail_coeff_check passed = {tail.passed}\n"
