@@ -55,7 +55,8 @@ def test_host_chunking():
     assert driver._host_chunks(4096, 32) == 6
     assert driver._host_chunks(2000, 64) == 2
     assert driver._host_chunks(100000, 32) == 6
-    assert driver._host_chunks(4096, 65) == 1       # Engine G: one host-orchestrated pass
+    assert driver._host_chunks(4096, 65) == 2       # Engine G: two stream-ordered graph chunks
+    assert driver._host_chunks(40, 512) == 1        # (chunks of >= 32 matrices only)
 
 
 def test_workspace_sizes_through_the_abi():
