@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--max-k", type=int, default=None,
+                    help="LogmOptions.max_k (default 5: the reference's shipped schemes; 6..9 opt-in)")
     args = ap.parse_args()
     cfg = args.config if args.config in ("3b", "5b") else int(args.config)
     args.warmup = max(args.warmup, 3)
@@ -240,7 +242,8 @@ def main():
     A_np = np.ascontiguousarray(A_all[lo:hi])
     B = A_np.shape[0]
     A = torch.from_numpy(A_np).to(dev)
-    opts = lp.LogmOptions(raise_on_error=False)
+    opts = lp.LogmOptions(raise_on_error=False) if args.max_k is None else \
+        lp.LogmOptions(raise_on_error=False, max_k=args.max_k)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
 
@@ -345,7 +348,8 @@ def main():
         "config": {"workload": f"config{args.config}:{name}", "n": n, "global_batch": Bg,
                    "batch_per_gpu": B, "parallelism": f"batch-sharded x{world} (no collective; result gather "
                                                       f"to rank 0 inside the timed region)",
-                   "l2": "flushed between timed steps (256 MiB write)", "engine": engine},
+                   "l2": "flushed between timed steps (256 MiB write)", "engine": engine,
+                   "max_k": opts.max_k},
         "achieved_tflops": achieved,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
