@@ -592,8 +592,10 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = r[rr];
       __syncwarp();
+      if (s1_a1kind < 0) {  // (with a stage-1 update the rows stay in T for the DMMA below)
 #pragma unroll
-      for (int c = 0; c < 32; ++c) r[c] = T[lane * 33 + c];
+        for (int c = 0; c < 32; ++c) r[c] = T[lane * 33 + c];
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) r[c] = 0.0;
@@ -622,7 +624,44 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
       w1s[c1][c] = Mi[(size_t)J.piv[p1 + c1] * n + k0 + c];
     }
     __syncthreads();
-    if (tid < n) {
+    if (tiled) {  // on the tensor cores: per warp C(32 x 32) = z1 T + A1 W1 (8 k-steps of DMMA)
+      if (warp * 32 < n) {
+        const int g = lane >> 2, t4 = lane & 3;
+        double acc[4][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int rs = J.rowstep[warp * 32 + mi * 8 + g];
+          const bool z1 = !(rs >= p1 && rs < k0);  // P1 pivot rows restart from zero
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[mi][ni][e] = z1 ? T[(mi * 8 + g) * 33 + ni * 8 + 2 * t4 + e] : 0.0;
+        }
+        const double* a1 = wkind(J, s1_a1kind) + (size_t)(warp * 32) * NB;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) a[mi] = a1[(size_t)(mi * 8 + g) * NB + k + t4];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) b[ni] = w1s[k + t4][ni * 8 + g];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) T[(mi * 8 + g) * 33 + ni * 8 + 2 * t4 + e] = acc[mi][ni][e];
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = T[lane * 33 + c];
+      }
+    } else if (tid < n) {
       const int rs = J.rowstep[tid];
       if (rs >= p1 && rs < k0) {  // P1 pivot row: z1 = 0
 #pragma unroll
