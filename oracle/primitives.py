@@ -70,14 +70,12 @@ def _note(margins, x, thr):
 # ----------------------------------------------------------------------------- matcore
 
 def as_square(A, name="matrix"):
-    """Square float64 validation (matcore.py:51-66); real path only."""
+    """Square float64 / complex128 validation (matcore.py:51-66)."""
     A = np.asarray(A)
     if A.ndim != 2 or A.shape[0] != A.shape[1] or A.shape[0] < 1:
         raise ValueError(f"{name} must be square, got shape {A.shape}")
-    if np.iscomplexobj(A):
-        raise ValueError("complex input is outside the oracle's real FP64 scope")
-    A = A.astype(np.float64, copy=False)
-    if not np.all(np.isfinite(A)):
+    A = A.astype(np.complex128 if np.iscomplexobj(A) else np.float64, copy=False)
+    if not np.all(np.isfinite(A.view(np.float64))):
         raise ValueError(f"{name} has non-finite entries")
     return A
 
@@ -158,7 +156,11 @@ def unbalance(L, scale):
 
 
 def _sign(Y):
-    return np.where(Y >= 0, 1.0, -1.0)        # matcore.py:226-231 (real branch)
+    """matcore.py:226-231: sign(Y), and Y / |Y| (1 where Y = 0) for complex Y."""
+    if np.iscomplexobj(Y):
+        a = np.abs(Y)
+        return np.where(a == 0, 1.0 + 0j, Y / np.where(a == 0, 1.0, a))
+    return np.where(Y >= 0, 1.0, -1.0)
 
 
 def est_product_norm(factors, counter=None, itmax=5, margins=None):

@@ -7,6 +7,7 @@ must reproduce them (same numpy/scipy call sequence => same bits on this image; 
 suite runs on a host whose OpenBLAS picks a different kernel).
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -195,3 +196,27 @@ def test_logm_failure_statuses(golden):
         D.logm(np.ones((2, 3)))
     with pytest.raises(P.ConvergenceError):
         D.logm(np.diag([-1.0, 2.0]))
+
+
+def test_oracle_complex_branch_vs_reference_primitives():
+    """complex128 (matcore.py:60-61, complex sign matcore.py:226-231): the restated driver over
+    the restated primitives reproduces the restated driver over the reference's own primitives
+    (tests/golden/golden_complex_v1.npz, make_golden_complex.py) bit for bit."""
+    from oracle import driver as D
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_complex_v1.npz"))
+    fields = [str(f) for f in g["drv_fields"]]
+    for name in (str(s) for s in g["drv_names"]):
+        A = g[f"drv/{name}/A"]
+        L, rep = D.logm_status(A, D.default_prims())
+        assert [rep[f] for f in fields] == list(g[f"drv/{name}/ints"]), name
+        if rep["status"] == 0:
+            assert L.dtype == np.complex128 and np.array_equal(L, g[f"drv/{name}/L"]), name
+    M = g["prim/est/M"]
+    for p in (1, 3, 8):
+        c = P.Counter()
+        v = P.est_power_norm(M, p, counter=c)
+        assert [v, c.estimation_passes] == list(g[f"prim/est/{p}"])
+    X, _ = P.sqrt_db(g["prim/sqrt/A"])
+    assert np.array_equal(X, g["prim/sqrt/X"])
+    B, sc, _ = P.balance(g["prim/bal/A"])
+    assert np.array_equal(B, g["prim/bal/B"]) and np.array_equal(sc, g["prim/bal/scale"])
