@@ -5,7 +5,7 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude
 SRC     := paper_2401_10089_b200/csrc
 OUT     := paper_2401_10089_b200/_build
-OBJS    := $(OUT)/lgm_api.o $(OUT)/lgm_grid.o
+OBJS    := $(OUT)/lgm_api.o $(OUT)/lgm_grid.o $(OUT)/lgm_spectrum.o
 LIB     := $(OUT)/liblogmpoly_b200.so
 
 all: $(LIB)
@@ -29,19 +29,19 @@ $(PROF): $(SRC)/lgm_api.cu $(SRC)/lgm_grid.cu $(wildcard $(SRC)/*.cuh $(SRC)/*.h
 	@mkdir -p $(OUT)
 	$(NVCC) $(NVFLAGS) -DLGM_PHASE_PROF -c $(SRC)/lgm_api.cu -o $(OUT)/lgm_api_prof.o
 	$(NVCC) $(NVFLAGS) -DLGM_PHASE_PROF -c $(SRC)/lgm_grid.cu -o $(OUT)/lgm_grid_prof.o
-	$(NVCC) $(ARCH) -shared -o $@ $(OUT)/lgm_api_prof.o $(OUT)/lgm_grid_prof.o
+	$(NVCC) $(ARCH) -shared -o $@ $(OUT)/lgm_api_prof.o $(OUT)/lgm_grid_prof.o $(OUT)/lgm_spectrum.o
 .PHONY: prof
 
 # A/B variants: make variant V=mb10 VFLAGS=-DLGM_F32_MINB=10  (tools/time_lib.py with LGM_LIB)
 variant:
 	@mkdir -p $(OUT)/var
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/lgm_api.cu -o $(OUT)/var/lgm_api_$(V).o
-	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/var/lgm_api_$(V).o $(OUT)/lgm_grid.o
+	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/var/lgm_api_$(V).o $(OUT)/lgm_grid.o $(OUT)/lgm_spectrum.o
 .PHONY: variant
 
 # A/B variants of the grid engine: make gvariant V=rt64 VFLAGS=-DG2_RT=64
 gvariant:
 	@mkdir -p $(OUT)/var
 	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/lgm_grid.cu -o $(OUT)/var/lgm_grid_$(V).o
-	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/lgm_api.o $(OUT)/var/lgm_grid_$(V).o
+	$(NVCC) $(ARCH) -shared -o $(OUT)/var/liblogmpoly_b200_$(V).so $(OUT)/lgm_api.o $(OUT)/var/lgm_grid_$(V).o $(OUT)/lgm_spectrum.o
 .PHONY: gvariant

@@ -139,6 +139,13 @@ int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z,
 int lgm_expm_ref_f64(const double* A, double* E, int64_t n, int64_t batch, int64_t ld,
                      void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
+/* eig_small pre-check (matcore.py:343-355) on the device: flags[b] = 1 when
+ * matrix b has an eigenvalue on the closed negative real axis, 0 when not, 2 when the QR
+ * iteration did not converge.  Hessenberg reduction + Francis double-shift QR per matrix;
+ * workspace >= batch * n * n doubles (lgm_block_workspace_bytes suffices). */
+int lgm_spectrum_check_f64(const double* A, int32_t* flags_dev, int64_t n, int64_t batch, int64_t ld,
+                           void* workspace, size_t workspace_bytes, lgm_stream_t stream);
+
 const char* lgm_status_string(int code);
 
 /* Number of CUDA kernels this library has launched so far (process-wide, monotonic):

@@ -3056,7 +3056,6 @@ __global__ void __launch_bounds__(CT) select_step_kernel(Ctl c, cudaGraphConditi
 // node slots: P2 = I - B (G_B), P3 = A_I2 (G_AP), P4.. (G_XI, G_YI, G_P6 .. G_P11); R temp G_Y,
 // L temp G_AM.  Scheme k_b's coefficient rows come from the call's parameter block.
 __constant__ int c_node_slot[12] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11};
-constexpr int h_node_slot[12] = {-1, -1, G_B, G_AP, G_XI, G_YI, G_P6, G_P7, G_P8, G_P9, G_P10, G_P11};
 
 __global__ void __launch_bounds__(CT) decide_poly_kernel(Ctl c) {
   __shared__ int s_w[33];

@@ -8,8 +8,10 @@ spectrum pre-check.
   per matrix s) -- no cuBLAS, no host round trip.
 * ``spectrum_violations(A, cap=512)`` is the principal-logarithm precondition check of
   ``eig_small`` (``matcore.py:343-355``): True where a matrix has an
-  eigenvalue on the closed negative real axis.  Matrices above ``cap`` are not checked (the
-  SPEC's cap: there violations surface as DB non-convergence).
+  eigenvalue on the closed negative real axis, decided by the library's own kernel
+  (``lgm_spectrum_check_f64``: Householder Hessenberg reduction + Francis double-shift QR, one
+  CTA per matrix).  Matrices above ``cap`` are not checked (the SPEC's cap: there violations
+  surface as DB non-convergence).
 """
 import math
 
@@ -43,16 +45,41 @@ def expm_ref_batched(A):
     return E
 
 
-def spectrum_violations(A, cap=512):
-    """Boolean mask (numpy, per matrix): an eigenvalue lies on the closed negative real axis
-    (real eigenvalue <= 0).  Matrices with n > cap are reported False (unchecked)."""
+def spectrum_check(A):
+    """Per-matrix flags of lgm_spectrum_check_f64 (the library's Hessenberg + Francis QR):
+    1 = an eigenvalue on the closed negative real axis, 0 = none, 2 = QR did not converge."""
+    import ctypes
+    from . import _lib
     torch = _torch()
     if not isinstance(A, torch.Tensor):
         A = torch.from_numpy(np.ascontiguousarray(A, dtype=np.float64))
     if A.dim() == 2:
         A = A.unsqueeze(0)
-    if A.shape[-1] > cap:
-        return np.zeros(A.shape[0], dtype=bool)
-    lam = torch.linalg.eigvals(A.to(torch.float64))
-    bad = (lam.imag == 0) & (lam.real <= 0)
-    return bad.any(dim=-1).cpu().numpy()
+    dev = A.device if A.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    A = A.to(device=dev, dtype=torch.float64).contiguous()
+    B, n, _ = A.shape
+    flags = torch.zeros(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    nb = B * n * n * 8
+    with torch.cuda.stream(stream):
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().lgm_spectrum_check_f64(A.data_ptr(), flags.data_ptr(), n, B, n, ws.data_ptr(), nb,
+                                                  ctypes.c_void_p(stream.cuda_stream)), "lgm_spectrum_check_f64")
+    return flags.cpu().numpy()
+
+
+def spectrum_violations(A, cap=512):
+    """Boolean mask (numpy, per matrix): an eigenvalue lies on the closed negative real axis
+    (real eigenvalue <= 0), decided on the device (spectrum_check).  Matrices with n > cap are
+    reported False (unchecked, as eig_small's cap); a QR non-convergence raises
+    ConvergenceError like eig_small (matcore.py:353-355)."""
+    from .exceptions import ConvergenceError
+    torch = _torch()
+    n = A.shape[-1]
+    if n > cap:
+        B = A.shape[0] if len(A.shape) == 3 else 1
+        return np.zeros(B, dtype=bool)
+    f = spectrum_check(A)
+    if (f == 2).any():
+        raise ConvergenceError("eigenvalue iteration failed (spectrum pre-check)", None)
+    return f == 1

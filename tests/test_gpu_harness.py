@@ -134,3 +134,33 @@ def test_expm_ref_kernels_vs_reference_recipe(n, scale):
     for b in range(3):
         ref = _expm_ref_np(X[b])
         assert np.linalg.norm(got[b] - ref) / np.linalg.norm(ref) <= 1e-13, b
+
+
+def test_spectrum_check_kernel_vs_numpy_eigvals():
+    """lgm_spectrum_check_f64 (Hessenberg + Francis QR on the device) against numpy's eigvals
+    (LAPACK dgeev, what eig_small calls) on matrices with clear-cut spectra."""
+    from paper_2401_10089_b200.validate import spectrum_check
+    rng = np.random.default_rng(3)
+    mats, want = [], []
+    for n in (1, 2, 5, 17, 64, 100, 257):
+        for kind in range(4):
+            Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+            lam = rng.uniform(0.5, 3.0, n)
+            if kind == 1:
+                lam[rng.integers(n)] = -rng.uniform(0.5, 2.0)        # one negative real eigenvalue
+            A = (Q * lam) @ Q.T
+            if kind == 2 and n >= 2:                                    # complex pairs, positive reals
+                R = np.eye(n)
+                R[:2, :2] = [[1.0, -2.0], [2.0, 1.0]]
+                A = Q @ R @ np.diag(lam) @ Q.T
+            if kind == 3:                                               # nonnormal, shifted spectrum
+                A = rng.standard_normal((n, n)) / np.sqrt(n) + 3.0 * np.eye(n)
+                if n >= 5:
+                    A[0, 0] = -10.0
+            ev = np.linalg.eigvals(A)
+            mats.append(A)
+            want.append(bool(((ev.imag == 0) & (ev.real <= 0)).any()))
+    for A, w in zip(mats, want):
+        assert spectrum_check(A)[0] == int(w), (A.shape, w)
+    batch = np.stack([m for m in mats if m.shape[0] == 17])
+    assert list(spectrum_check(batch)) == [int(w) for m, w in zip(mats, want) if m.shape[0] == 17]
