@@ -561,6 +561,9 @@ struct PanelSmem {
   double red[16];
   int piv_s[32];
   double w1s[32][34];
+#ifdef LGM_PANEL_1BAR
+  double cand[2][16][32];  // every warp's candidate pivot row (one barrier per pivot step)
+#endif
 };
 // Returns false when the panel hit an exact zero pivot (status set).
 template <int NT>
@@ -704,6 +707,13 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
         wkey32[par][warp] = wk;
         wval[par][warp] = wv;
       }
+#ifdef LGM_PANEL_1BAR
+      if (wk != 0u && lane == ((1023 - (int)(wk & 0x3ffu)) & 31)) {  // this warp's candidate row
+        double* cw = ps.cand[par][warp];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(cw + c) = make_double2(r[c], r[c + 1]);
+      }
+#endif
       __syncthreads();
       const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par][lane] : 0u);
       if (bk == 0u) {  // exact zero pivot (matcore.py:124-125)
@@ -713,6 +723,16 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
       const int p = 1023 - (int)(bk & 0x3ffu);
       const double rp = lgm_rcp(wval[par][p >> 5]);
       const bool own = (tid == p);
+#ifdef LGM_PANEL_1BAR
+      pr = ps.cand[par][p >> 5];
+      if (own) {
+        used = true;
+        mypiv = r0;
+        rowscale = rp;
+        my_step = k0 + kk;
+        piv_s[kk] = tid;
+      }
+#else
       if (own) {
         used = true;
         mypiv = r0;
@@ -724,6 +744,7 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
         piv_s[kk] = tid;
       }
       __syncthreads();
+#endif
       g = own ? 0.0 : r0 * rp;
       last = own ? 1.0 : -g;
     }
@@ -735,6 +756,9 @@ __device__ __forceinline__ bool panel_body(const InvJob& J, int n, int k0, int n
     }
     r[31] = last;
   }
+#ifdef LGM_PANEL_1BAR
+  __syncthreads();  // the last steps' piv_s entries (no second barrier per step)
+#endif
   const bool piv_here = my_step >= 0;
   if (piv_here) {
 #pragma unroll
@@ -1183,7 +1207,8 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
   double* Bs1 = As2 + RT * LDA_S;
   double* Bs2 = Bs1 + TK * LDB_S;
   double* Zs = Bs2 + TK * LDB_S;  // a zero row: the A1 operand of P2's pivot rows (z2 = 0)
-  const InvJob J = jobs[blockIdx.z];
+  // consecutive pairs traverse the jobs in opposite orders (L2 reuse across passes)
+  const InvJob J = jobs[(q & 1) ? gridDim.z - 1 - blockIdx.z : blockIdx.z];
   if (*J.status) return;  // (checked first: moving this load after the tile loads measured 7% slower)
   const double* W1 = wkind(J, 3 * q);
   const double* W2 = wkind(J, 3 * q + 1);
@@ -1879,8 +1904,13 @@ __global__ void est_nz_kernel(EstJob* jobs, int n) {
 #ifndef EST_FWD_R
 #define EST_FWD_R 4
 #endif
+// Job order alternates between consecutive thin products (boustrophedon): the matrices read
+// last by one product are read first by the next, while they are still L2 resident.
+__device__ __forceinline__ int est_job(int q, int flip, unsigned bi, unsigned nb) {
+  return ((q ^ flip) & 1) ? (int)(nb - 1 - bi) : (int)bi;
+}
 __global__ void __launch_bounds__(256) est_fwd_kernel(EstJob* jobs, int n, int q) {
-  EstJob& J = jobs[blockIdx.y];
+  EstJob& J = jobs[est_job(q, 0, blockIdx.y, gridDim.y)];
   if (J.done || q >= J.total) return;
   const double* M = (J.M2 && q == 0) ? J.M2 : J.M1;
   const double* x = (q & 1) ? J.V1 : J.V0;
@@ -1924,8 +1954,8 @@ __global__ void __launch_bounds__(256) est_fwd_kernel(EstJob* jobs, int n, int q
 constexpr int ADJ_ROWS = 64;
 // z = M^T x: thread per column, a 64-row slab per CTA (partials reduced in fixed order by
 // est_adj_reduce_kernel), 4 independent accumulators per column.
-__global__ void __launch_bounds__(128) est_adj_kernel(EstJob* jobs, int n, int q) {
-  EstJob& J = jobs[blockIdx.z];
+__global__ void __launch_bounds__(128) est_adj_kernel(EstJob* jobs, int n, int q, int flip) {
+  EstJob& J = jobs[est_job(q, flip, blockIdx.z, gridDim.z)];
   if (J.done || q >= J.total) return;
   const double* M = (q < J.p1) ? J.M1 : J.M2;
   const double* x = (q & 1) ? J.V1 : J.V0;
@@ -1954,8 +1984,8 @@ __global__ void __launch_bounds__(128) est_adj_kernel(EstJob* jobs, int n, int q
 
 // Even n: two adjacent columns per thread (16-byte loads: twice the bytes per request of the
 // kernel above, same per-column accumulation order, so the same partial sums).
-__global__ void __launch_bounds__(128) est_adj2_kernel(EstJob* jobs, int n, int q) {
-  EstJob& J = jobs[blockIdx.z];
+__global__ void __launch_bounds__(128) est_adj2_kernel(EstJob* jobs, int n, int q, int flip) {
+  EstJob& J = jobs[est_job(q, flip, blockIdx.z, gridDim.z)];
   if (J.done || q >= J.total) return;
   const double* M = (q < J.p1) ? J.M1 : J.M2;
   const double* x = (q & 1) ? J.V1 : J.V0;
@@ -3685,8 +3715,9 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
       GL est_fwd_kernel<<<dim3((n + 8 * EST_FWD_R - 1) / (8 * EST_FWD_R), nj), 256, 0, st>>>(C.c.est, n, q);
     GL est_after_fwd_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
     for (int q = 0; q < maxq; ++q) {
-      if ((n & 1) == 0) GL est_adj2_kernel<<<dim3((n + 255) / 256, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q);
-      else GL est_adj_kernel<<<dim3((n + 127) / 128, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q);
+      // (flip: the first adjoint product runs opposite to the last forward one)
+      if ((n & 1) == 0) GL est_adj2_kernel<<<dim3((n + 255) / 256, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q, maxq & 1);
+      else GL est_adj_kernel<<<dim3((n + 127) / 128, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q, maxq & 1);
       GL est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, q, C.c.splits);
     }
     GL est_after_adj_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
