@@ -63,6 +63,18 @@ bool use_g1(int n) {
 // columns not yet written from Src.
 bool inv_oop(int n) { return use_g1(n) || (n <= 512 && n % 64 == 0 && !(std::getenv("LGM_G2_RANK64") && std::getenv("LGM_G2_RANK64")[0] == '0')); }
 
+// Cluster-resident estimator for EST_FUSED_MAXN < n <= 512, opt-in (LGM_EST_CLUSTER=1): at
+// config 4 it measured 14.8 ms per 256-job estimate against 5.0 ms for the per-step kernels --
+// only 8 clusters of 16 CTAs run at once and each job's ~63 dependent thin products serialise
+// on cluster barriers and DSMEM gathers
+bool est_cluster_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_EST_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -2268,6 +2280,172 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
 }
 
 // ------------------------------------------------------------------------------------------
+// The whole estimate of one job per thread-block cluster (EST_FUSED_MAXN < n <= 512): the CL
+// CTAs of the cluster hold M1's rows in shared memory (rank r owns rows [r R, (r+1) R),
+// R = ceil(n / CL) <= 32) for every thin product of every sweep, instead of streaming M1
+// from HBM once per product.  Forward products are row-local (warp per row, lane-strided FMAs
+// and a butterfly, as est_fwd_kernel) followed by an all-gather of the row segments over
+// DSMEM; adjoint products form per-CTA column partials over the CTA's rows (4 interleaved
+// accumulators), reduce-scatter them in rank order over DSMEM and all-gather the column
+// segments.  The after-bodies (norms, argmax, top-k, history, stop tests) run redundantly on
+// every CTA's identical local copy of the vectors and job state; rank 0 publishes the result.
+// One cluster barrier per forward product, two per adjoint product.
+constexpr int ECL_NT = 256;
+constexpr int ECL_MAXR = 32;
+struct EclSmem {
+  EstJob S;           // this CTA's copy of the job state (V0 / V1 / hist point into shared)
+  double sred[8];
+  EstAdjSmem sa;
+  int hist[16];
+};
+template <int CL>
+__global__ void __launch_bounds__(ECL_NT, 1) est_cluster_kernel(EstJob* jobs, int n, double rsum, int itmax) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double ecl[];
+  __shared__ EclSmem es;
+  const int rank = (int)cl.block_rank();
+  EstJob& G = jobs[blockIdx.x / CL];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int R = (n + CL - 1) / CL;             // rows (and adjoint columns) per CTA
+  const int r0 = rank * R, r1 = min(n, r0 + R);
+  double* Ms = ecl;                             // [R][n] rows r0.. of M1
+  double* V0 = Ms + (size_t)ECL_MAXR * n;       // [2][n]
+  double* V1 = V0 + 2 * n;                      // [2][n]
+  double* part = V1 + 2 * n;                    // [2][n] column partials over this CTA's rows
+  const bool dead = !G.live || (G.zchk && !G.nzf);
+  if (dead) {  // (uniform over the cluster: every CTA reads the same job)
+    if (rank == 0 && tid == 0) {
+      G.done = 1;
+      G.est = 0.0;
+      G.passes = 0;
+      G.mm = INFINITY;
+    }
+    return;
+  }
+  EstJob& S = es.S;
+  if (tid == 0) {
+    S = G;
+    S.V0 = V0;
+    S.V1 = V1;
+    S.hist = es.hist;
+    const int t = n < 2 ? n : 2;
+    S.est = 0.0; S.best_j = 0; S.ncols = t; S.nhist = 0; S.passes = 0; S.mm = INFINITY;
+    S.total = S.p1 + (S.M2 ? 1 : 0);
+    S.done = 0;
+  }
+  for (int i = tid; i < n; i += ECL_NT) {
+    V0[i] = 1.0 / n;
+    if (n > 1) V0[n + i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
+  }
+  for (size_t idx = tid; idx < (size_t)(r1 - r0) * n; idx += ECL_NT) Ms[idx] = G.M1[(size_t)r0 * n + idx];
+  __syncthreads();
+  const int total = S.total, p1 = S.p1;
+  const double* M2 = S.M2;
+  for (int sweep = 0; sweep < itmax; ++sweep) {
+    if (S.done) break;
+    const int nc = S.ncols;
+    for (int q = 0; q < total; ++q) {  // forward: y = M x, my rows, then all-gather
+      const bool use2 = M2 && q == 0;
+      const double* x = (q & 1) ? V1 : V0;
+      double* y = (q & 1) ? V0 : V1;
+      for (int i = r0 + warp; i < r1; i += ECL_NT / 32) {
+        const double* Mr = use2 ? M2 + (size_t)i * n : Ms + (size_t)(i - r0) * n;
+        double a0 = 0.0, a1 = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          const double m = Mr[j];
+          a0 = fma(m, x[j], a0);
+          if (nc > 1) a1 = fma(m, x[n + j], a1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        }
+        if (lane == 0) {
+          y[i] = a0;
+          if (nc > 1) y[n + i] = a1;
+        }
+      }
+      cl.sync();
+      for (int p = 0; p < CL; ++p) {
+        if (p == rank) continue;
+        const int q0 = p * R, q1 = min(n, q0 + R);
+        const double* ry = cl.map_shared_rank(y, p);
+        for (int i = q0 + tid; i < q1; i += ECL_NT) {
+          y[i] = ry[i];
+          if (nc > 1) y[n + i] = ry[n + i];
+        }
+      }
+      __syncthreads();
+    }
+    cl.sync();  // every peer's gather done before the after-body rewrites the vectors in place
+    est_after_fwd_body(S, n, sweep, es.sred);
+    __syncthreads();
+    if (S.done) break;
+    const bool two = S.ncols > 1;
+    for (int q = 0; q < total; ++q) {  // adjoint: z = M^T x, partials, reduce-scatter, gather
+      const bool use2 = q >= p1;
+      const double* x = (q & 1) ? V1 : V0;
+      double* y = (q & 1) ? V0 : V1;
+      for (int c = tid; c < n; c += ECL_NT) {
+        double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+        int r = r0;
+        for (; r + 3 < r1; r += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double m = use2 ? M2[(size_t)(r + u) * n + c] : Ms[(size_t)(r + u - r0) * n + c];
+            a0[u] = fma(m, x[r + u], a0[u]);
+            if (two) a1[u] = fma(m, x[n + r + u], a1[u]);
+          }
+        }
+        for (; r < r1; ++r) {
+          const double m = use2 ? M2[(size_t)r * n + c] : Ms[(size_t)(r - r0) * n + c];
+          a0[0] = fma(m, x[r], a0[0]);
+          if (two) a1[0] = fma(m, x[n + r], a1[0]);
+        }
+        part[c] = (a0[0] + a0[1]) + (a0[2] + a0[3]);
+        part[n + c] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+      }
+      cl.sync();
+      for (int c = r0 + tid; c < r1; c += ECL_NT) {  // my column block, summed in rank order
+        double s0 = 0.0, s1 = 0.0;
+        for (int p = 0; p < CL; ++p) {
+          const double* rp = cl.map_shared_rank(part, p);
+          s0 += rp[c];
+          s1 += rp[n + c];
+        }
+        y[c] = s0;
+        if (two) y[n + c] = s1;
+      }
+      cl.sync();
+      for (int p = 0; p < CL; ++p) {
+        if (p == rank) continue;
+        const int q0 = p * R, q1 = min(n, q0 + R);
+        const double* ry = cl.map_shared_rank(y, p);
+        for (int c = q0 + tid; c < q1; c += ECL_NT) {
+          y[c] = ry[c];
+          if (two) y[n + c] = ry[n + c];
+        }
+      }
+      __syncthreads();
+    }
+    cl.sync();
+    est_after_adj_body(S, n, sweep, es.sa);
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+  if (rank == 0 && tid == 0) {
+    G.est = S.est;
+    G.best_j = S.best_j;
+    G.passes = S.passes;
+    G.mm = S.mm;
+    G.done = 1;
+  }
+}
+inline size_t ecl_smem(int n) { return ((size_t)ECL_MAXR * n + 6 * (size_t)n) * 8; }
+
+// ------------------------------------------------------------------------------------------
 // Graph-polynomial GEMM: C = L * R, L = sum_t c_t * P_t + c0 * I built on the fly in the
 // A-tile load (numpy _combine rounding: separate multiply and add), R a plain matrix.
 struct CombSpec {
@@ -3709,6 +3887,24 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
     GL est_fused_kernel<<<nj, 256, sm, st>>>(C.c.est, n, rsum, C.itmax);
     return 0;
   }
+  if (n > EST_FUSED_MAXN && n <= 512 && est_cluster_on()) {  // M1 resident in a cluster's smem
+    const int cl = n <= 256 ? 8 : 16;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nj * cl);
+    cfg.blockDim = dim3(ECL_NT);
+    cfg.dynamicSmemBytes = ecl_smem(n);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cl == 8) CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<8>, C.c.est, n, rsum, C.itmax)));
+    else CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<16>, C.c.est, n, rsum, C.itmax)));
+    return 0;
+  }
   GL est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, rsum);
   for (int sweep = 0; sweep < C.itmax; ++sweep) {
     for (int q = 0; q < maxq; ++q)
@@ -4190,6 +4386,9 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(expm_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(gj_update2_tma_kernel, mx, (int)ut_smem()));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<8>, mx, (int)ecl_smem(512)));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<16>, mx, (int)ecl_smem(512)));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
   return 0;
 }
