@@ -24,12 +24,28 @@ int lgm_count_launch() { g_lgm_launches.fetch_add(1, std::memory_order_relaxed);
 template <int NMAX, bool FULL>
 __global__ void __launch_bounds__(Cfg<NMAX>::NT, NMAX == 32 ? LGM_F32_MINB : 1) logm_fused_kernel(const double* __restrict__ A, double* __restrict__ L,
                                                                   lgm_report* rep, long long ld, int n, double* ws,
-                                                                  const __grid_constant__ LgmParams P) {
+                                                                  long long wst, const __grid_constant__ LgmParams P) {
   extern __shared__ __align__(16) double smem[];
   Ctx<NMAX, FULL> c;
   c.init(smem, n, &P);
   const long long b = blockIdx.x;
-  logm_one<NMAX, FULL>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * LGM_FUSED_WS * n * n);
+  logm_one<NMAX, FULL>(c, A + b * n * ld, L + b * n * ld, ld, rep + b, ws + b * wst);
+}
+
+// Engine F workspace stride per matrix (doubles): LGM_FUSED_WS n^2 (+ the LGM_WS_GUARD band)
+static long long fused_wst(int64_t n) { return (long long)LGM_FUSED_WS * n * n + (long long)(lgm_ws_guard_bytes() / 8); }
+
+// guard bands after each matrix's Engine F workspace: check = 0 fills (0xA5 bytes), 1 counts
+__global__ void fused_guard_kernel(unsigned long long* ws, long long n2, long long wst, long long batch, int check,
+                                   unsigned long long* bad) {
+  const long long gw = wst - n2;
+  unsigned long long nbad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < batch * gw; i += (long long)gridDim.x * blockDim.x) {
+    const long long at = (i / gw) * wst + n2 + i % gw;
+    if (check) nbad += ws[at] != 0xA5A5A5A5A5A5A5A5ull;
+    else ws[at] = 0xA5A5A5A5A5A5A5A5ull;
+  }
+  if (check && nbad) atomicAdd(bad, nbad);
 }
 
 template <int NMAX>
@@ -167,8 +183,11 @@ static int launch_fused(const double* A, double* L, lgm_report* rep, int64_t ld,
     return want > Cfg<NMAX>::SMEM_BYTES ? want : Cfg<NMAX>::SMEM_BYTES;
   }();
   if (prep<NMAX>(logm_fused_kernel<NMAX, FULL>, sm_bytes)) return LGM_ERR_CUDA;
+  const long long wst = fused_wst(n);
+  if (lgm_ws_guard_bytes())
+    fused_guard_kernel<<<256, 256, 0, s>>>((unsigned long long*)ws, (long long)LGM_FUSED_WS * n * n, wst, batch, 0, nullptr);
   lgm_count_launch(), logm_fused_kernel<NMAX, FULL><<<(unsigned)batch, Cfg<NMAX>::NT, sm_bytes, s>>>(
-                          A, L, rep, ld, (int)n, (double*)ws, P);
+                          A, L, rep, ld, (int)n, (double*)ws, wst, P);
   return check_launch();
 }
 
@@ -229,7 +248,7 @@ int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes) {
   if (!bytes || n < 1 || batch < 0) return LGM_ERR_ARG;
   // n <= 64: LGM_FUSED_WS n^2 doubles per matrix: polynomial nodes P4..P10 and A_prev / A_I2
   // (only P4..P6 and A_I2 are touched with the shipped k <= 5 schemes: L2 resident)
-  *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * LGM_FUSED_WS * n * n * sizeof(double)
+  *bytes = n <= LGM_FUSED_MAX ? (size_t)batch * fused_wst(n) * sizeof(double)
                    : lgm_grid_workspace_bytes(n, batch < grid_chunk() ? batch : grid_chunk());
   return 0;
 }
@@ -426,6 +445,25 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
     if (rc) return rc;
   }
   return 0;
+}
+
+// Diagnostics (LGM_WS_GUARD=1 only): the guard bands after every workspace region / slot.
+// check = 0 fills them with the pattern (the library also does so before each call that uses
+// the layout); check = 1 adds to *bad (device pointer) the number of guard bytes that no
+// longer hold it, i.e. out-of-bounds writes by the calls since the fill.  layout 1: the
+// lgm_logm_f64 workspace for n <= 64 (Engine F); 0: the Engine G / building-block workspace.
+// Returns 1 if done, 0 if guards are off.
+int lgm_debug_ws_guard(int64_t n, int64_t batch, int layout, void* ws, int check, unsigned long long* bad,
+                       lgm_stream_t stream) {
+  if (!lgm_ws_guard_bytes()) return 0;
+  if (!ws || (check && !bad) || n < 1 || batch < 1) return LGM_ERR_ARG;
+  if (layout == 1) {
+    fused_guard_kernel<<<256, 256, 0, (cudaStream_t)stream>>>((unsigned long long*)ws, (long long)LGM_FUSED_WS * n * n,
+                                                                fused_wst(n), batch, check, bad);
+    return cudaGetLastError() == cudaSuccess ? 1 : LGM_ERR_CUDA;
+  }
+  const int rc = lgm_grid_ws_guard(n, batch < grid_chunk() ? batch : grid_chunk(), ws, check, bad, (cudaStream_t)stream);
+  return rc < 0 ? rc : 1;
 }
 
 }  // extern "C"

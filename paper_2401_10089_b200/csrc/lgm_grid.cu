@@ -1539,7 +1539,8 @@ __global__ void __launch_bounds__(UT_THREADS, UT_MINB) gj_update2_tma_kernel(con
 struct Slots {
   double* ws;       // base of the n x n slots
   int n;
-  __device__ __host__ double* buf(int b, int k) const { return ws + ((size_t)b * NBUF + k) * (size_t)n * n; }
+  size_t st;        // slot stride in doubles: n^2 (+ a guard band under LGM_WS_GUARD=1)
+  __device__ __host__ double* buf(int b, int k) const { return ws + ((size_t)b * NBUF + k) * st; }
 };
 
 // Device-built matrix lists: ids[0 .. *cnt) (ascending matrix indices), capacity = batch.
@@ -2660,32 +2661,44 @@ struct Ctl {  // device pointers into the workspace (fixed per workspace)
   __host__ __device__ int* ids(int id) const { return lists + (size_t)id * batch; }
 };
 
-size_t ctl_bytes(int64_t n, int64_t batch) {
+// Workspace regions in carve order (byte sizes); each occupies its size rounded up to 256 B
+// plus the guard band (0 unless LGM_WS_GUARD=1; then every region and every n x n slot is
+// followed by lgm_ws_guard_bytes() of a fill pattern that lgm_debug_ws_guard_check verifies:
+// an out-of-bounds write detector standing in for compute-sanitizer memcheck).
+constexpr int NREG = 25;
+__host__ __device__ inline void ctl_sizes(int64_t n, int64_t batch, size_t slot_st, size_t* sz) {
   const int64_t splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
-  size_t s = 0;
-  auto add = [&](size_t b) { s += (b + 255) & ~size_t(255); };
-  add((size_t)batch * NBUF * n * n * 8);   // slots
-  add(sizeof(CallDesc));
-  add(batch * sizeof(MDev));
-  add((size_t)LS_N * batch * 4);
-  add(LS_N * 4);
-  add(2 * batch * sizeof(InvJob));
-  add(batch * sizeof(EstJob));
-  add(2 * batch * n * 4);                  // piv
-  add(2 * batch * n * 4);                  // step
-  add(12 * batch * NB * n * 8);            // W
-  add(2 * batch * 8);                      // logdet
-  add(2 * batch * 4);                      // istat
-  add(4);                                  // dead
-  add(batch * 4);                          // scaling
-  for (int q = 0; q < 4; ++q) add(batch * 8);  // nrm, nrm2, change, size
-  add(batch * 4);                          // flag
-  add((size_t)batch * n * 8);              // scale
-  add(batch * 8);                          // margin
-  add(batch * 4);                          // sweeps
-  add((size_t)batch * 4 * n * 8);          // vec
-  add((size_t)batch * splits * 2 * n * 8); // part
-  add(batch * 16 * 4);                     // hist
+  int i = 0;
+  sz[i++] = (size_t)batch * NBUF * slot_st * 8;  // slots
+  sz[i++] = sizeof(CallDesc);
+  sz[i++] = batch * sizeof(MDev);
+  sz[i++] = (size_t)LS_N * batch * 4;            // lists
+  sz[i++] = LS_N * 4;                            // cnt
+  sz[i++] = 2 * batch * sizeof(InvJob);
+  sz[i++] = batch * sizeof(EstJob);
+  sz[i++] = 2 * (size_t)batch * n * 4;           // piv
+  sz[i++] = 2 * (size_t)batch * n * 4;           // step
+  sz[i++] = 12 * (size_t)batch * NB * n * 8;     // W
+  sz[i++] = 2 * batch * 8;                       // logdet
+  sz[i++] = 2 * batch * 4;                       // istat
+  sz[i++] = 4;                                   // dead
+  sz[i++] = batch * 4;                           // scaling
+  for (int q = 0; q < 4; ++q) sz[i++] = batch * 8;  // nrm, nrm2, change, size
+  sz[i++] = batch * 4;                           // flag
+  sz[i++] = (size_t)batch * n * 8;               // scale
+  sz[i++] = batch * 8;                           // margin
+  sz[i++] = batch * 4;                           // sweeps
+  sz[i++] = (size_t)batch * 4 * n * 8;           // vec
+  sz[i++] = (size_t)batch * splits * 2 * n * 8;  // part
+  sz[i++] = batch * 16 * 4;                      // hist
+}
+__host__ __device__ inline size_t r256(size_t b) { return (b + 255) & ~size_t(255); }
+inline size_t slot_stride(int64_t n) { return (size_t)n * n + lgm_ws_guard_bytes() / 8; }
+
+size_t ctl_bytes(int64_t n, int64_t batch) {
+  size_t sz[NREG], s = 0;
+  ctl_sizes(n, batch, slot_stride(n), sz);
+  for (int r = 0; r < NREG; ++r) s += r256(sz[r]) + lgm_ws_guard_bytes();
   return s;
 }
 
@@ -2694,35 +2707,67 @@ Ctl ctl_carve(void* ws, int n, int batch) {
   c.n = n;
   c.batch = batch;
   c.splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  size_t sz[NREG];
+  ctl_sizes(n, batch, slot_stride(n), sz);
   char* p = (char*)ws;
-  auto take = [&](size_t b) { char* r = p; p += (b + 255) & ~size_t(255); return (void*)r; };
-  c.S.ws = (double*)take((size_t)batch * NBUF * n * n * 8);
+  int r = 0;
+  auto take = [&](size_t) { char* q = p; p += r256(sz[r++]) + lgm_ws_guard_bytes(); return (void*)q; };
+  c.S.ws = (double*)take(0);
   c.S.n = n;
-  c.desc = (CallDesc*)take(sizeof(CallDesc));
-  c.ms = (MDev*)take(batch * sizeof(MDev));
-  c.lists = (int*)take((size_t)LS_N * batch * 4);
-  c.cnt = (int*)take(LS_N * 4);
-  c.jobs = (InvJob*)take(2 * batch * sizeof(InvJob));
-  c.est = (EstJob*)take(batch * sizeof(EstJob));
-  c.piv = (int*)take(2 * (size_t)batch * n * 4);
-  c.step = (int*)take(2 * (size_t)batch * n * 4);
-  c.W = (double*)take(12 * (size_t)batch * NB * n * 8);
-  c.logdet = (double*)take(2 * batch * 8);
-  c.istat = (int*)take(2 * batch * 4);
-  c.dead = (int*)take(4);
-  c.scaling = (int*)take(batch * 4);
-  c.nrm = (double*)take(batch * 8);
-  c.nrm2 = (double*)take(batch * 8);
-  c.change = (double*)take(batch * 8);
-  c.size = (double*)take(batch * 8);
-  c.flag = (int*)take(batch * 4);
-  c.scale = (double*)take((size_t)batch * n * 8);
-  c.margin = (double*)take(batch * 8);
-  c.sweeps = (int*)take(batch * 4);
-  c.vec = (double*)take((size_t)batch * 4 * n * 8);
-  c.part = (double*)take((size_t)batch * c.splits * 2 * n * 8);
-  c.hist = (int*)take(batch * 16 * 4);
+  c.S.st = slot_stride(n);
+  c.desc = (CallDesc*)take(0);
+  c.ms = (MDev*)take(0);
+  c.lists = (int*)take(0);
+  c.cnt = (int*)take(0);
+  c.jobs = (InvJob*)take(0);
+  c.est = (EstJob*)take(0);
+  c.piv = (int*)take(0);
+  c.step = (int*)take(0);
+  c.W = (double*)take(0);
+  c.logdet = (double*)take(0);
+  c.istat = (int*)take(0);
+  c.dead = (int*)take(0);
+  c.scaling = (int*)take(0);
+  c.nrm = (double*)take(0);
+  c.nrm2 = (double*)take(0);
+  c.change = (double*)take(0);
+  c.size = (double*)take(0);
+  c.flag = (int*)take(0);
+  c.scale = (double*)take(0);
+  c.margin = (double*)take(0);
+  c.sweeps = (int*)take(0);
+  c.vec = (double*)take(0);
+  c.part = (double*)take(0);
+  c.hist = (int*)take(0);
   return c;
+}
+
+// Guard bands: check = 0 fills them with 0xA5 bytes, check = 1 counts bytes that differ.
+__global__ void ws_guard_kernel(unsigned char* ws, int64_t n, int64_t batch, size_t gb, int check,
+                                unsigned long long* bad) {
+  size_t sz[NREG];
+  const size_t st = (size_t)n * n + gb / 8;
+  ctl_sizes(n, batch, st, sz);
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+  unsigned long long nbad = 0;
+  size_t off = 0;
+  for (int r = 0; r < NREG; ++r) {  // region tails + guard bands (bytes)
+    const size_t lo = off + sz[r], hi = off + r256(sz[r]) + gb;
+    for (size_t i = lo + tid; i < hi; i += nth) {
+      if (check) nbad += ws[i] != 0xA5u;
+      else ws[i] = 0xA5u;
+    }
+    off = hi;
+  }
+  // the guard band after every n x n slot (8-byte words)
+  const size_t gw = gb / 8, nslots = (size_t)batch * NBUF;
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(ws);
+  for (size_t i = tid; i < nslots * gw; i += nth) {
+    const size_t at = (i / gw) * st + (size_t)n * n + i % gw;
+    if (check) nbad += w[at] != 0xA5A5A5A5A5A5A5A5ull;
+    else w[at] = 0xA5A5A5A5A5A5A5A5ull;
+  }
+  if (check && nbad) atomicAdd(bad, nbad);
 }
 
 // ------------------------------------------------------------------ decide-kernel helpers
@@ -4460,6 +4505,8 @@ int run_prog(const GraphKey& k0, void* ws, const CallDesc& d, cudaStream_t st) {
   CK(cudaGetDevice(&k.dev));
   k.ws = ws;
   const Ctl c = ctl_carve(ws, k.n, k.batch);
+  if (lgm_ws_guard_bytes())
+    ws_guard_kernel<<<256, 256, 0, st>>>((unsigned char*)ws, k.n, k.batch, lgm_ws_guard_bytes(), 0, nullptr);
   lgm_count_launch(), setup_kernel<<<1, 1, 0, st>>>(c.desc, d);
   CK(cudaGetLastError());
   std::lock_guard<std::mutex> lock(g_cache_mu);
@@ -4575,6 +4622,21 @@ int lgm_grid_expm(const double* A, double* E, int64_t n, int64_t batch, int64_t 
   d.ld = ld;
   GraphKey k{0, PROG_EXPM, (int)n, (int)batch, 0, 0, 0, nullptr, 0};
   return run_prog(k, ws, d, st);
+}
+
+size_t lgm_ws_guard_bytes() {
+  static const size_t v = [] {  // thread-safe once-init
+    const char* e = std::getenv("LGM_WS_GUARD");
+    return (e && e[0] == '1') ? (size_t)4096 : (size_t)0;
+  }();
+  return v;
+}
+
+int lgm_grid_ws_guard(int64_t n, int64_t batch, void* ws, int check, unsigned long long* bad, cudaStream_t st) {
+  if (!lgm_ws_guard_bytes()) return 0;
+  ws_guard_kernel<<<256, 256, 0, st>>>((unsigned char*)ws, n, batch, lgm_ws_guard_bytes(), check, bad);
+  CK(cudaGetLastError());
+  return 1;
 }
 
 // kernels executed inside graphs on the current device (read back synchronously: stats only)

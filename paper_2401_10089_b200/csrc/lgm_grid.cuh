@@ -16,5 +16,8 @@ int lgm_grid_balance(const double* A, double* B, double* scale, int64_t n, int64
 int lgm_grid_degopt(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int k,
                     int* products, const LgmParams& P, void* ws, cudaStream_t s);
 int lgm_grid_expm(const double* A, double* E, int64_t n, int64_t batch, int64_t ld, void* ws, cudaStream_t s);
+// LGM_WS_GUARD=1: guard band (bytes) after every workspace region / slot (0 otherwise)
+size_t lgm_ws_guard_bytes();
+int lgm_grid_ws_guard(int64_t n, int64_t batch, void* ws, int check, unsigned long long* bad, cudaStream_t s);
 // kernels executed inside Engine G graphs on the current device (synchronous read; stats only)
 unsigned long long lgm_grid_exec_nodes();

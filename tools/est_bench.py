@@ -54,3 +54,5 @@ passes = ps.cpu().numpy()
 gb = passes.sum() * n * n * 8 / 1e9
 print(f"n {n} batch {B} p {p} product {prod}: {ms:.3f} ms per estimate, passes mean {passes.mean():.1f}, "
       f"{gb:.1f} GB streamed -> {gb / (ms * 1e-3):.0f} GB/s")
+if os.environ.get("EST_OUT"):  # bitwise A/B of estimator paths
+    np.savez(os.environ["EST_OUT"], est=est.cpu().numpy(), passes=passes)
