@@ -1,8 +1,8 @@
 #!/bin/bash
 # round-2 measurement session: full GPU suite, bench lines per config, reference arm, ncu
-O=gpurun_out/final; mkdir -p $O
+O=gpurun_out/${1:-final}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=20 > $O/gputest.log 2>&1; echo "rc=$?" >> $O/gputest.log
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=25 > $O/gputest.log 2>&1; echo "rc=$?" >> $O/gputest.log
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_cfg4.jsonl 2> $O/bench_cfg4.err
 for c in 2 3 3b 1; do timeout 900 python bench.py --config $c --steps 20 --warmup 5 >> $O/bench_other.jsonl 2>> $O/bench_other.err; done
 timeout 1200 python bench.py --config 5b --steps 3 --warmup 3 --no-cpu-baseline >> $O/bench_other.jsonl 2>> $O/bench_other.err
