@@ -75,6 +75,15 @@ bool est_cluster_on() {
   return on;
 }
 
+// G3 warp-specialised inverter (gj_inv_ws_kernel) for 256 < n <= 512, n % 64 == 0 (LGM_G3=0/1)
+bool g3_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_G3");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -1306,6 +1315,418 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
       const bool in = j >= col_lo && j < col_hi && !(j >= p2lo && j < p2hi) && !(j >= ex_lo && j < ex_hi);
       if (in) *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// G3: the whole inversion of one job per CTA with warp specialisation (256 < n <= 512,
+// n % 64 == 0).  16 panel warps (P: row `tid` of the current 32-column panel in registers,
+// G1's pivot rule and shift-in-FMA frame) factor pair p+1 while 8 update warps (U) apply pair
+// p's delayed rank-64 update (G2's combined pass: C <- z C + z2 A1 W1 + A2 W2) to the rest of
+// the matrix, 64 x 64 tiles through a 2-stage cp.async pipeline -- so the latency-bound pivot
+// steps run under DMMA work instead of owning an SM, and there is no per-panel launch.  Per pair:
+//   U: wait PANEL_DONE(p) -> form W1 / W2 of pair p -> the tiles of pair p+1's columns ->
+//      arrive NARROW_DONE(p) -> every other tile;
+//   P: wait NARROW_DONE(p) -> factor pair p+1 (P2's stage-1 by P1 as FMA chains, as G2's
+//      untiled panel path) -> arrive PANEL_DONE(p+1).
+// Persistent: gridDim.x CTAs walk the job table.  Named barriers: 1 = P (512), 2 = U (256),
+// 3 = PANEL_DONE (P arrive, U sync), 4 = NARROW_DONE (U arrive, P sync).
+constexpr int G3_THREADS = 768, G3_P = 512, G3_U = 256;
+#ifdef LGM_G3_PROF  // clock64 phase sums (thread 0 of each role): see lgm_debug_g3_cycles
+__device__ unsigned long long g_g3_cyc[8];  // P: wait narrow, panels; U: wait panel, W, narrow tiles, rest tiles
+#define G3T(v) long long v = clock64()
+#define G3ADD(i, a, b) if ((threadIdx.x & (G3_P - 1)) == 0 || threadIdx.x == G3_P) atomicAdd(&g_g3_cyc[i], (unsigned long long)((b) - (a)))
+#define G3SET(a, b) a = b
+#else
+#define G3SET(a, b)
+#define G3T(v)
+#define G3ADD(i, a, b)
+#endif
+constexpr int G3_LDC = 72;  // C tile row stride (conflict-free 16-byte fragment reads)
+constexpr size_t G3_STAGE = (size_t)2 * 64 * LDA_S + 2 * TK * LDB_S + 64 * G3_LDC;  // doubles
+struct G3Smem {
+  double prow[2][40];
+  unsigned wkey32[2][16];
+  double wval[2][16];
+  double red[16];
+  double w1s[32][34];   // P2's stage-1 operand (pivot rows of P1 in P2's columns)
+  double zs[32];        // zero row (A1 operand of P2's pivot rows in the update)
+  int piv_s[64];        // the current pair's pivots
+  int rstep[512];       // rowstep of every row
+  int abort_;           // exact zero pivot: the job stops
+};
+constexpr size_t g3_smem() { return 2 * G3_STAGE * 8; }
+
+__device__ __forceinline__ void g3_bar(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+__device__ __forceinline__ void g3_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+
+// P warps: one 32-column panel [kp, kp+32) of the job (row = tid < n).  s1_kind >= 0: the
+// previous panel's stage-1 update first (multipliers in kind s1_kind); a1_kind >= 0: the
+// output also goes to that multiplier copy.  Returns false on an exact zero pivot.
+__device__ __forceinline__ bool g3_panel(const InvJob& J, int n, int kp, int pofs, int a1_kind, int s1_kind, G3Smem& gs,
+                                         bool& used, double& mypiv, int& my_step) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* Mi = (J.Src && kp < 2 * NB) ? J.Src : J.M;  // out-of-place first pair
+  const bool row_ok = tid < n;
+  double r[32];
+#pragma unroll
+  for (int c = 0; c < 32; c += 2) {
+    double2 v = make_double2(0.0, 0.0);
+    if (row_ok) v = *reinterpret_cast<const double2*>(&Mi[(size_t)tid * n + kp + c]);
+    r[c] = v.x;
+    r[c + 1] = v.y;
+  }
+  if (s1_kind >= 0) {  // r <- z1 r + A1[row] W1[:, this panel] (FMA chains in c1 order)
+    const int p1 = kp - NB;
+    for (int idx = tid; idx < 32 * 32; idx += G3_P) {
+      const int c1 = idx >> 5, c = idx & 31;
+      gs.w1s[c1][c] = Mi[(size_t)J.piv[p1 + c1] * n + kp + c];
+    }
+    g3_bar(1, G3_P);
+    if (row_ok) {
+      const int rs = gs.rstep[tid];
+      if (rs >= p1 && rs < kp) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = 0.0;
+      }
+      const double* a1 = wkind(J, s1_kind) + (size_t)tid * NB;
+#pragma unroll 1
+      for (int c1 = 0; c1 < 32; c1 += 4) {
+        const double2 x01 = *reinterpret_cast<const double2*>(a1 + c1);
+        const double2 x23 = *reinterpret_cast<const double2*>(a1 + c1 + 2);
+        const double av[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const double2 w = *reinterpret_cast<const double2*>(&gs.w1s[c1 + u][c]);
+            r[c] = fma(av[u], w.x, r[c]);
+            r[c + 1] = fma(av[u], w.y, r[c + 1]);
+          }
+      }
+    }
+  }
+  double rowscale = 1.0;
+#pragma unroll 1
+  for (int kk = 0; kk < 32; ++kk) {
+    const int par = kk & 1;
+    const double r0 = r[0];
+    const bool cand = row_ok && !used && r0 != 0.0;
+    const unsigned key = cand ? ((((unsigned)__double2hiint(r0) & 0x7fffffffu) & ~0x3ffu) | (unsigned)(1023 - tid)) : 0u;
+    const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+    const double wv = __shfl_sync(0xffffffffu, r0, (1023 - (int)(wk & 0x3ffu)) & 31);
+    if (lane == 0) {
+      gs.wkey32[par][warp] = wk;
+      gs.wval[par][warp] = wv;
+    }
+    g3_bar(1, G3_P);
+    const unsigned bk = __reduce_max_sync(0xffffffffu, lane < 16 ? gs.wkey32[par][lane] : 0u);
+    if (bk == 0u) return false;  // exact zero pivot (matcore.py:124-125), uniform
+    const int p = 1023 - (int)(bk & 0x3ffu);
+    const double rp = lgm_rcp(gs.wval[par][p >> 5]);
+    const bool own = (tid == p);
+    if (own) {
+      used = true;
+      mypiv = r0;
+      rowscale = rp;
+      double* pw = gs.prow[par];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
+      my_step = kp + kk;
+      gs.piv_s[pofs + kk] = tid;
+      gs.rstep[tid] = kp + kk;
+    }
+    g3_bar(1, G3_P);
+    const double g = own ? 0.0 : r0 * rp;
+    const double last = own ? 1.0 : -g;
+    const double* pr = gs.prow[par];
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
+      if (c > 0) r[c - 1] = fma(-g, p2.x, r[c]);
+      r[c] = fma(-g, p2.y, r[c + 1]);
+    }
+    r[31] = last;
+  }
+  if (my_step >= kp && my_step < kp + 32) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] *= rowscale;
+  }
+  if (row_ok) {
+#pragma unroll
+    for (int c = 0; c < 32; c += 2)
+      *reinterpret_cast<double2*>(&J.M[(size_t)tid * n + kp + c]) = make_double2(r[c], r[c + 1]);
+    if (a1_kind >= 0) {
+      double* A1 = wkind(J, a1_kind) + (size_t)tid * NB;
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(A1 + c) = make_double2(r[c], r[c + 1]);
+    }
+  }
+  if (tid < 32) J.piv[kp + tid] = gs.piv_s[pofs + tid];
+  g3_bar(1, G3_P);  // P1's outputs (global, piv_s) before P2's stage-1 reads them
+  return true;
+}
+
+__global__ void __launch_bounds__(G3_THREADS, 1) gj_inv_ws_kernel(const InvJob* jobs, int nj, int n) {
+  extern __shared__ __align__(16) double g3sm[];
+  __shared__ __align__(16) G3Smem gs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool is_p = tid < G3_P;
+  const int npairs = n / (2 * NB);
+  for (int jb = blockIdx.x; jb < nj; jb += gridDim.x) {
+    const InvJob J = jobs[jb];
+    if (!J.M) continue;  // unused slot of the device-built job table (uniform)
+    for (int i = tid; i < 512; i += G3_THREADS) gs.rstep[i] = i < n ? -1 : 0x3fffffff;
+    if (tid < 32) gs.zs[tid] = 0.0;
+    if (tid == 0) gs.abort_ = 0;
+    __syncthreads();
+    if (is_p) {
+      // ================================================================ P warps
+      bool used = false;
+      double mypiv = 1.0;
+      int my_step = -1;
+      bool ok = true;
+      for (int pp = 0; pp < npairs && ok; ++pp) {
+        const int kp = pp * 2 * NB, q = pp & 1;
+        G3T(ta);
+        if (pp > 0) g3_bar(4, G3_THREADS);  // NARROW_DONE(pp - 1): this pair's columns are updated
+        G3T(tb);
+        ok = g3_panel(J, n, kp, 0, 3 * q + 2, -1, gs, used, mypiv, my_step) &&
+             g3_panel(J, n, kp + NB, NB, -1, 3 * q + 2, gs, used, mypiv, my_step);
+        G3T(tc);
+        G3ADD(0, ta, tb);
+        G3ADD(1, tb, tc);
+        if (!ok && tid == 0) gs.abort_ = 1;
+        __threadfence_block();
+        g3_arrive(3, G3_THREADS);  // PANEL_DONE(pp)
+      }
+      // publish rowstep, log|det| (warp-order CTA sum over the P warps)
+      if (tid < n) J.rowstep[tid] = my_step;
+      double lg = my_step >= 0 ? log(fabs(mypiv)) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lg += __shfl_xor_sync(0xffffffffu, lg, o);
+      if (lane == 0) gs.red[warp] = lg;
+      g3_bar(1, G3_P);
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 16; ++w) t += gs.red[w];
+        *J.logdet = t;
+        *J.status = ok ? 0 : 1;
+      }
+    } else {
+      // ================================================================ U warps
+      const int ut = tid - G3_P, uw = ut >> 5;  // 0..255, warp 0..7
+      const int g = lane >> 2, t = lane & 3;
+      for (int pp = 0; pp < npairs; ++pp) {
+        G3T(ua);
+        g3_bar(3, G3_THREADS);  // PANEL_DONE(pp)
+        G3T(ub);
+        G3ADD(2, ua, ub);
+        if (*(volatile int*)&gs.abort_) break;
+        const int k0 = pp * 2 * NB, q = pp & 1;
+        const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
+        const bool next = pp + 1 < npairs;
+        const int kn = k0 + 2 * NB;
+        double* W1 = wkind(J, 3 * q);
+        double* W2 = wkind(J, 3 * q + 1);
+        const double* A1 = wkind(J, 3 * q + 2);
+        // ---- W1 / W2 of this pair (gj_w2_mma_kernel's arithmetic), two 64-column blocks at a time
+        {
+          double* a1s = g3sm;                  // [32][LDA_S]
+          double* w1s = a1s + 32 * LDA_S;      // [2][32][LDB_S]
+          for (int idx = ut; idx < NB * NB; idx += G3_U) {
+            const int c = idx >> 5, cc = idx & 31;
+            a1s[c * LDA_S + cc] = A1[(size_t)gs.piv_s[NB + c] * NB + cc];
+          }
+          const int half = uw >> 2, wc = (uw & 3) * 16;
+          for (int jb2 = 0; jb2 < n; jb2 += 128) {
+            for (int idx = ut; idx < 2 * NB * 32; idx += G3_U) {  // W1 rows of both blocks, 16-byte chunks
+              const int h = idx / (NB * 32), rem = idx - h * (NB * 32);
+              const int cc = rem >> 5, jj = (rem & 31) * 2, j = jb2 + h * 64 + jj;
+              if (j >= n) continue;  // n % 128 == 64: the last pair of blocks has one
+              const double* Ms = (J.Src && k0 == 0 && j >= 2 * NB) ? J.Src : J.M;
+              double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)gs.piv_s[cc] * n + j]);
+              if (j >= k0 && j < k0 + NB) v = make_double2(0.0, 0.0);
+              *reinterpret_cast<double2*>(&w1s[(h * 32 + cc) * LDB_S + jj]) = v;
+              *reinterpret_cast<double2*>(&W1[(size_t)cc * n + j]) = v;
+            }
+            g3_bar(2, G3_U);
+            const int j0 = jb2 + half * 64;
+            const double* wsh = w1s + half * 32 * LDB_S;
+            if (j0 < n) {  // (warp-uniform)
+            double acc[4][2][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) {
+                const int jc = j0 + wc + ni * 8 + 2 * t;
+                const double* Ms = (J.Src && k0 == 0 && jc >= 2 * NB) ? J.Src : J.M;
+                const double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)gs.piv_s[NB + mi * 8 + g] * n + jc]);
+                acc[mi][ni][0] = v.x;
+                acc[mi][ni][1] = v.y;
+              }
+#pragma unroll
+            for (int k = 0; k < NB; k += 4) {
+              double a[4], b[2];
+#pragma unroll
+              for (int mi = 0; mi < 4; ++mi) a[mi] = a1s[(mi * 8 + g) * LDA_S + k + t];
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) b[ni] = wsh[(k + t) * LDB_S + wc + ni * 8 + g];
+#pragma unroll
+              for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+              const int c = mi * 8 + g;
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) {
+                const int j = j0 + wc + ni * 8 + 2 * t;
+                double2 v = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+                if (j >= k0 && j < k0 + NB) v = make_double2(a1s[c * LDA_S + j - k0], a1s[c * LDA_S + j + 1 - k0]);
+                else if (j >= k0 + NB && j < k0 + 2 * NB) v = make_double2(0.0, 0.0);
+                *reinterpret_cast<double2*>(&W2[(size_t)c * n + j]) = v;
+              }
+            }
+            }
+            g3_bar(2, G3_U);  // w1s reused by the next blocks
+          }
+          __threadfence_block();
+          g3_bar(2, G3_U);  // W1 / W2 (global) complete before the tiles read them
+        }
+        G3T(uc);
+        G3ADD(3, ub, uc);
+        // ---- the combined rank-64 update, 64 x 64 tiles: next pair's columns first
+        const int nrb = n / 64, nct = n / 64;
+        const int cx_next = next ? kn / 64 : -1;
+        const int ntile = next ? nrb * nct : nrb * nct;  // every (rb, cx); next pair's column first
+        auto tile_of = [&](int i, int& rb, int& cx) {
+          if (next) {
+            if (i < nrb) { rb = i; cx = cx_next; return; }
+            const int r = i - nrb;  // the remaining (nct - 1) columns
+            rb = r / (nct - 1);
+            const int c = r - rb * (nct - 1);
+            cx = c < cx_next ? c : c + 1;
+          } else {
+            rb = i / nct;
+            cx = i - rb * nct;
+          }
+        };
+        const int nt = next ? nrb * nct : nrb * nct;
+        (void)ntile;
+        auto issue = [&](int i, int stg) {
+          int rb, cx;
+          tile_of(i, rb, cx);
+          double* S = g3sm + stg * G3_STAGE;
+          double* As1 = S;
+          double* As2 = As1 + 64 * LDA_S;
+          double* Bs1 = As2 + 64 * LDA_S;
+          double* Bs2 = Bs1 + TK * LDB_S;
+          double* Cs = Bs2 + TK * LDB_S;
+          const int row0 = rb * 64, col0 = cx * 64;
+          for (int idx = ut; idx < 64 * (TK / 2); idx += G3_U) {
+            const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
+            cp_async16(&As1[r * LDA_S + c], &A1[(size_t)(row0 + r) * NB + c]);
+            cp_async16(&As2[r * LDA_S + c], &J.M[(size_t)(row0 + r) * n + p2lo + c]);
+          }
+          for (int idx = ut; idx < TK * 32; idx += G3_U) {
+            const int c = idx >> 5, jj = (idx & 31) * 2;
+            cp_async16(&Bs1[c * LDB_S + jj], &W1[(size_t)c * n + col0 + jj]);
+            cp_async16(&Bs2[c * LDB_S + jj], &W2[(size_t)c * n + col0 + jj]);
+          }
+          for (int idx = ut; idx < 64 * 32; idx += G3_U) {
+            const int r = idx >> 5, jj = (idx & 31) * 2, j = col0 + jj;
+            const double* Csrc = (J.Src && k0 == 0 && j >= 2 * NB) ? J.Src : J.M;
+            cp_async16(&Cs[r * G3_LDC + jj], &Csrc[(size_t)(row0 + r) * n + j]);
+          }
+          asm volatile("cp.async.commit_group;\n" ::);
+        };
+        const int lr0 = (uw >> 2) * 32, lc0 = (uw & 3) * 16;
+        issue(0, 0);
+        for (int i = 0; i < nt; ++i) {
+          if (i + 1 < nt) {
+            issue(i + 1, (i + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+          } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+          }
+          g3_bar(2, G3_U);
+          int rb, cx;
+          tile_of(i, rb, cx);
+          const double* S = g3sm + (i & 1) * G3_STAGE;
+          const double* As1 = S;
+          const double* As2 = As1 + 64 * LDA_S;
+          const double* Bs1 = As2 + 64 * LDA_S;
+          const double* Bs2 = Bs1 + TK * LDB_S;
+          const double* Cs = Bs2 + TK * LDB_S;
+          const int r0 = rb * 64 + lr0, c0 = cx * 64 + lc0;
+          double acc[4][2][2];
+          const double* aptr[4];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const int rs = gs.rstep[r0 + mi * 8 + g];
+            const bool z1 = !(rs >= p1lo && rs < p2lo), z2 = !(rs >= p2lo && rs < p2hi);
+            aptr[mi] = z2 ? As1 + (lr0 + mi * 8 + g) * LDA_S : gs.zs;
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) {
+              const int j = c0 + ni * 8 + 2 * t;
+              const bool keep = (j >= p1lo && j < p2lo) ? z2 : (z1 && z2);
+              const double2 v = *reinterpret_cast<const double2*>(&Cs[(lr0 + mi * 8 + g) * G3_LDC + lc0 + ni * 8 + 2 * t]);
+              acc[mi][ni][0] = keep ? v.x : 0.0;
+              acc[mi][ni][1] = keep ? v.y : 0.0;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < TK; k += 4) {  // + z2 A1 W1
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = aptr[mi][k + t];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs1[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          }
+#pragma unroll
+          for (int k = 0; k < TK; k += 4) {  // + A2 W2
+            double a[4], b[2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As2[(lr0 + mi * 8 + g) * LDA_S + k + t];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) b[ni] = Bs2[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          }
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const int ii = r0 + mi * 8 + g;
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) {
+              const int j = c0 + ni * 8 + 2 * t;
+              if (!(j >= p2lo && j < p2hi))
+                *reinterpret_cast<double2*>(&J.M[(size_t)ii * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+            }
+          }
+          if (next && i == nrb - 1) {  // the next pair's columns are complete
+            __threadfence_block();
+            g3_bar(2, G3_U);
+            g3_arrive(4, G3_THREADS);  // NARROW_DONE(pp)
+            G3T(ud);
+            G3ADD(4, uc, ud);
+            G3SET(uc, ud);
+          } else {
+            g3_bar(2, G3_U);  // stage (i & 1) is refilled at i + 2
+          }
+        }
+        G3T(ue);
+        G3ADD(5, uc, ue);
+      }
+    }
+    __syncthreads();  // job end: every role done (the next job reuses the shared state)
   }
 }
 
@@ -3992,6 +4413,13 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
     if (n <= 256) return launch_g1<256>(C, st, nj);
     return launch_g1<512>(C, st, nj);
   }
+  if (g3_on() && n > 256 && n <= 512 && n % (2 * NB) == 0) {  // one warp-specialised CTA per job
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GL gj_inv_ws_kernel<<<std::min(nj, sms), G3_THREADS, g3_smem(), st>>>(d_jobs, nj, n);
+    return 0;
+  }
   cudaStream_t sB = C.side(st);
   cudaEvent_t evN = C.evN, evP = C.evP;
   GL gj_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(d_jobs, n);
@@ -4425,6 +4853,7 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_panel_pair_kernel<512>, mx, 16 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
+  CK(cudaFuncSetAttribute(gj_inv_ws_kernel, mx, (int)g3_smem()));
   CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(expm_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
@@ -4644,6 +5073,20 @@ unsigned long long lgm_grid_exec_nodes() {
   unsigned long long v = 0;
   if (cudaMemcpyFromSymbol(&v, g_exec_nodes, sizeof(v)) != cudaSuccess) return 0;
   return v;
+}
+
+extern "C" int lgm_debug_g3_cycles(unsigned long long* out, int reset) {
+#ifdef LGM_G3_PROF
+  cudaMemcpyFromSymbol(out, g_g3_cyc, sizeof(g_g3_cyc));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_g3_cyc, z, sizeof(z));
+  }
+  return 8;
+#else
+  (void)out; (void)reset;
+  return 0;
+#endif
 }
 
 extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
