@@ -20,8 +20,8 @@
  * stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream): they
  * never block the host (n > 64 runs as one CUDA graph whose loops are device-side
  * conditional nodes).  No hidden device allocation: scratch comes from the caller's
- * `workspace` (lgm_workspace_bytes / lgm_block_workspace_bytes; none is needed by the
- * building blocks for n <= 64).  Argument / launch errors are returned synchronously
+ * `workspace` (lgm_workspace_bytes / lgm_block_workspace_bytes; the n <= 64 building
+ * blocks other than lgm_eval_degopt_f64 with k > 5 and lgm_expm_ref_f64 ignore it).  Argument / launch errors are returned synchronously
  * (< 0).  Per-matrix numerical outcomes are reported per matrix through status
  * codes (LGM_OK ... LGM_NONFINITE), which the Python layer maps onto the
  * reference's exceptions (exceptions.py:6-18); a failed matrix's L is all NaN.
@@ -51,7 +51,7 @@ enum {
   LGM_DB_NOCONV = 2,       /* DB maxiter / collapse     -> ConvergenceError   (sqrtm.py:69-78)    */
   LGM_SCALING_MAXITER = 3, /* s reached opts.maxiter_s  -> ConvergenceError       */
   LGM_NONFINITE = 4,       /* NaN/Inf input or iterate  -> ValueError         (matcore.py:64-65)  */
-  LGM_SPECTRUM = 5         /* set by the host-side eig_small pre-check when enabled  */
+  LGM_SPECTRUM = 5         /* set by the eig_small pre-check (lgm_spectrum_check_f64) when enabled */
 };
 
 /* call-level errors (return values) */
@@ -63,7 +63,7 @@ enum {
 };
 
 typedef struct lgm_opts {
-  int32_t max_k;      /* highest scheme index, 1..5 (shipped coefficients)       default 5  */
+  int32_t max_k;      /* highest scheme index: 1..5 shipped, 6..9 generated      default 5  */
   int32_t maxiter_s;  /* square-root cap (LogmOptions.maxiter)       default 40 */
   int32_t db_maxiter; /* sqrt_db maxiter (sqrtm.py:27)                            default 50 */
   int32_t est_itmax;  /* est_power_norm itmax (matcore.py:300)                    default 5  */
@@ -93,11 +93,12 @@ typedef struct lgm_report { /* per matrix, written to device memory */
 
 void lgm_default_opts(lgm_opts* opts);
 
-/* Workspace the caller must provide to lgm_logm_f64: 4 n^2 doubles per matrix for the
- * fused n <= 64 path (polynomial nodes, A_I2), the Engine G slots and tables beyond. */
+/* Workspace the caller must provide to lgm_logm_f64: 8 n^2 doubles per matrix for the
+ * fused n <= 64 path (polynomial nodes P4..P10, A_prev / A_I2), the Engine G slots and
+ * tables beyond (both + guard bands under LGM_WS_GUARD=1, see lgm_debug_ws_guard). */
 int lgm_workspace_bytes(int64_t n, int64_t batch, size_t* bytes);
 
-/* Workspace of the building blocks below (0 for n <= 64). */
+/* Workspace of the building blocks below (sized for the graph path at every n). */
 int lgm_block_workspace_bytes(int64_t n, int64_t batch, size_t* bytes);
 
 /* Largest n handled by the fused one-CTA-per-matrix engine. */
@@ -147,6 +148,14 @@ int lgm_spectrum_check_f64(const double* A, int32_t* flags_dev, int64_t n, int64
                            void* workspace, size_t workspace_bytes, lgm_stream_t stream);
 
 const char* lgm_status_string(int code);
+
+/* Diagnostics, not part of the reference interface.  With LGM_WS_GUARD=1 in the environment
+ * (read once per process) every workspace region and n x n slot is followed by a guard band;
+ * check = 0 fills the bands of `workspace` (layout 1: lgm_logm_f64 with n <= 64, 0: every
+ * other workspace), check = 1 adds the number of changed guard bytes to *bad_dev (device
+ * uint64).  Returns 1 if done, 0 if guards are off, < 0 on error. */
+int lgm_debug_ws_guard(int64_t n, int64_t batch, int layout, void* workspace, int check,
+                       unsigned long long* bad_dev, lgm_stream_t stream);
 
 /* Number of CUDA kernels this library has launched so far (process-wide, monotonic):
  * direct launches plus the kernels executed inside Engine G graphs (counted on the device;
