@@ -86,7 +86,8 @@ typedef struct lgm_report { /* per matrix, written to device memory */
   int32_t balance_sweeps;
   int32_t db_plateau;        /* DB stop tests taken with rel in [tol/10, 10 tol]: the    */
                              /* iteration count is rounding-noise dependent */
-  int32_t reserved;
+  int32_t inv_skipped;       /* DB X-inversions not executed: a root's last iteration needs */
+                             /* only Y^-1 (its Y' is discarded), taken when predicted       */
   double alpha_used;         /* alpha certifying k (<= Theta_k on success)          */
   double min_margin;         /* min |x - thr| / |thr| over every discrete decision  */
 } lgm_report;

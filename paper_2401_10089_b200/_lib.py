@@ -35,7 +35,7 @@ class Opts(ctypes.Structure):
 REPORT_DTYPE = np.dtype([("status", "<i4"), ("s", "<i4"), ("k", "<i4"), ("db_iters", "<i4"),
                          ("products", "<i4"), ("divisions", "<i4"), ("estimation_passes", "<i4"),
                          ("norm_estimations", "<i4"), ("balanced", "<i4"), ("balance_sweeps", "<i4"),
-                         ("db_plateau", "<i4"), ("reserved", "<i4"), ("alpha_used", "<f8"), ("min_margin", "<f8")])
+                         ("db_plateau", "<i4"), ("inv_skipped", "<i4"), ("alpha_used", "<f8"), ("min_margin", "<f8")])
 assert REPORT_DTYPE.itemsize == 64
 
 _lib = None

@@ -84,6 +84,23 @@ bool g3_on() {
   return on;
 }
 
+// Lazy X^-1 on predicted-last DB iterations (LGM_LAZYX=0 disables; LGM_LAZYX_F = prediction
+// factor f: predict when rel <= f sqrt(tol))
+bool lazyx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_LAZYX");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+double lazyx_f() {
+  static const double v = [] {
+    const char* e = std::getenv("LGM_LAZYX_F");
+    return e ? std::atof(e) : 1.0;
+  }();
+  return v;
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -2203,6 +2220,34 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
   if (threadIdx.x == 0) { sweeps_out[b] = sweeps; margin[b] = s_mm; }
 }
 
+__device__ unsigned long long g_exec_nodes;  // kernel nodes executed inside graphs (lgm_launch_count)
+
+__device__ __forceinline__ void count_nodes(int nodes) {
+  if (threadIdx.x == 0) atomicAdd(&g_exec_nodes, (unsigned long long)nodes);
+}
+
+// per-matrix Algorithm-1 state (oracle/driver.py _State + the running root / request)
+static_assert(2 * 14 + 2 <= 32, "estimate cache covers powers up to m_K + 1");
+struct MDev {
+  int status, s, db_iters, nest, passes, products, k, plateau, sweeps;
+  int finish, have_ai2, post_fail;
+  int dbit, dbst, dbplat;           // running square root: iterations, status, plateau tests
+  int dbpred;                       // this iteration is predicted to be the root's last (lazy X^-1)
+  int dbskip;                       // X inversions skipped by the lazy order (whole call)
+  int jcur, max_in;                 // select sweep
+  int am, need1, need2, adone;      // alpha request (power m) and its progress
+  unsigned cvalid;                  // estimate cache validity bits, by power
+  double dbmm;                      // running root's margin
+  double th, t1, Pm, t2, aout;      // alpha request threshold and terms
+  double alpha_loop, mm, nA, nI2, cert, cert_max;
+  double cache[32];  // estimates by power m (<= m_K + 1 = 29 with k = 9)
+  __device__ void note(double x, double thr) {
+    const double d = fabs(thr);
+    mm = fmin(mm, d > 0 ? fabs(x - thr) / d : fabs(x - thr));
+  }
+  __device__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
+};
+
 // ------------------------------------------------------------------------------------------
 // Scaled DB update (sqrtm.py:57-67) fused with the column sums of |X'-X| and |X'|.
 struct DbArgs {
@@ -2220,6 +2265,8 @@ struct DbArgs {
   double* size;
   const int* istat;    // [2][b] singular flags of this iteration's X / Y inversions
   int batch;
+  MDev* ms;            // dbpred: X' goes to slot xn_slot, Y is left for the fix-up (lazy X^-1)
+  int xn_slot;
 };
 
 __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
@@ -2229,6 +2276,44 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   if (a.istat[b] || (!a.first && a.istat[a.batch + b])) return;  // singular iterate: X, Y kept
+  if (!a.first && a.ms[b].dbpred) {  // predicted last iteration: X' (no X^-1 needed) to a spare slot
+    const double* X = a.S.buf(b, G_B);
+    double* Xn = a.S.buf(b, a.xn_slot);
+    const double* RY = a.S.buf(b, G_YI);
+    const int* yp = a.ypiv + (size_t)b * n;
+    const int qyc = a.ystep[(size_t)b * n + c];
+    double mu = 1.0;
+    if (a.scaling[b]) mu = fmin(fmax(exp(-(a.xlog[b] + a.ylog[b]) / (2.0 * n)), LGM_MU_MIN), LGM_MU_MAX);
+    const double inv_mu = 1.0 / mu;
+    double dsum = 0.0, ssum = 0.0;
+    constexpr int U = 8;
+    int r = 0;
+    for (; r + U <= n; r += U) {
+      double yi[U], xo[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        yi[u] = RY[(size_t)yp[r + u] * n + qyc];
+        xo[u] = X[(size_t)(r + u) * n + c];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double xn = 0.5 * (mu * xo[u] + yi[u] * inv_mu);
+        Xn[(size_t)(r + u) * n + c] = xn;
+        dsum = (r + u == 0) ? fabs(xn - xo[u]) : dsum + fabs(xn - xo[u]);
+        ssum = (r + u == 0) ? fabs(xn) : ssum + fabs(xn);
+      }
+    }
+    for (; r < n; ++r) {
+      const double xo = X[(size_t)r * n + c];
+      const double xn = 0.5 * (mu * xo + RY[(size_t)yp[r] * n + qyc] * inv_mu);
+      Xn[(size_t)r * n + c] = xn;
+      dsum = (r == 0) ? fabs(xn - xo) : dsum + fabs(xn - xo);
+      ssum = (r == 0) ? fabs(xn) : ssum + fabs(xn);
+    }
+    atomic_max_nonneg(&a.change[b], dsum);
+    atomic_max_nonneg(&a.size[b], ssum);
+    return;
+  }
   double* X = a.S.buf(b, G_B);
   double* Y = a.S.buf(b, G_Y);
   const double* RX = a.S.buf(b, G_XI);
@@ -2281,6 +2366,39 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   }
   atomic_max_nonneg(&a.change[b], dsum);
   atomic_max_nonneg(&a.size[b], ssum);
+}
+
+// Lazy X^-1 fix-up (matrices of LS_PMISS: predicted last, not converged): Y' from the X^-1 just
+// formed (db_update_kernel's formula), X <- X' from the spare slot.  An exactly singular X
+// ends the root as the eager order would have (status SINGULAR, that iteration not counted).
+__global__ void __launch_bounds__(128) db_fix_kernel(DbArgs a, int nodes) {
+  if (blockIdx.x == 0 && blockIdx.y == 0) count_nodes(nodes);
+  if (blockIdx.y >= *a.L.cnt) return;
+  const int b = a.L.ids[blockIdx.y];
+  const int n = a.S.n;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.istat[b]) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.ms[b].dbst = LGM_SINGULAR;
+      a.ms[b].dbit -= 1;
+    }
+    return;
+  }
+  if (c >= n) return;
+  double* X = a.S.buf(b, G_B);
+  double* Y = a.S.buf(b, G_Y);
+  const double* Xn = a.S.buf(b, a.xn_slot);
+  const double* RX = a.S.buf(b, G_XI);
+  const int* xp = a.xpiv + (size_t)b * n;
+  const int qxc = a.xstep[(size_t)b * n + c];
+  double mu = 1.0;
+  if (a.scaling[b]) mu = fmin(fmax(exp(-(a.xlog[b] + a.ylog[b]) / (2.0 * n)), LGM_MU_MIN), LGM_MU_MAX);
+  const double inv_mu = 1.0 / mu;
+  for (int r = 0; r < n; ++r) {
+    const size_t e = (size_t)r * n + c;
+    Y[e] = 0.5 * (mu * Y[e] + RX[(size_t)xp[r] * n + qxc] * inv_mu);
+    X[e] = Xn[e];
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -3011,29 +3129,11 @@ __global__ void __launch_bounds__(128) gemm_comb_kernel(Slots S, DList DL, CombS
 
 enum {
   LS_ALL = 0, LS_LIVE, LS_ACT, LS_ACTAI2, LS_ROOTS, LS_DB, LS_OK, LS_SEL, LS_NEED, LS_NEEDAI2, LS_CUR, LS_FAILED,
+  LS_POK, LS_PMISS,           // lazy X inverse: predicted-last iterations that stopped / continue
   LS_POLY0,                   // LS_POLY0 + j, j = 1..K_MAX-1: selected matrices with k > j
   LS_N = LS_POLY0 + LGM_K_MAX
 };
 
-// per-matrix Algorithm-1 state (oracle/driver.py _State + the running root / request)
-static_assert(2 * 14 + 2 <= 32, "estimate cache covers powers up to m_K + 1");
-struct MDev {
-  int status, s, db_iters, nest, passes, products, k, plateau, sweeps;
-  int finish, have_ai2, post_fail;
-  int dbit, dbst, dbplat;           // running square root: iterations, status, plateau tests
-  int jcur, max_in;                 // select sweep
-  int am, need1, need2, adone;      // alpha request (power m) and its progress
-  unsigned cvalid;                  // estimate cache validity bits, by power
-  double dbmm;                      // running root's margin
-  double th, t1, Pm, t2, aout;      // alpha request threshold and terms
-  double alpha_loop, mm, nA, nI2, cert, cert_max;
-  double cache[32];  // estimates by power m (<= m_K + 1 = 29 with k = 9)
-  __device__ void note(double x, double thr) {
-    const double d = fabs(thr);
-    mm = fmin(mm, d > 0 ? fabs(x - thr) / d : fabs(x - thr));
-  }
-  __device__ bool le(double x, double thr) { note(x, thr); return x <= thr; }
-};
 
 // per-call pointers and parameters (the graph's kernels read them from the workspace)
 struct CallDesc {
@@ -3229,11 +3329,6 @@ __device__ int blk_append(bool pred, int* s_w, int& off) {
 
 __device__ __forceinline__ double dpow(double x, double y) { return pow(x, y); }
 
-__device__ unsigned long long g_exec_nodes;  // kernel nodes executed inside graphs (lgm_launch_count)
-
-__device__ __forceinline__ void count_nodes(int nodes) {
-  if (threadIdx.x == 0) atomicAdd(&g_exec_nodes, (unsigned long long)nodes);
-}
 
 // Device-side phase timer (diagnostics: lgm_debug_grid_phase_ns): every decide kernel charges
 // the globaltimer interval since the previous mark to the phase that just ended.  One stream
@@ -3474,7 +3569,7 @@ __global__ void __launch_bounds__(CT) decide_roots_kernel(Ctl c) {
       M.alpha_loop = M.aout;
       M.finish = M.le(M.aout, thK);
       r = !M.finish;
-      if (r) { M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbmm = INFINITY; c.scaling[b] = 1; }
+      if (r) { M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbpred = 0; M.dbmm = INFINITY; c.scaling[b] = 1; }
     }
     const int pos = blk_append(r, s_w, off);
     if (r) c.ids(LS_ROOTS)[pos] = b;
@@ -3524,36 +3619,54 @@ __global__ void __launch_bounds__(CT) decide_post_kernel(Ctl c, cudaGraphConditi
 }
 
 // ------------------------------------------------------------------ DB square root (sqrtm.py:27-78)
-// Job table for this iteration: X of every DB-active matrix, then (it > 1) Y; unused slots
-// carry M = nullptr and the always-1 status.  Also zeroes the per-iteration accumulators.
+// Job table for this iteration: X of every DB-active matrix (except those whose iteration is
+// predicted to be the root's last: their X^-1 is formed later only if needed), then (it > 1)
+// Y; unused slots carry M = nullptr and the always-1 status.  Also zeroes the per-iteration
+// accumulators.
+__device__ InvJob make_job(const Ctl& c, int b, int w, int oop) {
+  InvJob J{};
+  J.M = c.S.buf(b, w ? G_YI : G_XI);
+  J.Src = oop ? c.S.buf(b, w ? G_Y : G_B) : nullptr;
+  J.piv = c.piv + ((size_t)w * c.batch + b) * c.n;
+  J.rowstep = c.step + ((size_t)w * c.batch + b) * c.n;
+  J.Wb = c.W + ((size_t)w * c.batch + b) * NB * c.n;
+  J.wst = (long long)2 * c.batch * NB * c.n;
+  J.logdet = c.logdet + w * c.batch + b;
+  J.status = c.istat + w * c.batch + b;
+  return J;
+}
+__device__ InvJob null_job(const Ctl& c) {
+  InvJob J{};
+  J.M = nullptr;
+  J.status = c.dead;
+  return J;
+}
 __global__ void __launch_bounds__(CT) build_jobs_kernel(Ctl c, int first, int oop) {
+  __shared__ int s_w[33];
   const int na = c.cnt[LS_DB];
-  const int nj = first ? na : 2 * na;
   const int cap = first ? c.batch : 2 * c.batch;
-  for (int q = threadIdx.x; q < cap; q += CT) {
-    InvJob J{};
-    if (q < nj) {
-      const int w = q < na ? 0 : 1;
-      const int b = c.ids(LS_DB)[w ? q - na : q];
-      J.M = c.S.buf(b, w ? G_YI : G_XI);
-      J.Src = oop ? c.S.buf(b, w ? G_Y : G_B) : nullptr;
-      J.piv = c.piv + ((size_t)w * c.batch + b) * c.n;
-      J.rowstep = c.step + ((size_t)w * c.batch + b) * c.n;
-      J.Wb = c.W + ((size_t)w * c.batch + b) * NB * c.n;
-      J.wst = (long long)2 * c.batch * NB * c.n;
-      J.logdet = c.logdet + w * c.batch + b;
-      J.status = c.istat + w * c.batch + b;
-      if (w == 0) {
-        c.change[b] = 0.0;
-        c.size[b] = 0.0;
-        if (first) c.logdet[c.batch + b] = 0.0;
-      }
-    } else {
-      J.M = nullptr;
-      J.status = c.dead;
+  int off = 0;
+  FOR_LIST(c, LS_DB)
+    const bool px = b >= 0 && !first && c.ms[b].dbpred;  // predicted last: no X inverse now
+    const bool want = b >= 0 && !px;
+    const int pos = blk_append(want, s_w, off);
+    if (want) c.jobs[pos] = make_job(c, b, 0, oop);
+    if (b >= 0) {
+      c.change[b] = 0.0;
+      c.size[b] = 0.0;
+      if (first) c.logdet[c.batch + b] = 0.0;
+      if (px) c.istat[b] = 0;
     }
-    c.jobs[q] = J;
   }
+  const int nj = first ? off : off + na;
+  for (int e = threadIdx.x; !first && e < na; e += CT) c.jobs[off + e] = make_job(c, c.ids(LS_DB)[e], 1, oop);
+  for (int q = nj + threadIdx.x; q < cap; q += CT) c.jobs[q] = null_job(c);
+}
+
+// lazy X^-1, second phase: X jobs of the predicted-last matrices that did not converge
+__global__ void __launch_bounds__(CT) build_jobs_px_kernel(Ctl c, int oop) {
+  const int nm = c.cnt[LS_PMISS];
+  for (int q = threadIdx.x; q < c.batch; q += CT) c.jobs[q] = q < nm ? make_job(c, c.ids(LS_PMISS)[q], 0, oop) : null_job(c);
 }
 
 // sqrt_db building block: every live matrix takes one root
@@ -3562,7 +3675,7 @@ __global__ void __launch_bounds__(CT) decide_db_start_kernel(Ctl c) {
   for (int e = threadIdx.x; e < na; e += CT) {
     const int b = c.ids(LS_LIVE)[e];
     MDev& M = c.ms[b];
-    M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbmm = INFINITY;
+    M.dbit = 0; M.dbst = 0; M.dbplat = 0; M.dbpred = 0; M.dbmm = INFINITY;
     c.scaling[b] = 1;
     c.ids(LS_ROOTS)[e] = b;
     c.ids(LS_DB)[e] = b;
@@ -3571,8 +3684,13 @@ __global__ void __launch_bounds__(CT) decide_db_start_kernel(Ctl c) {
 }
 
 // stop test of the iteration just done (sqrtm.py:66-78), mu switch, next DB list
+// Lazy X^-1: when an unscaled iteration's rel is below pred_f * sqrt(tol) the next one is
+// predicted to converge, so its X^-1 (needed only for Y', which a converged root discards) is
+// deferred: db_update forms X' from Y^-1 alone; a converged root keeps X' (LS_POK); otherwise
+// (LS_PMISS) the IF body h2 inverts X and completes Y'.  Bit-identical to the eager order.
 __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphConditionalHandle h, int nodes, int first,
-                                                        int block_mode) {
+                                                        int block_mode, cudaGraphConditionalHandle h2, int lazy,
+                                                        double pred_f) {
   __shared__ int s_w[33];
   phase_mark(PH_DB);
   const CallDesc& D = *c.desc;
@@ -3580,11 +3698,13 @@ __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphCondition
   const double tol_in = block_mode ? D.tol : D.P.db_tol;
   const int maxiter = block_mode ? D.maxiter : D.P.db_maxiter;
   const double tol = tol_in > 0.0 ? tol_in : 10.0 * n * LGM_UNIT_ROUNDOFF;
-  int off = 0;
+  int off = 0, offk = 0, offm = 0;
   FOR_LIST(c, LS_DB)
-    bool next = false;
-    if (b >= 0) {
+    bool next = false, pok = false, pmiss = false;
+    if (b >= 0 && c.ms[b].dbst == 0) {  // (a singular X met by the last fix-up ends the root)
       MDev& M = c.ms[b];
+      const bool px = !first && M.dbpred;
+      M.dbpred = 0;
       const int it = ++M.dbit;
       const bool sing = c.istat[b] || (!first && c.istat[c.batch + b]);
       const double ch = c.change[b], sz = c.size[b];
@@ -3606,14 +3726,27 @@ __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphCondition
           if (it == maxiter) M.dbst = LGM_DB_NOCONV;
           else next = true;
         }
+        if (lazy && next && !c.scaling[b] && rel <= pred_f * sqrt(tol)) M.dbpred = 1;
+      }
+      if (px) {
+        pmiss = next;   // X^-1 and Y' still needed
+        pok = !next;    // the root stops: X <- X'
+        if (pok) M.dbskip++;
       }
     }
     const int pos = blk_append(next, s_w, off);
     if (next) c.ids(LS_DB)[pos] = b;  // in place: pos <= e_, ascending, read before written
+    const int pk = blk_append(pok, s_w, offk);
+    if (pok) c.ids(LS_POK)[pk] = b;
+    const int pm = blk_append(pmiss, s_w, offm);
+    if (pmiss) c.ids(LS_PMISS)[pm] = b;
   }
   if (threadIdx.x == 0) {
     c.cnt[LS_DB] = off;
+    c.cnt[LS_POK] = offk;
+    c.cnt[LS_PMISS] = offm;
     cudaGraphSetConditional(h, off > 0 ? 1u : 0u);
+    if (!first && lazy) cudaGraphSetConditional(h2, offm > 0 ? 1u : 0u);
   }
   count_nodes(nodes);
 }
@@ -4153,6 +4286,7 @@ __global__ void report_kernel(Ctl c, int nodes) {
     r.balanced = D.P.balance;
     r.balance_sweeps = M.sweeps;
     r.db_plateau = M.plateau;
+    r.inv_skipped = M.dbskip;
     r.alpha_used = keep ? M.cert : 0.0;
     r.min_margin = M.mm;
     D.rep[b] = r;
@@ -4549,20 +4683,29 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
   return 0;
 }
 
-// one DB iteration over LS_DB (first: X only, Y = I), ending in decide_db_kernel(h)
-int cap_db_iter(Cap& C, cudaStream_t st, bool first, cudaGraphConditionalHandle h, int block_mode) {
+int cap_if_after(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaGraph_t g;
+  CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  *body = p.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  return 0;
+}
+
+DbArgs db_args(Cap& C, bool first, int list) {
   const int n = C.n;
-  const int n0 = t_cap_nodes;
-  const bool oop = inv_oop(n);
-  GL build_jobs_kernel<<<1, CT, 0, st>>>(C.c, first ? 1 : 0, oop ? 1 : 0);
-  if (!oop) {  // G2 inverts in place: copies first
-    if (cap_ew(C, st, LS_DB, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
-    if (!first && cap_ew(C, st, LS_DB, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
-  }
-  if (cap_invert(C, st, first ? C.batch : 2 * C.batch)) return LGM_ERR_CUDA;
   DbArgs a;
   a.S = C.c.S;
-  a.L = C.c.list(LS_DB);
+  a.L = C.c.list(list);
   a.xpiv = C.c.piv;
   a.xstep = C.c.step;
   a.ypiv = C.c.piv + (size_t)C.batch * n;
@@ -4575,9 +4718,47 @@ int cap_db_iter(Cap& C, cudaStream_t st, bool first, cudaGraphConditionalHandle 
   a.size = C.c.size;
   a.istat = C.c.istat;
   a.batch = C.batch;
-  GL db_update_kernel<<<dim3((n + 127) / 128, C.batch), 128, 0, st>>>(a);
-  const int nodes = t_cap_nodes - n0 + 1;
-  GL decide_db_kernel<<<1, CT, 0, st>>>(C.c, h, first ? 0 : nodes, first ? 1 : 0, block_mode);
+  a.ms = C.c.ms;
+  a.xn_slot = G_Q0;
+  return a;
+}
+
+// one DB iteration over LS_DB (first: X only, Y = I), ending in decide_db_kernel(h); later
+// iterations add the lazy-X^-1 tail (IF body captured on st_if)
+int cap_db_iter(Cap& C, cudaStream_t st, bool first, cudaGraphConditionalHandle h, int block_mode,
+                cudaStream_t st_if = nullptr) {
+  const int n = C.n;
+  const int n0 = t_cap_nodes;
+  const bool oop = inv_oop(n);
+  const bool lazy = !first && st_if && lazyx_on();
+  cudaGraphConditionalHandle h2 = 0;
+  if (lazy && new_handle(st, &h2)) return LGM_ERR_CUDA;
+  GL build_jobs_kernel<<<1, CT, 0, st>>>(C.c, first ? 1 : 0, oop ? 1 : 0);
+  if (!oop) {  // G2 inverts in place: copies first
+    if (cap_ew(C, st, LS_DB, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
+    if (!first && cap_ew(C, st, LS_DB, 1, G_YI, G_Y, G_Y)) return LGM_ERR_CUDA;
+  }
+  if (cap_invert(C, st, first ? C.batch : 2 * C.batch)) return LGM_ERR_CUDA;
+  GL db_update_kernel<<<dim3((n + 127) / 128, C.batch), 128, 0, st>>>(db_args(C, first, LS_DB));
+  const int nodes = t_cap_nodes - n0 + 1 + (lazy ? 1 : 0);
+  GL decide_db_kernel<<<1, CT, 0, st>>>(C.c, h, first ? 0 : nodes, first ? 1 : 0, block_mode, h2, lazy ? 1 : 0,
+                                         lazyx_f());
+  if (lazy) {
+    if (cap_ew(C, st, LS_POK, 1, G_B, G_Q0, G_Q0)) return LGM_ERR_CUDA;  // converged: X <- X'
+    cudaGraph_t body;
+    if (cap_if_after(st, h2, &body)) return LGM_ERR_CUDA;
+    const int saved = t_cap_nodes;
+    CK(cudaStreamBeginCaptureToGraph(st_if, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int m0 = t_cap_nodes;
+    GL build_jobs_px_kernel<<<1, CT, 0, st_if>>>(C.c, oop ? 1 : 0);
+    if (!oop && cap_ew(C, st_if, LS_PMISS, 1, G_XI, G_B, G_B)) return LGM_ERR_CUDA;
+    if (cap_invert(C, st_if, C.batch)) return LGM_ERR_CUDA;
+    const int mnodes = t_cap_nodes - m0 + 1;
+    GL db_fix_kernel<<<dim3((n + 127) / 128, C.batch), 128, 0, st_if>>>(db_args(C, false, LS_PMISS), mnodes);
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(st_if, &tmp));
+    t_cap_nodes = saved;  // the IF body's kernels are counted by db_fix_kernel when it runs
+  }
   return 0;
 }
 
@@ -4597,7 +4778,7 @@ int cap_sqrt_db(Cap& C, int depth, int block_mode) {
   cudaStream_t sb = C.s[depth + 1];
   const int saved = t_cap_nodes;  // the body's kernels are counted by its decide kernel
   CK(cudaStreamBeginCaptureToGraph(sb, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  if (cap_db_iter(C, sb, false, h, block_mode)) return LGM_ERR_CUDA;
+  if (cap_db_iter(C, sb, false, h, block_mode, depth + 2 < 4 ? C.s[depth + 2] : nullptr)) return LGM_ERR_CUDA;
   cudaGraph_t tmp;
   CK(cudaStreamEndCapture(sb, &tmp));
   t_cap_nodes = saved;
