@@ -101,6 +101,15 @@ double lazyx_f() {
   return v;
 }
 
+// Single-K-half-slot combined pass (gj_update2s_kernel; LGM_UP2S=0 selects the one-shot kernel)
+bool up2s_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_UP2S");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -1318,6 +1327,117 @@ __global__ void __launch_bounds__(2 * RT) gj_update2_kernel(const InvJob* jobs, 
     for (int mi = 0; mi < 4; ++mi) a[mi] = As2[(lr0 + mi * 8 + g) * LDA_S + k + t];
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) b[ni] = Bs2[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = c0 + ni * 8 + 2 * t;
+      const bool in = j >= col_lo && j < col_hi && !(j >= p2lo && j < p2hi) && !(j >= ex_lo && j < ex_hi);
+      if (in) *reinterpret_cast<double2*>(&J.M[(size_t)i * n + j]) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+    }
+  }
+}
+
+// The same combined pass with one K-half slot in shared memory (A1 / W1, products, then A2 / W2
+// into the same slot, products): 36 KB per CTA instead of 72, so 4 CTAs (16 warps) per SM hide
+// the loads of each other's halves -- the one-shot kernel above holds 3.  Per output element the
+// accumulation order is unchanged (C, + z2 A1 W1 in k order, + A2 W2 in k order): bit-identical.
+#ifndef UP2S_MINB
+#define UP2S_MINB 4
+#endif
+template <int RT>
+constexpr size_t up2s_smem() { return (size_t)(RT * LDA_S + TK * LDB_S + TK) * 8; }
+template <int RT>
+__global__ void __launch_bounds__(2 * RT, UP2S_MINB) gj_update2s_kernel(const InvJob* jobs, int n, int k0, int col_base,
+                                                         int col_lo, int col_hi, int ex_lo, int ex_hi, int q) {
+  extern __shared__ __align__(16) double u2sm[];
+  double* As = u2sm;               // one K-half slot: A1 / W1, then A2 / W2
+  double* Bs = As + RT * LDA_S;
+  double* Zs = Bs + TK * LDB_S;  // a zero row: the A1 operand of P2's pivot rows (z2 = 0)
+  // consecutive pairs traverse the jobs in opposite orders (L2 reuse across passes)
+  const InvJob J = jobs[(q & 1) ? gridDim.z - 1 - blockIdx.z : blockIdx.z];
+  if (*J.status) return;  // (checked first: moving this load after the tile loads measured 7% slower)
+  const double* W1 = wkind(J, 3 * q);
+  const double* W2 = wkind(J, 3 * q + 1);
+  const double* A1 = wkind(J, 3 * q + 2);
+  const int col0 = col_base + blockIdx.x * TN, row0 = blockIdx.y * RT;
+  const int p1lo = k0, p2lo = k0 + NB, p2hi = k0 + 2 * NB;
+  if (col0 >= col_hi || col0 + TN <= col_lo) return;
+  if (col0 >= p2lo && col0 + TN <= p2hi) return;
+  if (col0 >= ex_lo && col0 + TN <= ex_hi) return;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int r0 = row0 + (warp >> 1) * 32, c0 = col0 + (warp & 1) * 32;
+  // stage A1 / A2 / W1 / W2 (cp.async; n % 64 == 0 so every 16-byte chunk is in range)
+  auto stage = [&](const double* Ag, size_t lda, size_t aoff0, const double* Wg) {
+    for (int idx = tid; idx < RT * (TK / 2); idx += 2 * RT) {
+      const int r = idx / (TK / 2), c = (idx - r * (TK / 2)) * 2;
+      cp_async16(&As[r * LDA_S + c], &Ag[(size_t)(row0 + r) * lda + aoff0 + c]);
+    }
+    for (int idx = tid; idx < TK * (TN / 2); idx += 2 * RT) {
+      const int c = idx / (TN / 2), jj = (idx - c * (TN / 2)) * 2;
+      cp_async16(&Bs[c * LDB_S + jj], &Wg[(size_t)c * n + col0 + jj]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  stage(A1, NB, 0, W1);  // K-half 1: A1 / W1 (A2 / W2 reuse the slot after the first products)
+  if (tid < TK) Zs[tid] = 0.0;
+  // C fragments while the tiles land; z1 / z2 masks per row
+  double acc[4][4][2];
+  bool z2r[4];
+  // out-of-place first pair: columns beyond the pair are still only in Src
+  const double* Cs = (J.Src && k0 == 0 && c0 >= 2 * NB) ? J.Src : J.M;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int i = r0 + mi * 8 + g;
+    const int rs = J.rowstep[i];
+    const bool z1 = !(rs >= p1lo && rs < p2lo), z2 = !(rs >= p2lo && rs < p2hi);
+    z2r[mi] = z2;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int j = c0 + ni * 8 + 2 * t;  // j, j+1 on the same side of every 32-aligned boundary
+      const bool keep = (j >= p1lo && j < p2lo) ? z2 : (z1 && z2);
+      const double2 v = *reinterpret_cast<const double2*>(&Cs[(size_t)i * n + j]);
+      acc[mi][ni][0] = keep ? v.x : 0.0;
+      acc[mi][ni][1] = keep ? v.y : 0.0;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int lr0 = (warp >> 1) * 32, lc0 = (warp & 1) * 32;
+  int aoff[4];  // A1 rows, or the zero row where z2 = 0 (offsets into the shared array: LDS,
+                // no select in the k loop)
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) aoff[mi] = z2r[mi] ? (lr0 + mi * 8 + g) * LDA_S : (int)(Zs - u2sm);
+#pragma unroll
+  for (int k = 0; k < TK; k += 4) {  // + z2 A1 W1
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = u2sm[aoff[mi] + k + t];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k + t) * LDB_S + lc0 + ni * 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+  __syncthreads();  // every warp is done with A1 / W1
+  stage(J.M, (size_t)n, (size_t)p2lo, W2);  // K-half 2: P2's multipliers / W2
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TK; k += 4) {  // + A2 W2
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = As[(lr0 + mi * 8 + g) * LDA_S + k + t];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k + t) * LDB_S + lc0 + ni * 8 + g];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -4623,6 +4743,13 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
       if (tma) {
         GL gj_update2_tma_kernel<<<dim3((n + UT_ROWS - 1) / UT_ROWS, nj), UT_THREADS, ut_smem(), st>>>(d_jobs, n, k0p, cb, clo, chi, exlo,
                                                                                       exhi, qq, C.c.W, C.wmap);
+      } else if (up2s_on()) {  // one K-half slot per CTA (4 CTAs/SM)
+        if (narrow)
+          GL gj_update2s_kernel<64><<<dim3(1, tiles, nj), 128, up2s_smem<64>(), st>>>(d_jobs, n, k0p, cb, clo, chi, exlo,
+                                                                                     exhi, qq);
+        else
+          GL gj_update2s_kernel<64><<<dim3(tiles, n / 64, nj), 128, up2s_smem<64>(), st>>>(d_jobs, n, k0p, cb, clo, chi,
+                                                                                          exlo, exhi, qq);
       } else if (narrow) {
         GL gj_update2_kernel<64><<<dim3(1, tiles, nj), 128, up2_smem<64>(), st>>>(d_jobs, n, k0p, cb, clo, chi, exlo,
                                                                                  exhi, qq);
@@ -5034,6 +5161,7 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_panel_pair_kernel<512>, mx, 16 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
+  CK(cudaFuncSetAttribute(gj_update2s_kernel<64>, mx, (int)up2s_smem<64>()));
   CK(cudaFuncSetAttribute(gj_inv_ws_kernel, mx, (int)g3_smem()));
   CK(cudaFuncSetAttribute(gemm_plain_kernel, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<true>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
