@@ -68,7 +68,11 @@ typedef struct lgm_opts {
   int32_t db_maxiter; /* sqrt_db maxiter (sqrtm.py:27)                            default 50 */
   int32_t est_itmax;  /* est_power_norm itmax (matcore.py:300)                    default 5  */
   int32_t balance;    /* LogmOptions.balance                                      default 1  */
-  int32_t reserved;
+  int32_t embedded_complex; /* 1: A holds the real 2m x 2m embeddings [[X, -Y], [Y, X]] of
+                       * m x m complex matrices Z = X + iY (n = 2m); every norm, estimate,
+                       * balancing and stop test is taken on Z as the reference's complex128
+                       * path does (matcore.py:60-61, 226-231); L is the embedding of log Z.
+                       * Always the graph engine; workspace from lgm_block_workspace_bytes. 0 */
   double db_tol;      /* sqrt_db tol; 0 -> 10 n u (sqrtm.py:44-45)                default 0  */
   const double* theta;/* HOST pointer to max_k thresholds; NULL -> frozen table             */
 } lgm_opts;

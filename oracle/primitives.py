@@ -252,7 +252,7 @@ def sqrt_db(A, tol=None, maxiter=50, counter=None, margins=None):
     if tol is None:
         tol = 10.0 * n * UNIT_ROUNDOFF
     X = A.copy()
-    Y = np.eye(n)
+    Y = np.eye(n, dtype=A.dtype)  # identity_like (matcore.py:69-70): complex for complex A
     scaling = True
     for it in range(1, maxiter + 1):
         try:

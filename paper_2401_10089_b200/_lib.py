@@ -28,7 +28,7 @@ EXPORTS = ("lgm_default_opts", "lgm_workspace_bytes", "lgm_block_workspace_bytes
 class Opts(ctypes.Structure):
     _fields_ = [("max_k", ctypes.c_int32), ("maxiter_s", ctypes.c_int32),
                 ("db_maxiter", ctypes.c_int32), ("est_itmax", ctypes.c_int32),
-                ("balance", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("balance", ctypes.c_int32), ("embedded_complex", ctypes.c_int32),
                 ("db_tol", ctypes.c_double), ("theta", ctypes.POINTER(ctypes.c_double))]
 
 

@@ -143,6 +143,7 @@ static void fill_params(LgmParams& P, const lgm_opts* o) {
   P.db_maxiter = o->db_maxiter;
   P.est_itmax = o->est_itmax;
   P.balance = o->balance;
+  P.cplx = o->embedded_complex ? 1 : 0;
   P.db_tol = o->db_tol;
   for (int k = 0; k < LGM_K_MAX; ++k) {
     P.theta[k] = (o->theta && k < o->max_k) ? o->theta[k] : LGM_THETA_DEFAULT[k];
@@ -200,7 +201,7 @@ void lgm_default_opts(lgm_opts* o) {
   o->db_maxiter = 50;
   o->est_itmax = 5;
   o->balance = 1;
-  o->reserved = 0;
+  o->embedded_complex = 0;
   o->db_tol = 0.0;
   o->theta = nullptr;
 }
@@ -306,12 +307,14 @@ int lgm_logm_f64(const double* A, double* L, int64_t n, int64_t batch, int64_t l
   fill_params(P, opts);
   if (P.max_k < 1 || P.max_k > LGM_K_MAX || P.maxiter_s < 0 || P.db_maxiter < 1 || P.est_itmax < 1)
     return LGM_ERR_ARG;
+  if (P.cplx && (n & 1)) return LGM_ERR_ARG;  // a complex embedding is 2m x 2m
   if (batch == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   size_t need = 0;
-  lgm_workspace_bytes(n, batch, &need);
+  if (P.cplx) lgm_block_workspace_bytes(n, batch, &need);  // always the graph engine
+  else lgm_workspace_bytes(n, batch, &need);
   if (!ws || ws_bytes < need) return LGM_ERR_WORKSPACE;
-  if (n <= LGM_FUSED_MAX) {
+  if (n <= LGM_FUSED_MAX && !P.cplx) {
     // FULL instantiations (n == NMAX) carry n as a compile-time constant
     const bool full = (n == 32 || n == 64);
     if (n <= 32)

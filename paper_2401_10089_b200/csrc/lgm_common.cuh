@@ -18,6 +18,7 @@ int lgm_count_launch();
 // Everything the driver needs besides the matrices; passed by value as a kernel parameter.
 struct LgmParams {
   int max_k, maxiter_s, db_maxiter, est_itmax, balance;
+  int cplx;       // input = real 2n x 2n embeddings of n x n complex matrices (decisions on Z)
   double db_tol;  // 0 -> 10 n u
   double theta[LGM_K_MAX];
   int order[LGM_K_MAX];

@@ -2153,13 +2153,20 @@ __global__ void ew_kernel(Slots S, DList L, int op, int dk, int sk, int s2k) {
 
 // onenorm exactly as numpy (column sums accumulated over rows in order), max via atomicMax
 // into out[b] (zeroed beforehand).
-__global__ void onenorm_kernel(Slots S, DList L, int k, double* out) {
+// Complex embeddings (P->cplx): the norm of Z, |z_ij| = hypot(E[i][j], E[i+m][j]) over the
+// m x m complex entries (numpy's abs of complex128, then the same row-order column sums).
+__global__ void onenorm_kernel(Slots S, DList L, int k, double* out, const LgmParams* P) {
   const int n = S.n;
-  LIST_LOOP(L, (size_t)n)
+  const bool cx = P && P->cplx;
+  const int m = cx ? n / 2 : n;
+  LIST_LOOP(L, (size_t)m)
     const double* M = S.buf(b, k);
     const int j = (int)idx;
     double acc = 0.0;
-    for (int i = 0; i < n; ++i) acc = (i == 0) ? fabs(M[(size_t)i * n + j]) : acc + fabs(M[(size_t)i * n + j]);
+    for (int i = 0; i < m; ++i) {
+      const double v = cx ? hypot(M[(size_t)i * n + j], M[(size_t)(i + m) * n + j]) : fabs(M[(size_t)i * n + j]);
+      acc = (i == 0) ? v : acc + v;
+    }
     atomic_max_nonneg(&out[b], acc);
   }
 }
@@ -2229,15 +2236,21 @@ static int host_pw_leaves(int n) {
 static int bal_threads(int n) { return n <= 256 ? 64 : (n >= 2048 ? 1024 : 256); }
 static size_t bal_smem(int n) { return (size_t)2 * host_pw_leaves(n) * 8 * sizeof(double); }
 
+// Complex embeddings (P->cplx): Osborne on Z (m x m, |z| = hypot of the two blocks' entries),
+// each scaling applied to the embedding's rows / columns i and i + m.
 __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, double* scale, int* sweeps_out,
                                                         int max_sweeps, double* margin, const int* enable,
-                                                        const int* max_sweeps_p) {
+                                                        const int* max_sweeps_p, const LgmParams* P) {
   if (blockIdx.x >= *L.cnt || (enable && !*enable)) return;
   if (max_sweeps_p) max_sweeps = *max_sweeps_p;
   const int b = L.ids[blockIdx.x];
-  const int n = S.n;
+  const int nfull = S.n;
+  const bool cx = P && P->cplx;
+  const int n = cx ? nfull / 2 : nfull;  // the matrix balanced (Z's order for an embedding)
+  const size_t imoff = (size_t)n * nfull;  // offset of Im(z_ij) from Re(z_ij) in the embedding
+  auto absv = [&](const double* p, size_t off) { return cx ? hypot(p[off], p[off + imoff]) : fabs(p[off]); };
   double* B = S.buf(b, G_B);
-  double* sc = scale + (size_t)b * n;
+  double* sc = scale + (size_t)b * nfull;
   __shared__ int loff[128], llen[128];
   __shared__ double lsum[2][128];
   extern __shared__ double lacc_dyn[];  // [2][nleaf * 8] (sized by the host: bal_smem)
@@ -2249,7 +2262,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
     s_ntok = pw_tokens(n, tok, 0);
     s_mm = margin[b];
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sc[i] = 1.0;
+  for (int i = threadIdx.x; i < nfull; i += blockDim.x) sc[i] = 1.0;
   __syncthreads();
   const int nleaf = s_nleaf;
   int sweeps = 0;
@@ -2264,20 +2277,20 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
         const int which = t / (nleaf * 8), rem = t - which * nleaf * 8, q = rem >> 3, a = rem & 7;
         const int len = llen[q];
         if (len < 8) continue;
-        const double* p = which == 0 ? B + (size_t)loff[q] * n + i : B + (size_t)i * n + loff[q];
-        const size_t stride = which == 0 ? (size_t)n : 1;
+        const double* p = which == 0 ? B + (size_t)loff[q] * nfull + i : B + (size_t)i * nfull + loff[q];
+        const size_t stride = which == 0 ? (size_t)nfull : 1;
         const int m8 = len - len % 8;
         double r;
         if (m8 == 128) {  // full leaf: all 16 loads in flight, then the in-order sum
           double v[16];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = fabs(p[(a + 8 * u) * stride]);
+          for (int u = 0; u < 16; ++u) v[u] = absv(p, (a + 8 * u) * stride);
           r = v[0];
 #pragma unroll
           for (int u = 1; u < 16; ++u) r += v[u];
         } else {
-          r = fabs(p[a * stride]);
-          for (int k = 8 + a; k < m8; k += 8) r += fabs(p[k * stride]);
+          r = absv(p, a * stride);
+          for (int k = 8 + a; k < m8; k += 8) r += absv(p, k * stride);
         }
         lacc_dyn[which * nleaf * 8 + rem] = r;
       }
@@ -2285,16 +2298,16 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
       for (int l = threadIdx.x; l < 2 * nleaf; l += blockDim.x) {
         const int which = l / nleaf, q = l - which * nleaf;
         const int len = llen[q];
-        const double* p = which == 0 ? B + (size_t)loff[q] * n + i : B + (size_t)i * n + loff[q];
-        const size_t stride = which == 0 ? (size_t)n : 1;
+        const double* p = which == 0 ? B + (size_t)loff[q] * nfull + i : B + (size_t)i * nfull + loff[q];
+        const size_t stride = which == 0 ? (size_t)nfull : 1;
         double res;
         if (len < 8) {
           res = 0.0;
-          for (int k = 0; k < len; ++k) res += fabs(p[k * stride]);
+          for (int k = 0; k < len; ++k) res += absv(p, k * stride);
         } else {
           const double* r = &lacc_dyn[which * nleaf * 8 + q * 8];
           res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-          for (int k = len - len % 8; k < len; ++k) res += fabs(p[k * stride]);
+          for (int k = len - len % 8; k < len; ++k) res += absv(p, k * stride);
         }
         lsum[which][q] = res;
       }
@@ -2306,7 +2319,7 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
         rr = __shfl_sync(0x3u, cr, 1);
       }
       if (threadIdx.x == 0) {
-        double dg = fabs(B[(size_t)i * n + i]);
+        double dg = absv(B, (size_t)i * nfull + i);
         double c = cr - dg;
         double r = rr - dg;
         double mm = s_mm;
@@ -2327,10 +2340,19 @@ __global__ void __launch_bounds__(1024) balance_kernel_g(Slots S, DList L, doubl
       __syncthreads();
       if (s_do) {
         const double f = s_f, inv = 1.0 / f;
-        for (int q = threadIdx.x; q < n; q += blockDim.x) B[(size_t)q * n + i] *= f;
+        for (int q = threadIdx.x; q < nfull; q += blockDim.x) {
+          B[(size_t)q * nfull + i] *= f;
+          if (cx) B[(size_t)q * nfull + i + n] *= f;
+        }
         __syncthreads();
-        for (int q = threadIdx.x; q < n; q += blockDim.x) B[(size_t)i * n + q] *= inv;
-        if (threadIdx.x == 0) sc[i] *= f;
+        for (int q = threadIdx.x; q < nfull; q += blockDim.x) {
+          B[(size_t)i * nfull + q] *= inv;
+          if (cx) B[(size_t)(i + n) * nfull + q] *= inv;
+        }
+        if (threadIdx.x == 0) {
+          sc[i] *= f;
+          if (cx) sc[i + n] = sc[i];
+        }
         moved = true;
       }
       __syncthreads();
@@ -2387,6 +2409,7 @@ struct DbArgs {
   int batch;
   MDev* ms;            // dbpred: X' goes to slot xn_slot, Y is left for the fix-up (lazy X^-1)
   int xn_slot;
+  const LgmParams* P;  // P->cplx: change / size are the complex 1-norms of Z's m x m block
 };
 
 __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
@@ -2396,6 +2419,8 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   if (a.istat[b] || (!a.first && a.istat[a.batch + b])) return;  // singular iterate: X, Y kept
+  const bool cx = a.P && a.P->cplx;
+  const int m = cx ? n / 2 : n;
   if (!a.first && a.ms[b].dbpred) {  // predicted last iteration: X' (no X^-1 needed) to a spare slot
     const double* X = a.S.buf(b, G_B);
     double* Xn = a.S.buf(b, a.xn_slot);
@@ -2406,6 +2431,26 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
     if (a.scaling[b]) mu = fmin(fmax(exp(-(a.xlog[b] + a.ylog[b]) / (2.0 * n)), LGM_MU_MIN), LGM_MU_MAX);
     const double inv_mu = 1.0 / mu;
     double dsum = 0.0, ssum = 0.0;
+    if (cx) {  // rows r and r + m together: the complex entry of row r (column c < m)
+      for (int r = 0; r < m; ++r) {
+        const size_t e = (size_t)r * n + c, e2 = (size_t)(r + m) * n + c;
+        const double xo = X[e], xo2 = X[e2];
+        const double xn = 0.5 * (mu * xo + RY[(size_t)yp[r] * n + qyc] * inv_mu);
+        const double xn2 = 0.5 * (mu * xo2 + RY[(size_t)yp[r + m] * n + qyc] * inv_mu);
+        Xn[e] = xn;
+        Xn[e2] = xn2;
+        if (c < m) {
+          const double d = hypot(xn - xo, xn2 - xo2), sz = hypot(xn, xn2);
+          dsum = (r == 0) ? d : dsum + d;
+          ssum = (r == 0) ? sz : ssum + sz;
+        }
+      }
+      if (c < m) {
+        atomic_max_nonneg(&a.change[b], dsum);
+        atomic_max_nonneg(&a.size[b], ssum);
+      }
+      return;
+    }
     constexpr int U = 8;
     int r = 0;
     for (; r + U <= n; r += U) {
@@ -2446,6 +2491,32 @@ __global__ void __launch_bounds__(128) db_update_kernel(DbArgs a) {
   if (a.scaling[b]) mu = fmin(fmax(exp(-(a.xlog[b] + a.ylog[b]) / (2.0 * n)), LGM_MU_MIN), LGM_MU_MAX);
   const double inv_mu = 1.0 / mu;
   double dsum = 0.0, ssum = 0.0;
+  if (cx) {  // rows r and r + m together: the complex entry of row r (column c < m)
+    for (int r = 0; r < m; ++r) {
+      double xn2[2], xo2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = r + h * m;
+        const size_t e = (size_t)rr * n + c;
+        const double xi = RX[(size_t)xp[rr] * n + qxc];
+        const double yi = a.first ? ((rr == c) ? 1.0 : 0.0) : RY[(size_t)yp[rr] * n + qyc];
+        xo2[h] = X[e];
+        xn2[h] = 0.5 * (mu * xo2[h] + yi * inv_mu);
+        X[e] = xn2[h];
+        Y[e] = 0.5 * (mu * Y[e] + xi * inv_mu);
+      }
+      if (c < m) {
+        const double d = hypot(xn2[0] - xo2[0], xn2[1] - xo2[1]), sz = hypot(xn2[0], xn2[1]);
+        dsum = (r == 0) ? d : dsum + d;
+        ssum = (r == 0) ? sz : ssum + sz;
+      }
+    }
+    if (c < m) {
+      atomic_max_nonneg(&a.change[b], dsum);
+      atomic_max_nonneg(&a.size[b], ssum);
+    }
+    return;
+  }
   // rows in chunks of 8 with every load of the chunk issued before the (row-ordered) sums:
   // the permuted-storage gathers are scattered, so their latency needs overlapping when
   // few columns (threads) are in flight (small batches at large n)
@@ -2531,6 +2602,7 @@ struct EstJob {
   int zchk;           // est_power_norm's zero-matrix shortcut applies (matcore.py:309-310)
   int nzf;            // set by est_nz_kernel when M1 has a nonzero entry
   int owner, key;     // matrix index and cache key (power) of the request
+  int cplx;           // vectors are complex embeddings [Re; Im] of length n = 2m (decisions on Z)
   double* V0;         // ping
   double* V1;         // pong
   double* part;       // adjoint partial sums [splits][2][n]
@@ -2541,17 +2613,27 @@ struct EstJob {
   double mm;
 };
 
-__global__ void est_init_kernel(EstJob* jobs, int n, double rsum) {
+// initial block X (matcore.py:265-271): ones / m and the normalised alternating ramp, m = the
+// operator's order (Z's for a complex embedding: [Re; Im] with zero imaginary parts)
+__device__ __forceinline__ int est_x0(const EstJob& J, int n, double rsum, double rsum_c, int i0, int step) {
+  const bool cx = J.cplx;
+  const int m = cx ? n / 2 : n;
+  const double rs = cx ? rsum_c : rsum;
+  const int t = m < 2 ? m : 2;
+  for (int i = i0; i < n; i += step) {
+    const bool re = i < m;
+    J.V0[i] = re ? 1.0 / m : 0.0;
+    if (t > 1) J.V0[n + i] = re ? (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(m > 1 ? m - 1 : 1))) / rs : 0.0;
+  }
+  return t;
+}
+__global__ void est_init_kernel(EstJob* jobs, int n, double rsum, double rsum_c) {
   EstJob& J = jobs[blockIdx.y];
   if (!J.live) {  // unused slot of a device-built table (its vectors are not assigned)
     if (blockIdx.x == 0 && threadIdx.x == 0) J.done = 1;
     return;
   }
-  const int t = n < 2 ? n : 2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    J.V0[i] = 1.0 / n;
-    if (t > 1) J.V0[n + i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
-  }
+  const int t = est_x0(J, n, rsum, rsum_c, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
     J.total = J.p1 + (J.M2 ? 1 : 0);
@@ -2721,14 +2803,17 @@ __device__ __forceinline__ void mgap(double& mm, double a, double b) {
 
 // After the forward application: column 1-norms, argmax, estimate update, S = sign(Y).
 // (CTA-wide body: 256 threads per job, shared by the per-step kernels and est_fused_kernel)
-__device__ void est_after_fwd_body(EstJob& J, int n, int sweep, double* sred) {
+template <bool CXT>
+__device__ void est_after_fwd_impl(EstJob& J, int n, int sweep, double* sred) {
   if (J.done) return;
   double* Yv = (J.total & 1) ? J.V1 : J.V0;
   const int nc = J.ncols;
+  constexpr bool cx = CXT;
+  const int m = cx ? n / 2 : n;  // Z's order; an entry's Im part sits m below its Re part
   double cn[2] = {0.0, 0.0};
   for (int c = 0; c < nc; ++c) {
     double v = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v += fabs(Yv[c * n + i]);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) v += cx ? hypot(Yv[c * n + i], Yv[c * n + i + m]) : fabs(Yv[c * n + i]);
     cn[c] = block_sum(v, sred);
   }
   const int j = (nc > 1 && cn[1] > cn[0]) ? 1 : 0;
@@ -2746,20 +2831,29 @@ __device__ void est_after_fwd_body(EstJob& J, int n, int sweep, double* sred) {
     J.est = est; J.best_j = best; J.mm = mm; J.passes += J.total;
     if (stop) J.done = 1;
   }
-  if (!stop) {  // S = sign(Y) in place (matcore.py:231); the adjoint reads it as step 0 input
+  if (!stop) {  // S = sign(Y) in place (matcore.py:226-231); the adjoint reads it as step 0 input
+    double* D = (J.total & 1) ? J.V0 : Yv;  // adjoint starts from V0: move if Y landed in V1
     for (int c = 0; c < nc; ++c)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double v = Yv[c * n + i];
-        double s = (v >= 0.0) ? 1.0 : -1.0;
-        // adjoint starts from V0: move if the forward result landed in V1
-        if (J.total & 1) J.V0[c * n + i] = s;
-        else Yv[c * n + i] = s;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        if (cx) {  // complex sign: y / |y|, 1 where y = 0
+          const double re = Yv[c * n + i], im = Yv[c * n + i + m];
+          const double a = hypot(re, im);
+          D[c * n + i] = a == 0.0 ? 1.0 : re / a;
+          D[c * n + i + m] = a == 0.0 ? 0.0 : im / a;
+        } else {
+          D[c * n + i] = (Yv[c * n + i] >= 0.0) ? 1.0 : -1.0;
+        }
       }
   }
 }
+__device__ void est_after_fwd_body(EstJob& J, int n, int sweep, double* sred) {
+  if (J.cplx) est_after_fwd_impl<true>(J, n, sweep, sred);
+  else est_after_fwd_impl<false>(J, n, sweep, sred);
+}
+template <bool CX>
 __global__ void __launch_bounds__(256) est_after_fwd_kernel(EstJob* jobs, int n, int sweep) {
   __shared__ double sred[8];
-  est_after_fwd_body(jobs[blockIdx.x], n, sweep, sred);
+  est_after_fwd_impl<CX>(jobs[blockIdx.x], n, sweep, sred);
 }
 
 // After the adjoint: h = row max |Z|, top-(4t+1) order, picks, stopping test, next X.
@@ -2769,7 +2863,8 @@ struct EstAdjSmem {
   int order[9];
   double hval[9];
 };
-__device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) {
+template <bool CXT>
+__device__ void est_after_adj_impl(EstJob& J, int n, int sweep, EstAdjSmem& sa) {
   uint64_t* skey = sa.skey;
   int* sidx = sa.sidx;
   int* order = sa.order;
@@ -2777,18 +2872,21 @@ __device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) 
   if (J.done) return;
   const double* Z = (J.total & 1) ? J.V1 : J.V0;
   const int nc = J.ncols;
-  const int t = n < 2 ? n : 2;
-  const int ntop = n < 4 * t + 1 ? n : 4 * t + 1;
+  constexpr bool cx = CXT;
+  const int m = cx ? n / 2 : n;  // Z's order (complex embeddings: Im parts m below)
+  auto zabs = [&](int off) { return cx ? hypot(Z[off], Z[off + m]) : fabs(Z[off]); };
+  const int t = m < 2 ? m : 2;
+  const int ntop = m < 4 * t + 1 ? m : 4 * t + 1;
   // repeated block argmax over h with exclusion of already taken rows
   for (int qq = 0; qq < ntop; ++qq) {
     uint64_t key = 0ull;
     int idx = 0x7fffffff;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
       bool taken = false;
       for (int u = 0; u < qq; ++u) taken |= (order[u] == i);
       if (taken) continue;
-      double h = fabs(Z[i]);
-      if (nc > 1) h = fmax(h, fabs(Z[n + i]));
+      double h = zabs(i);
+      if (nc > 1) h = fmax(h, zabs(n + i));
       uint64_t kq = dkey(h);
       if (kq > key) { key = kq; idx = i; }
     }
@@ -2809,7 +2907,7 @@ __device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) 
       for (int u = 0; u < J.nhist; ++u) seen |= (J.hist[u] == i);
       if (!seen) picks[np++] = i;
     }
-    auto hrow = [&](int i) { double h = fabs(Z[i]); if (nc > 1) h = fmax(h, fabs(Z[n + i])); return h; };
+    auto hrow = [&](int i) { double h = zabs(i); if (nc > 1) h = fmax(h, zabs(n + i)); return h; };
     const double h0 = hval[0], hb = hrow(J.best_j);
     if (sweep > 0 && order[0] != J.best_j) mgap(mm, h0, hb);
     J.mm = mm;
@@ -2830,9 +2928,14 @@ __device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) 
     J.V0[n + i] = (i == order[1]) ? 1.0 : 0.0;
   }
 }
+__device__ void est_after_adj_body(EstJob& J, int n, int sweep, EstAdjSmem& sa) {
+  if (J.cplx) est_after_adj_impl<true>(J, n, sweep, sa);
+  else est_after_adj_impl<false>(J, n, sweep, sa);
+}
+template <bool CX>
 __global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n, int sweep) {
   __shared__ EstAdjSmem sa;
-  est_after_adj_body(jobs[blockIdx.x], n, sweep, sa);
+  est_after_adj_impl<CX>(jobs[blockIdx.x], n, sweep, sa);
 }
 
 // The whole estimate for one job per CTA (256 threads), M1 resident in shared memory
@@ -2841,7 +2944,8 @@ __global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n,
 // lane-strided FMAs + butterfly; adjoint: thread per column, 64-row slabs with 4 accumulators,
 // slab partials summed in order; the after-bodies are shared), so the two paths agree bit for bit.
 constexpr int EST_FUSED_MAXN = 160;
-__global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, int itmax) {
+template <bool CX>
+__global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
   extern __shared__ __align__(16) double Ms[];
   __shared__ double sred[8];
   __shared__ EstAdjSmem sa;
@@ -2852,11 +2956,7 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
     return;
   }
   {  // est_init_kernel
-    const int t = n < 2 ? n : 2;
-    for (int i = tid; i < n; i += 256) {
-      J.V0[i] = 1.0 / n;
-      if (t > 1) J.V0[n + i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
-    }
+    const int t = est_x0(J, n, rsum, rsum_c, tid, 256);
     if (tid == 0) {
       J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
       J.total = J.p1 + (J.M2 ? 1 : 0);
@@ -2895,7 +2995,7 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
       }
       __syncthreads();
     }
-    est_after_fwd_body(J, n, sweep, sred);
+    est_after_fwd_impl<CX>(J, n, sweep, sred);
     __syncthreads();
     if (J.done) break;
     const bool two = J.ncols > 1;
@@ -2934,7 +3034,7 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
       }
       __syncthreads();
     }
-    est_after_adj_body(J, n, sweep, sa);
+    est_after_adj_impl<CX>(J, n, sweep, sa);
     __syncthreads();
   }
 }
@@ -3554,6 +3654,7 @@ __device__ void est_slot(Ctl& c, int q, int b, const double* M1, int p1, const d
   J.nzf = 0;
   J.owner = b;
   J.key = key;
+  J.cplx = c.desc->P.cplx;
   J.V0 = c.vec + (size_t)q * 4 * c.n;
   J.V1 = J.V0 + 2 * c.n;
   J.part = c.part + (size_t)q * c.splits * 2 * c.n;
@@ -3817,7 +3918,8 @@ __global__ void __launch_bounds__(CT) decide_db_kernel(Ctl c, cudaGraphCondition
   const int n = c.n;
   const double tol_in = block_mode ? D.tol : D.P.db_tol;
   const int maxiter = block_mode ? D.maxiter : D.P.db_maxiter;
-  const double tol = tol_in > 0.0 ? tol_in : 10.0 * n * LGM_UNIT_ROUNDOFF;
+  const int nz = D.P.cplx ? n / 2 : n;  // Z's order for a complex embedding
+  const double tol = tol_in > 0.0 ? tol_in : 10.0 * nz * LGM_UNIT_ROUNDOFF;
   int off = 0, offk = 0, offm = 0;
   FOR_LIST(c, LS_DB)
     bool next = false, pok = false, pmiss = false;
@@ -4507,6 +4609,7 @@ struct Cap {
   cudaEvent_t evN, evP;
   int itmax;
   int mk = 14;          // m_K: estimator thin products <= m_K + 1 (s = 0) / m_K / 2 + 1
+  bool cplx = false;    // complex embeddings (lgm_opts.embedded_complex): estimator variants
   bool tma = false;     // rank-64 passes by gj_update2_tma_kernel (W stored transposed)
   CUtensorMap wmap;     // the W region as (12 batch n) rows x NB doubles, 64 x 16 boxes
 };
@@ -4593,7 +4696,7 @@ int cap_ew(Cap& C, cudaStream_t st, int lst, int op, int dk, int sk, int s2k) {
 
 int cap_norm(Cap& C, cudaStream_t st, int lst, int slot, double* out) {
   CK(cudaMemsetAsync(out, 0, C.batch * 8, st));
-  GL onenorm_kernel<<<ew_blocks(), 128, 0, st>>>(C.c.S, C.c.list(lst), slot, out);
+  GL onenorm_kernel<<<ew_blocks(), 128, 0, st>>>(C.c.S, C.c.list(lst), slot, out, &C.c.desc->P);
   return 0;
 }
 
@@ -4601,10 +4704,12 @@ int cap_norm(Cap& C, cudaStream_t st, int lst, int slot, double* out) {
 int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
   const int n = C.n, nj = C.batch;
   const double rsum = host_pairwise_abs_ramp(n);
+  const double rsum_c = host_pairwise_abs_ramp(n > 1 ? n / 2 : 1);  // complex embeddings (order n / 2)
   GL est_nz_kernel<<<dim3(std::max(1, std::min(32, n * n / 4096)), nj), 256, 0, st>>>(C.c.est, n);
   if (n <= EST_FUSED_MAXN && est_fused_on()) {
     const int sm = n * n * 8;
-    GL est_fused_kernel<<<nj, 256, sm, st>>>(C.c.est, n, rsum, C.itmax);
+    if (C.cplx) GL est_fused_kernel<true><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
+    else GL est_fused_kernel<false><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
     return 0;
   }
   if (n > EST_FUSED_MAXN && n <= 512 && est_cluster_on()) {  // M1 resident in a cluster's smem
@@ -4625,18 +4730,20 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
     else CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<16>, C.c.est, n, rsum, C.itmax)));
     return 0;
   }
-  GL est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, rsum);
+  GL est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, rsum, rsum_c);
   for (int sweep = 0; sweep < C.itmax; ++sweep) {
     for (int q = 0; q < maxq; ++q)
       GL est_fwd_kernel<<<dim3((n + 8 * EST_FWD_R - 1) / (8 * EST_FWD_R), nj), 256, 0, st>>>(C.c.est, n, q);
-    GL est_after_fwd_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+    if (C.cplx) GL est_after_fwd_kernel<true><<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+    else GL est_after_fwd_kernel<false><<<nj, 256, 0, st>>>(C.c.est, n, sweep);
     for (int q = 0; q < maxq; ++q) {
       // (flip: the first adjoint product runs opposite to the last forward one)
       if ((n & 1) == 0) GL est_adj2_kernel<<<dim3((n + 255) / 256, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q, maxq & 1);
       else GL est_adj_kernel<<<dim3((n + 127) / 128, C.c.splits, nj), 128, 0, st>>>(C.c.est, n, q, maxq & 1);
       GL est_adj_reduce_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, q, C.c.splits);
     }
-    GL est_after_adj_kernel<<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+    if (C.cplx) GL est_after_adj_kernel<true><<<nj, 256, 0, st>>>(C.c.est, n, sweep);
+    else GL est_after_adj_kernel<false><<<nj, 256, 0, st>>>(C.c.est, n, sweep);
   }
   return 0;
 }
@@ -4847,6 +4954,7 @@ DbArgs db_args(Cap& C, bool first, int list) {
   a.batch = C.batch;
   a.ms = C.c.ms;
   a.xn_slot = G_Q0;
+  a.P = &C.c.desc->P;
   return a;
 }
 
@@ -4971,7 +5079,8 @@ int cap_logm(Cap& C) {
   GL decide_live_kernel<<<1, CT, 0, st>>>(C.c);
   // balance (matcore.py:180-215); the kernel returns at once when the call disables it
   GL balance_kernel_g<<<C.batch, bal_threads(n), bal_smem(n), st>>>(C.c.S, C.c.list(LS_LIVE), C.c.scale, C.c.sweeps,
-                                                                    100, C.c.margin, &C.c.desc->P.balance, nullptr);
+                                                                    100, C.c.margin, &C.c.desc->P.balance, nullptr,
+                                                                    &C.c.desc->P);
   if (cap_ew(C, st, LS_LIVE, 0, G_AM, G_B, G_B)) return LGM_ERR_CUDA;
   if (cap_norm(C, st, LS_LIVE, G_AM, C.c.nrm)) return LGM_ERR_CUDA;
   GL decide_start_kernel<<<1, CT, 0, st>>>(C.c);
@@ -5056,7 +5165,7 @@ int cap_block(Cap& C, int prog, int has2, int p1) {
   } else if (prog == PROG_BALANCE) {
     if (cap_load(C, st, &C.c.desc->A, G_B)) return LGM_ERR_CUDA;
     GL balance_kernel_g<<<C.batch, bal_threads(n), bal_smem(n), st>>>(C.c.S, C.c.list(LS_ALL), C.c.scale, C.c.sweeps,
-                                                                      0, C.c.margin, nullptr, &C.c.desc->max_sweeps);
+                                                                      0, C.c.margin, nullptr, &C.c.desc->max_sweeps, nullptr);
     GL store_kernel<<<ew_blocks(), 256, 0, st>>>(C.c.S, C.c.list(LS_ALL), C.c.desc, G_B);
     GL block_out_kernel<<<(C.batch + 255) / 256, 256, 0, st>>>(C.c, 2, t_cap_nodes + 1);
   } else if (prog == PROG_EXPM) {
@@ -5120,9 +5229,10 @@ struct GraphKey {
   int dev, prog, n, batch, itmax, has2, p1;
   const void* ws;
   int mk;  // m_K of the call's max_k (bounds the estimator's thin-product count)
+  int cplx = 0;  // complex embeddings (estimator kernel variants)
   bool operator==(const GraphKey& o) const {
     return dev == o.dev && prog == o.prog && n == o.n && batch == o.batch && itmax == o.itmax && has2 == o.has2 &&
-           p1 == o.p1 && ws == o.ws && mk == o.mk;
+           p1 == o.p1 && ws == o.ws && mk == o.mk && cplx == o.cplx;
   }
 };
 struct GraphEntry {
@@ -5149,7 +5259,8 @@ struct CapStreams {
 // dynamic shared-memory limits are per device: set before every capture (no process-wide flag)
 int set_attrs(int n) {
   const cudaFuncAttribute mx = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  CK(cudaFuncSetAttribute(est_fused_kernel, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
+  CK(cudaFuncSetAttribute(est_fused_kernel<false>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
+  CK(cudaFuncSetAttribute(est_fused_kernel<true>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128>, mx, (int)G1Smem<128>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<256>, mx, (int)G1Smem<256>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<512>, mx, (int)G1Smem<512>::bytes));
@@ -5200,6 +5311,7 @@ int build_exec(const GraphKey& k, void* ws, cudaGraphExec_t* out) {
   C.evP = cs.evP;
   C.itmax = k.itmax;
   C.mk = k.mk > 0 ? k.mk : LGM_ORDER_DEFAULT[LGM_K_DEFAULT - 1];
+  C.cplx = k.cplx != 0;
   C.tma = g2_tma_on() && k.n <= 512 && k.n % (2 * NB) == 0 && !use_g1(k.n);
   if (C.tma && make_wmap(C)) return LGM_ERR_CUDA;
   cudaGraph_t g;
@@ -5291,7 +5403,7 @@ int lgm_grid_logm(const double* A, double* L, int64_t n, int64_t batch, int64_t 
   d.L = L;
   d.ld = ld;
   d.rep = rep;
-  GraphKey k{0, PROG_LOGM, (int)n, (int)batch, P.est_itmax, 0, 0, nullptr, P.order[P.max_k - 1]};
+  GraphKey k{0, PROG_LOGM, (int)n, (int)batch, P.est_itmax, 0, 0, nullptr, P.order[P.max_k - 1], P.cplx};
   return run_prog(k, ws, d, st);
 }
 

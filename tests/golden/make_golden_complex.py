@@ -40,6 +40,14 @@ def cases():
     # complex-spectrum rotation (eigenvalues e^{+-i 0.7} etc.) and a negative real eigenvalue
     out.append(("rot2c", np.array([[np.cos(0.7), -np.sin(0.7)], [np.sin(0.7), np.cos(0.7)]]) * (1 + 0.5j)))
     out.append(("negreal3", np.diag([-2.0 + 0j, 1.0, 3.0j])))
+    # nonnormal S T S^-1 with a complex log-uniform spectrum at n = 128 (several square roots;
+    # pins the restated sqrt_db's complex identity at sizes where numpy's result layout changes)
+    n = 128
+    mag = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), n))
+    ph = rng.uniform(-2.5, 2.5, n)
+    T = np.diag(mag * np.exp(1j * ph)) + np.triu((0.3 / n) * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))), 1)
+    S = np.eye(n) + 0.1 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
+    out.append(("nonnormal128", S @ T @ np.linalg.inv(S)))
     return out
 
 

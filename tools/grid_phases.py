@@ -19,7 +19,7 @@ cfg = cfg if cfg in ("3b", "5b") else int(cfg)
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else None
 A = torch.from_numpy(synth.config(cfg, batch=batch)).cuda()
 opts = lp.LogmOptions(raise_on_error=False)
-lib = _lib.load()
+lib = _lib.load(os.environ.get("LGM_LIB", _lib.LIB_PATH))  # LGM_LIB: A/B builds
 lib.lgm_debug_grid_phase_ns.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = (ctypes.c_ulonglong * 8)()
 driver.run_device(A, opts)
