@@ -12,6 +12,8 @@
  *   lgm_est_product_norm_f64  <- est_product_norm([(M1,p1),(M2,1)], ...) (matcore.py:234-297)
  *   lgm_balance_f64           <- balance(A, max_sweeps)                 (matcore.py:180-215)
  *   lgm_eval_degopt_f64       <- eval_degopt(builtin_scheme(k), A, counter, first_product)
+ *   lgm_eval_degopt_scheme_f64 <- eval_degopt(scheme, A, counter, first_product) for any
+ *                                 GraphScheme with k <= 9 products (schemes.py:50-126)
  *                                                                       (schemes.py:104-126, 337-350)
  *
  * Conventions: every matrix pointer is a DEVICE pointer to `batch` row-major n x n
@@ -138,6 +140,16 @@ int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_
 int lgm_eval_degopt_f64(const double* X, const double* first_product, double* Z, int64_t n,
                         int64_t batch, int64_t ld, int32_t k, int32_t* products_dev,
                         void* workspace, size_t workspace_bytes, lgm_stream_t stream);
+
+/* The same for a caller's scheme (GraphScheme: P1 = I, P2 = X, P_{j+2} = (sum_i lhs[j][i] P_i)
+ * (sum_i rhs[j][i] P_i), z = sum_i out[i] P_i) with k = 1..9 products; coef (HOST) holds the
+ * k lhs rows (row j has j + 2 entries), then the k rhs rows, then the k + 2 out entries.
+ * first_product (X^2) requires lhs[0] == rhs[0] == (0, 1) (the caller checks, as schemes.py
+ * does); non-finite coefficients -> LGM_ERR_ARG. */
+int lgm_eval_degopt_scheme_f64(const double* X, const double* first_product, double* Z, int64_t n,
+                               int64_t batch, int64_t ld, int32_t k, const double* coef,
+                               int32_t* products_dev, void* workspace, size_t workspace_bytes,
+                               lgm_stream_t stream);
 
 /* E = expm(A) by the reference's test-oracle recipe (matcore.py:318-336 expm_ref): scale to
  * ||A||_1 <= 1/2, degree-20 Taylor in Horner form, square back.  Validation helper (round

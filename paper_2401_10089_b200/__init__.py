@@ -16,6 +16,8 @@ from .exceptions import (ConvergenceError, ExtensionMissingError, SchemeFormatEr
 from .matio import format_matrix, parse_matrix, read_matrix, write_matrix
 from .primitives import (BalanceTransform, balance, balance_batched, est_power_norm, est_product_norm,
                          eval_degopt, sqrt_db, sqrt_db_batched)
+from .schemes import (GraphScheme, SchemeMeta, builtin_scheme, load_scheme, read_scheme, save_scheme,
+                      write_scheme)
 
 __version__ = "0.1.0"
 
@@ -25,4 +27,5 @@ __all__ = [
     "SpectrumError", "BalanceTransform", "balance", "balance_batched", "est_power_norm",
     "est_product_norm", "eval_degopt", "sqrt_db", "sqrt_db_batched", "constants",
     "SchemeFormatError", "format_matrix", "parse_matrix", "read_matrix", "write_matrix",
+    "GraphScheme", "SchemeMeta", "builtin_scheme", "load_scheme", "read_scheme", "save_scheme", "write_scheme",
 ]

@@ -22,7 +22,7 @@ ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED, ERR_WORKSPACE = -1, -2, -3, -4
 EXPORTS = ("lgm_default_opts", "lgm_workspace_bytes", "lgm_block_workspace_bytes", "lgm_max_fused_n", "lgm_logm_f64",
            "lgm_sqrt_db_f64", "lgm_est_power_norm_f64", "lgm_est_product_norm_f64",
            "lgm_balance_f64", "lgm_eval_degopt_f64", "lgm_expm_ref_f64", "lgm_spectrum_check_f64", "lgm_status_string", "lgm_launch_count",
-           "lgm_debug_ws_guard")
+           "lgm_debug_ws_guard", "lgm_eval_degopt_scheme_f64")
 
 
 class Opts(ctypes.Structure):
@@ -67,6 +67,7 @@ def load(path=LIB_PATH):
     lib.lgm_est_product_norm_f64.argtypes = [_P, _I32, _P, _I64, _I64, _I64, _I32, _P, _P, _P, _W, _P]
     lib.lgm_balance_f64.argtypes = [_P, _P, _P, _I64, _I64, _I64, _I32, _P, _P, _W, _P]
     lib.lgm_eval_degopt_f64.argtypes = [_P, _P, _P, _I64, _I64, _I64, _I32, _P, _P, _W, _P]
+    lib.lgm_eval_degopt_scheme_f64.argtypes = [_P, _P, _P, _I64, _I64, _I64, _I32, _P, _P, _P, _W, _P]
     lib.lgm_expm_ref_f64.argtypes = [_P, _P, _I64, _I64, _I64, _P, _W, _P]
     lib.lgm_spectrum_check_f64.argtypes = [_P, _P, _I64, _I64, _I64, _P, _W, _P]
     lib.lgm_status_string.argtypes = [ctypes.c_int]

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 
 #include "lgm_fused.cuh"
@@ -420,14 +421,23 @@ int lgm_balance_f64(const double* A, double* B, double* scale, int64_t n, int64_
   return 0;
 }
 
-int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
-                        int32_t* products, void* ws, size_t ws_bytes, lgm_stream_t stream) {
+// eval_degopt for scheme k: the shipped coefficients, or (coef != NULL) the caller's scheme with
+// k products in the same layout (lhs rows j = 0..k-1 with j + 2 entries, rhs rows, out k + 2),
+// which takes the place of scheme k in the parameter block
+static int degopt_impl(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
+                       const double* coef, int32_t* products, void* ws, size_t ws_bytes, lgm_stream_t stream) {
   if (!args_ok(X, n, batch, ld) || !Z || !products || k < 1 || k > LGM_K_MAX) return LGM_ERR_ARG;
   const bool fused = n <= LGM_FUSED_MAX && k <= 5;  // node storage of the fused kernel: P4..P6
   if (!block_ws_ok(n, batch, ws, ws_bytes, fused)) return LGM_ERR_WORKSPACE;
   if (batch == 0) return 0;
   LgmParams P;
   fill_params(P, nullptr);
+  if (coef) {
+    const int len = k * (k + 3) + k + 2;
+    for (int i = 0; i < len; ++i)
+      if (!std::isfinite(coef[i])) return LGM_ERR_ARG;
+    std::memcpy(P.coef + P.coef_off[k - 1], coef, (size_t)len * sizeof(double));
+  }
   if (fused && n <= 32) {
     if (prep<32>(degopt_kernel<32>, Cfg<32>::SMEM_BYTES_X)) return LGM_ERR_CUDA;
     lgm_count_launch(), degopt_kernel<32><<<(unsigned)batch, Cfg<32>::NT, Cfg<32>::SMEM_BYTES_X, (cudaStream_t)stream>>>(X, FP, Z, ld, (int)n,
@@ -448,6 +458,18 @@ int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n,
     if (rc) return rc;
   }
   return 0;
+}
+
+int lgm_eval_degopt_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld, int32_t k,
+                        int32_t* products, void* ws, size_t ws_bytes, lgm_stream_t stream) {
+  return degopt_impl(X, FP, Z, n, batch, ld, k, nullptr, products, ws, ws_bytes, stream);
+}
+
+int lgm_eval_degopt_scheme_f64(const double* X, const double* FP, double* Z, int64_t n, int64_t batch, int64_t ld,
+                               int32_t k, const double* coef, int32_t* products, void* ws, size_t ws_bytes,
+                               lgm_stream_t stream) {
+  if (!coef) return LGM_ERR_ARG;
+  return degopt_impl(X, FP, Z, n, batch, ld, k, coef, products, ws, ws_bytes, stream);
 }
 
 // Diagnostics (LGM_WS_GUARD=1 only): the guard bands after every workspace region / slot.

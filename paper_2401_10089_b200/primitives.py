@@ -14,8 +14,10 @@ import ctypes
 import numpy as np
 
 from . import _lib
+from . import constants as C
 from .driver import OpCounter, _as_batch, _raise_for, _torch
 from .exceptions import ConvergenceError, SingularMatrixError
+from .schemes import GraphScheme
 
 
 class BalanceTransform:
@@ -161,9 +163,24 @@ def balance(A, max_sweeps=100):
     return Bo, [BalanceTransform(s) for s in sc]
 
 
-def eval_degopt(k, A, counter=None, first_product=None):
+def eval_degopt(scheme, A, counter=None, first_product=None):
+    """z(A) for a scheme (schemes.py:104-126): ``scheme`` is a GraphScheme (any coefficients,
+    k <= 9 products) or an int k (the shipped scheme k)."""
     torch = _torch()
-    k = int(getattr(k, "mults", k))
+    custom = None
+    if isinstance(scheme, int):
+        k = scheme
+    else:
+        if not isinstance(scheme, GraphScheme):  # a reference-style object with lhs / rhs / out
+            scheme = GraphScheme(lhs=tuple(map(tuple, scheme.lhs)), rhs=tuple(map(tuple, scheme.rhs)),
+                                 out=tuple(scheme.out))
+        k = scheme.mults
+        if k > C.K_MAX:
+            raise ValueError(f"schemes with more than {C.K_MAX} products are not supported")
+        if first_product is not None and not scheme.is_normalized:
+            raise ValueError("first_product reuse requires a normalized scheme")
+        flat = scheme.flat()
+        custom = (ctypes.c_double * len(flat))(*flat)
     Ad, was_numpy, squeeze = _dev(A)
     B, n, _ = Ad.shape
     FP = None
@@ -172,9 +189,15 @@ def eval_degopt(k, A, counter=None, first_product=None):
     Z = torch.empty_like(Ad)
     pr = torch.zeros(B, dtype=torch.int32, device=Ad.device)
     ws, wp, wb = _block_ws(n, B, Ad.device)
-    _lib.check(_lib.load().lgm_eval_degopt_f64(Ad.data_ptr(), FP.data_ptr() if FP is not None else None,
-                                               Z.data_ptr(), n, B, n, k, pr.data_ptr(), wp, wb, _stream(Ad.device)),
-               "lgm_eval_degopt_f64")
+    lib = _lib.load()
+    fp = FP.data_ptr() if FP is not None else None
+    if custom is None:
+        rc = lib.lgm_eval_degopt_f64(Ad.data_ptr(), fp, Z.data_ptr(), n, B, n, k, pr.data_ptr(), wp, wb,
+                                     _stream(Ad.device))
+    else:
+        rc = lib.lgm_eval_degopt_scheme_f64(Ad.data_ptr(), fp, Z.data_ptr(), n, B, n, k, custom, pr.data_ptr(), wp,
+                                            wb, _stream(Ad.device))
+    _lib.check(rc, "lgm_eval_degopt")
     if counter is not None:
         counter.products += int(pr.cpu().numpy().sum())
     return _out(Z, was_numpy, squeeze)

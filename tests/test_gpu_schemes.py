@@ -52,3 +52,30 @@ def test_logm_max_k_high_vs_oracle(c, n, B):
     ok = (reps["status"] == 0) & (reps5["status"] == 0)
     assert (reps["s"][ok] <= reps5["s"][ok]).all()
     assert (reps["alpha_used"][ok] <= np.array(C.THETA)[reps["k"][ok] - 1]).all()
+
+
+@pytest.mark.parametrize("n", [24, 64, 100])
+@pytest.mark.parametrize("k", [1, 3, 5, 7])
+def test_eval_degopt_caller_scheme(n, k):
+    """Any GraphScheme (schemes.py:50-126) through lgm_eval_degopt_scheme_f64: random
+    coefficients (first rows pinned to (0, 1) so first_product applies), GPU vs the oracle's
+    eval_degopt on the same coefficients; an unnormalized scheme with first_product raises."""
+    rng = np.random.default_rng(100 * n + k)
+    rows = lambda: tuple([(0.0, 1.0)] + [tuple(0.5 * rng.standard_normal(j + 2)) for j in range(1, k)])  # noqa: E731
+    s = lp.GraphScheme(lhs=rows(), rhs=rows(), out=tuple(0.5 * rng.standard_normal(k + 2)))
+    G = rng.standard_normal((2, n, n))
+    X = 0.3 * G / np.linalg.norm(G, 2, axis=(1, 2))[:, None, None]
+    c, c2 = lp.OpCounter(), lp.OpCounter()
+    Z = lp.eval_degopt(s, X, counter=c)
+    Z2 = lp.eval_degopt(s, X, counter=c2, first_product=X @ X)
+    for b in range(2):
+        Zo = P.eval_degopt((s.lhs, s.rhs, s.out), X[b])
+        assert rel_err(Z[b], Zo) <= 1e-13 and rel_err(Z2[b], Zo) <= 1e-13, (rel_err(Z[b], Zo), rel_err(Z2[b], Zo))
+    assert c.products == 2 * k and c2.products == 2 * (k - 1)
+    # the built-in path is untouched by a caller's scheme call (its coefficients live in the call)
+    Zb = lp.eval_degopt(k, X)
+    for b in range(2):
+        assert rel_err(Zb[b], P.eval_degopt(C.SCHEMES[k - 1], X[b])) <= 1e-13
+    bad = lp.GraphScheme(lhs=((0.5, 1.0),) + s.lhs[1:], rhs=s.rhs, out=s.out)
+    with pytest.raises(ValueError):
+        lp.eval_degopt(bad, X, first_product=X @ X)
