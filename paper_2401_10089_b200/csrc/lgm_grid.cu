@@ -63,10 +63,11 @@ bool use_g1(int n) {
 // columns not yet written from Src.
 bool inv_oop(int n) { return use_g1(n) || (n <= 512 && n % 64 == 0 && !(std::getenv("LGM_G2_RANK64") && std::getenv("LGM_G2_RANK64")[0] == '0')); }
 
-// Cluster-resident estimator for EST_FUSED_MAXN < n <= 512, opt-in (LGM_EST_CLUSTER=1): at
-// config 4 it measured 14.8 ms per 256-job estimate against 5.0 ms for the per-step kernels --
-// only 8 clusters of 16 CTAs run at once and each job's ~63 dependent thin products serialise
-// on cluster barriers and DSMEM gathers
+// Cluster-resident estimator for EST_FUSED_MAXN < n <= 512, opt-in (LGM_EST_CLUSTER=1): bit-
+// identical to the per-step kernels; at config 4 it measured 6.4 ms per 256-job estimate (round 1
+// design: 14.8 ms) against 5.0 ms for the per-step kernels -- only 8 clusters of 16 CTAs run at
+// once and each job's ~42 dependent thin products serialise on shared-memory bandwidth, DSMEM
+// pushes and cluster barriers
 bool est_cluster_on() {
   static const bool on = [] {
     const char* e = std::getenv("LGM_EST_CLUSTER");
@@ -2857,6 +2858,7 @@ __global__ void __launch_bounds__(256) est_after_fwd_kernel(EstJob* jobs, int n,
 }
 
 // After the adjoint: h = row max |Z|, top-(4t+1) order, picks, stopping test, next X.
+constexpr int ETK_PER = 16;  // rows per lane of the warp top-k (m <= 512)
 struct EstAdjSmem {
   uint64_t skey[8];
   int sidx[8];
@@ -2877,24 +2879,65 @@ __device__ void est_after_adj_impl(EstJob& J, int n, int sweep, EstAdjSmem& sa) 
   auto zabs = [&](int off) { return cx ? hypot(Z[off], Z[off + m]) : fabs(Z[off]); };
   const int t = m < 2 ? m : 2;
   const int ntop = m < 4 * t + 1 ? m : 4 * t + 1;
-  // repeated block argmax over h with exclusion of already taken rows
-  for (int qq = 0; qq < ntop; ++qq) {
-    uint64_t key = 0ull;
-    int idx = 0x7fffffff;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      bool taken = false;
-      for (int u = 0; u < qq; ++u) taken |= (order[u] == i);
-      if (taken) continue;
-      double h = zabs(i);
-      if (nc > 1) h = fmax(h, zabs(n + i));
-      uint64_t kq = dkey(h);
-      if (kq > key) { key = kq; idx = i; }
+  if (m <= 32 * ETK_PER) {
+    // warp 0: lane l keeps the keys of rows l + 32 e in registers; ntop rounds of a warp
+    // argmax (max key, ties -> lowest row), the winner's key cleared -- the same order as the
+    // repeated block argmax below, without a block barrier per round
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint64_t kk[ETK_PER];
+#pragma unroll
+      for (int e = 0; e < ETK_PER; ++e) {
+        const int i = lane + 32 * e;
+        uint64_t k = 0ull;
+        if (i < m) {
+          double h = zabs(i);
+          if (nc > 1) h = fmax(h, zabs(n + i));
+          k = dkey(h);
+        }
+        kk[e] = k;
+      }
+      for (int qq = 0; qq < ntop; ++qq) {
+        uint64_t key = 0ull;
+        int idx = 0x7fffffff;
+#pragma unroll
+        for (int e = 0; e < ETK_PER; ++e)
+          if (kk[e] > key) { key = kk[e]; idx = lane + 32 * e; }  // rows ascend with e: ties keep the lowest
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, key, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+          if (k2 > key || (k2 == key && i2 < idx)) { key = k2; idx = i2; }
+        }
+        if ((idx & 31) == lane) {
+#pragma unroll
+          for (int e = 0; e < ETK_PER; ++e)
+            if (lane + 32 * e == idx) kk[e] = 0ull;
+        }
+        if (lane == 0) { order[qq] = idx; hval[qq] = __longlong_as_double((long long)(key - 1ull)); }
+      }
     }
-    uint64_t kmax;
-    int p;
-    block_argmax(key, idx, skey, sidx, kmax, p);
-    if (threadIdx.x == 0) { order[qq] = p; hval[qq] = __longlong_as_double((long long)(kmax - 1ull)); }
     __syncthreads();
+  } else {
+    // repeated block argmax over h with exclusion of already taken rows
+    for (int qq = 0; qq < ntop; ++qq) {
+      uint64_t key = 0ull;
+      int idx = 0x7fffffff;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        bool taken = false;
+        for (int u = 0; u < qq; ++u) taken |= (order[u] == i);
+        if (taken) continue;
+        double h = zabs(i);
+        if (nc > 1) h = fmax(h, zabs(n + i));
+        uint64_t kq = dkey(h);
+        if (kq > key) { key = kq; idx = i; }
+      }
+      uint64_t kmax;
+      int p;
+      block_argmax(key, idx, skey, sidx, kmax, p);
+      if (threadIdx.x == 0) { order[qq] = p; hval[qq] = __longlong_as_double((long long)(kmax - 1ull)); }
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) {
     double mm = J.mm;
@@ -3040,39 +3083,148 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
 }
 
 // ------------------------------------------------------------------------------------------
-// The whole estimate of one job per thread-block cluster (EST_FUSED_MAXN < n <= 512): the CL
-// CTAs of the cluster hold M1's rows in shared memory (rank r owns rows [r R, (r+1) R),
-// R = ceil(n / CL) <= 32) for every thin product of every sweep, instead of streaming M1
-// from HBM once per product.  Forward products are row-local (warp per row, lane-strided FMAs
-// and a butterfly, as est_fwd_kernel) followed by an all-gather of the row segments over
-// DSMEM; adjoint products form per-CTA column partials over the CTA's rows (4 interleaved
-// accumulators), reduce-scatter them in rank order over DSMEM and all-gather the column
-// segments.  The after-bodies (norms, argmax, top-k, history, stop tests) run redundantly on
-// every CTA's identical local copy of the vectors and job state; rank 0 publishes the result.
-// One cluster barrier per forward product, two per adjoint product.
+// The whole estimate of one job per thread-block cluster (EST_FUSED_MAXN < n <= 512), M1
+// resident in the cluster's shared memory for every thin product of every sweep instead of
+// streamed from HBM once per product.  The cluster has CL = 2 ceil(n / 64) CTAs (<= 16): CTA
+// q = 2 s + h holds the rows of the per-step adjoint's 64-row slab s whose residue u (mod 4)
+// inside the slab's full 4-row groups is 2h or 2h + 1, plus (h = 0) the slab's remainder rows,
+// so every reduction is the per-step kernels' own (bit-identical estimates):
+//  * forward y = M x: a warp per row, lane-strided FMAs + butterfly (est_fwd_kernel); the row
+//    results are pushed into every CTA's copy of y (DSMEM stores), one cluster barrier;
+//  * adjoint z = M^T x: per column the CTA forms its two interleaved accumulators of the slab
+//    (a_2h, a_2h+1, remainder rows into a_0) and their sum -- half of est_adj_kernel's
+//    (a0 + a1) + (a2 + a3) -- and pushes it to the column's owner CTA; barrier; the owner adds
+//    the slab halves and the slabs in order (est_adj_reduce_kernel) and pushes the column into
+//    every CTA's y; barrier.
+// The after-bodies (norms, argmax, top-k, history, stop tests) run redundantly on every CTA's
+// identical local copy of the vectors and job state (one barrier after each, so no push of
+// the next product lands in a vector a slower peer still reads); rank 0 publishes the result.
 constexpr int ECL_NT = 256;
-constexpr int ECL_MAXR = 32;
+constexpr int ECL_MAXR = 32;   // rows per CTA
+constexpr int ECL_MAXC = 32;   // adjoint columns owned per CTA
+constexpr int ECL_MAXCL = 16;
 struct EclSmem {
   EstJob S;           // this CTA's copy of the job state (V0 / V1 / hist point into shared)
   double sred[8];
   EstAdjSmem sa;
   int hist[16];
+  int grow[ECL_MAXR];                 // local row -> global row
+  double own[2][ECL_MAXC];            // owned adjoint columns (both vectors)
 };
-template <int CL>
-__global__ void __launch_bounds__(ECL_NT, 1) est_cluster_kernel(EstJob* jobs, int n, double rsum, int itmax) {
+inline int ecl_cl(int n) { return 2 * ((n + 63) / 64); }
+inline size_t ecl_smem(int n) {
+  return ((size_t)ECL_MAXR * n + 4 * (size_t)n + (size_t)ECL_MAXCL * 2 * ECL_MAXC) * 8;
+}
+// forward rows lr0 .. lr0 + nr - 1 of the cluster estimator (est_fwd_kernel's per-row order):
+// from shared memory (M1) or, for the product form's first step, from M2 in global memory
+template <bool GM>
+__device__ __forceinline__ void ecl_fwd_rows(const double* M2, const int* grow, const double* Ms, int n, int lr0,
+                                             int nr, int nc, const double* x, int lane, double (&a0)[4],
+                                             double (&a1)[4]) {
+  const double* Mr[4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int lr = lr0 + (rr < nr ? rr : nr - 1);
+    Mr[rr] = GM ? M2 + (size_t)grow[lr] * n : Ms + (size_t)lr * n;
+  }
+#pragma unroll 4
+  for (int j = lane; j < n; j += 32) {
+    const double x0 = x[j], x1 = nc > 1 ? x[n + j] : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      if (rr < nr) {
+        const double m = Mr[rr][j];
+        a0[rr] = fma(m, x0, a0[rr]);
+        if (nc > 1) a1[rr] = fma(m, x1, a1[rr]);
+      }
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0[rr] += __shfl_xor_sync(0xffffffffu, a0[rr], o);
+      a1[rr] += __shfl_xor_sync(0xffffffffu, a1[rr], o);
+    }
+  }
+}
+// adjoint slab halves of columns tid and tid + ECL_NT (est_adj_kernel's accumulators a_2h,
+// a_2h+1, remainder rows into a_0), pushed to each column's owner CTA
+template <bool GM>
+__device__ __forceinline__ void ecl_adj_cols(const double* M2, const int* grow, const double* Ms, int n, int NG, int R,
+                                             bool two, const double* x, int tid, int rank, int RC, double* recv,
+                                             cooperative_groups::cluster_group& cl) {
+  const int c0 = tid, c1 = tid + ECL_NT;
+  const bool v0 = c0 < n, v1 = c1 < n;
+  const int d0 = v0 ? c0 : 0, d1 = v1 ? c1 : 0;
+  double lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [column][vector]
+#pragma unroll 2
+  for (int i = 0; i < NG; ++i) {
+    const int g0 = grow[2 * i], g1 = grow[2 * i + 1];
+    const double* r0 = GM ? M2 + (size_t)g0 * n : Ms + (size_t)(2 * i) * n;
+    const double* r1 = GM ? M2 + (size_t)g1 * n : Ms + (size_t)(2 * i + 1) * n;
+    const double m00 = r0[d0], m10 = r1[d0], m01 = r0[d1], m11 = r1[d1];
+    const double xa = x[g0], xb = x[g1];
+    lo[0][0] = fma(m00, xa, lo[0][0]);
+    hi[0][0] = fma(m10, xb, hi[0][0]);
+    lo[1][0] = fma(m01, xa, lo[1][0]);
+    hi[1][0] = fma(m11, xb, hi[1][0]);
+    if (two) {
+      const double ya = x[n + g0], yb = x[n + g1];
+      lo[0][1] = fma(m00, ya, lo[0][1]);
+      hi[0][1] = fma(m10, yb, hi[0][1]);
+      lo[1][1] = fma(m01, ya, lo[1][1]);
+      hi[1][1] = fma(m11, yb, hi[1][1]);
+    }
+  }
+  for (int lr = 2 * NG; lr < R; ++lr) {  // remainder rows (h = 0): accumulator a_0
+    const int g = grow[lr];
+    const double* rr = GM ? M2 + (size_t)g * n : Ms + (size_t)lr * n;
+    const double ma = rr[d0], mb = rr[d1];
+    lo[0][0] = fma(ma, x[g], lo[0][0]);
+    lo[1][0] = fma(mb, x[g], lo[1][0]);
+    if (two) {
+      lo[0][1] = fma(ma, x[n + g], lo[0][1]);
+      lo[1][1] = fma(mb, x[n + g], lo[1][1]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int c = k ? c1 : c0;
+    if (k ? v1 : v0) {
+      const int ow = c / RC, oc = c - ow * RC;
+      double* rv = cl.map_shared_rank(recv, ow);
+      rv[(rank * 2 + 0) * ECL_MAXC + oc] = lo[k][0] + hi[k][0];
+      rv[(rank * 2 + 1) * ECL_MAXC + oc] = lo[k][1] + hi[k][1];
+    }
+  }
+}
+#ifdef ECL_PROF  // clock64 phase split of job 0's estimate (rank 0, thread 0), printed per launch
+#define ECL_T(v) long long v = clock64()
+#define ECL_ADD(i, a, b) ecl_cyc[i] += (b) - (a)
+#else
+#define ECL_T(v)
+#define ECL_ADD(i, a, b)
+#endif
+template <bool CX>
+__global__ void __launch_bounds__(ECL_NT, 1) est_cluster_kernel(EstJob* jobs, int n, double rsum, double rsum_c,
+                                                                int itmax) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double ecl[];
   __shared__ EclSmem es;
+  const int CL = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
   EstJob& G = jobs[blockIdx.x / CL];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int R = (n + CL - 1) / CL;             // rows (and adjoint columns) per CTA
-  const int r0 = rank * R, r1 = min(n, r0 + R);
-  double* Ms = ecl;                             // [R][n] rows r0.. of M1
+  double* Ms = ecl;                             // [ECL_MAXR][n] my rows of M1 (local order)
   double* V0 = Ms + (size_t)ECL_MAXR * n;       // [2][n]
   double* V1 = V0 + 2 * n;                      // [2][n]
-  double* part = V1 + 2 * n;                    // [2][n] column partials over this CTA's rows
+  double* recv = V1 + 2 * n;                    // [CL][2][ECL_MAXC] adjoint slab halves
+#ifdef ECL_PROF
+  long long ecl_cyc[10] = {};
+#endif
+  ECL_T(t_init);
   const bool dead = !G.live || (G.zchk && !G.nzf);
   if (dead) {  // (uniform over the cluster: every CTA reads the same job)
     if (rank == 0 && tid == 0) {
@@ -3083,118 +3235,159 @@ __global__ void __launch_bounds__(ECL_NT, 1) est_cluster_kernel(EstJob* jobs, in
     }
     return;
   }
+  // my rows: slab s, half h (see above)
+  const int s = rank >> 1, h = rank & 1;
+  const int L = min(64, n - 64 * s), NG = L >> 2, rem = L & 3;
+  const int R = 2 * NG + (h == 0 ? rem : 0);
+  const int RC = (n + CL - 1) / CL;             // adjoint columns owned per CTA
+  if (tid < ECL_MAXR) {
+    const int lr = tid;
+    es.grow[lr] = lr < 2 * NG ? 64 * s + 4 * (lr >> 1) + 2 * h + (lr & 1) : 64 * s + 4 * NG + (lr - 2 * NG);
+  }
   EstJob& S = es.S;
   if (tid == 0) {
     S = G;
     S.V0 = V0;
     S.V1 = V1;
     S.hist = es.hist;
-    const int t = n < 2 ? n : 2;
-    S.est = 0.0; S.best_j = 0; S.ncols = t; S.nhist = 0; S.passes = 0; S.mm = INFINITY;
-    S.total = S.p1 + (S.M2 ? 1 : 0);
-    S.done = 0;
   }
-  for (int i = tid; i < n; i += ECL_NT) {
-    V0[i] = 1.0 / n;
-    if (n > 1) V0[n + i] = (((i & 1) ? -1.0 : 1.0) * (1.0 + (double)i / (double)(n > 1 ? n - 1 : 1))) / rsum;
-  }
-  for (size_t idx = tid; idx < (size_t)(r1 - r0) * n; idx += ECL_NT) Ms[idx] = G.M1[(size_t)r0 * n + idx];
   __syncthreads();
+  {
+    const int t = est_x0(S, n, rsum, rsum_c, tid, ECL_NT);
+    if (tid == 0) {
+      S.est = 0.0; S.best_j = 0; S.ncols = t; S.nhist = 0; S.passes = 0; S.mm = INFINITY;
+      S.total = S.p1 + (S.M2 ? 1 : 0);
+      S.done = 0;
+    }
+  }
+  for (int lr0 = 0; lr0 < R; lr0 += ECL_NT / 32) {  // warp per row, all of a lane's loads in flight
+    const int lr = lr0 + warp;
+    if (lr < R) {
+      const double* src = G.M1 + (size_t)es.grow[lr] * n;
+      double* dst = Ms + (size_t)lr * n;
+      if ((n & 1) == 0) {
+        double2 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 2 * lane + 64 * e;
+          if (j < n) v[e] = *reinterpret_cast<const double2*>(src + j);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 2 * lane + 64 * e;
+          if (j < n) *reinterpret_cast<double2*>(dst + j) = v[e];
+        }
+      } else {
+        double v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int j = lane + 32 * e;
+          if (j < n) v[e] = src[j];
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int j = lane + 32 * e;
+          if (j < n) dst[j] = v[e];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  cl.sync();  // every CTA's vectors initialised before the first push
+  ECL_T(t_ld);
+  ECL_ADD(0, t_init, t_ld);
   const int total = S.total, p1 = S.p1;
   const double* M2 = S.M2;
   for (int sweep = 0; sweep < itmax; ++sweep) {
     if (S.done) break;
     const int nc = S.ncols;
-    for (int q = 0; q < total; ++q) {  // forward: y = M x, my rows, then all-gather
+    for (int q = 0; q < total; ++q) {  // forward: y = M x for my rows, pushed to every CTA
+      ECL_T(f0);
       const bool use2 = M2 && q == 0;
       const double* x = (q & 1) ? V1 : V0;
       double* y = (q & 1) ? V0 : V1;
-      for (int i = r0 + warp; i < r1; i += ECL_NT / 32) {
-        const double* Mr = use2 ? M2 + (size_t)i * n : Ms + (size_t)(i - r0) * n;
-        double a0 = 0.0, a1 = 0.0;
-        for (int j = lane; j < n; j += 32) {
-          const double m = Mr[j];
-          a0 = fma(m, x[j], a0);
-          if (nc > 1) a1 = fma(m, x[n + j], a1);
-        }
+      const int lr0 = warp * 4;
+      if (lr0 < R) {
+        const int nr = min(4, R - lr0);
+        double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+        if (use2) ecl_fwd_rows<true>(M2, es.grow, Ms, n, lr0, nr, nc, x, lane, a0, a1);
+        else ecl_fwd_rows<false>(M2, es.grow, Ms, n, lr0, nr, nc, x, lane, a0, a1);
+        ECL_T(f1);
+        ECL_ADD(1, f0, f1);
+        if (lane < CL) {  // lane p stores the warp's rows into CTA p's y
+          double* ry = cl.map_shared_rank(y, lane);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        }
-        if (lane == 0) {
-          y[i] = a0;
-          if (nc > 1) y[n + i] = a1;
+          for (int rr = 0; rr < 4; ++rr) {
+            if (rr < nr) {
+              const int gi = es.grow[lr0 + rr];
+              ry[gi] = a0[rr];
+              if (nc > 1) ry[n + gi] = a1[rr];
+            }
+          }
         }
       }
+      ECL_T(f2);
       cl.sync();
-      for (int p = 0; p < CL; ++p) {
-        if (p == rank) continue;
-        const int q0 = p * R, q1 = min(n, q0 + R);
-        const double* ry = cl.map_shared_rank(y, p);
-        for (int i = q0 + tid; i < q1; i += ECL_NT) {
-          y[i] = ry[i];
-          if (nc > 1) y[n + i] = ry[n + i];
-        }
-      }
-      __syncthreads();
+      ECL_T(f3);
+      ECL_ADD(2, f0, f2);
+      ECL_ADD(3, f2, f3);
     }
-    cl.sync();  // every peer's gather done before the after-body rewrites the vectors in place
-    est_after_fwd_body(S, n, sweep, es.sred);
+    ECL_T(af0);
+    est_after_fwd_impl<CX>(S, n, sweep, es.sred);
     __syncthreads();
+    ECL_T(af1);
+    ECL_ADD(4, af0, af1);
+    cl.sync();  // no push of the adjoint lands in a vector a slower peer's after-body reads
     if (S.done) break;
     const bool two = S.ncols > 1;
-    for (int q = 0; q < total; ++q) {  // adjoint: z = M^T x, partials, reduce-scatter, gather
+    for (int q = 0; q < total; ++q) {  // adjoint: slab halves -> owner -> every CTA
+      ECL_T(a0t);
       const bool use2 = q >= p1;
       const double* x = (q & 1) ? V1 : V0;
       double* y = (q & 1) ? V0 : V1;
-      for (int c = tid; c < n; c += ECL_NT) {
-        double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
-        int r = r0;
-        for (; r + 3 < r1; r += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double m = use2 ? M2[(size_t)(r + u) * n + c] : Ms[(size_t)(r + u - r0) * n + c];
-            a0[u] = fma(m, x[r + u], a0[u]);
-            if (two) a1[u] = fma(m, x[n + r + u], a1[u]);
-          }
-        }
-        for (; r < r1; ++r) {
-          const double m = use2 ? M2[(size_t)r * n + c] : Ms[(size_t)(r - r0) * n + c];
-          a0[0] = fma(m, x[r], a0[0]);
-          if (two) a1[0] = fma(m, x[n + r], a1[0]);
-        }
-        part[c] = (a0[0] + a0[1]) + (a0[2] + a0[3]);
-        part[n + c] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
-      }
+      if (use2) ecl_adj_cols<true>(M2, es.grow, Ms, n, NG, R, two, x, tid, rank, RC, recv, cl);
+      else ecl_adj_cols<false>(M2, es.grow, Ms, n, NG, R, two, x, tid, rank, RC, recv, cl);
+      ECL_T(a1t);
       cl.sync();
-      for (int c = r0 + tid; c < r1; c += ECL_NT) {  // my column block, summed in rank order
+      ECL_T(a2t);
+      ECL_ADD(5, a0t, a1t);
+      ECL_ADD(6, a1t, a2t);
+      const int c0 = rank * RC, nown = max(0, min(RC, n - c0));
+      if (tid < nown) {  // my columns: slab halves, then slabs in order, from 0.0
         double s0 = 0.0, s1 = 0.0;
-        for (int p = 0; p < CL; ++p) {
-          const double* rp = cl.map_shared_rank(part, p);
-          s0 += rp[c];
-          s1 += rp[n + c];
+        for (int sl = 0; sl < CL / 2; ++sl) {
+          s0 += recv[((2 * sl) * 2 + 0) * ECL_MAXC + tid] + recv[((2 * sl + 1) * 2 + 0) * ECL_MAXC + tid];
+          s1 += recv[((2 * sl) * 2 + 1) * ECL_MAXC + tid] + recv[((2 * sl + 1) * 2 + 1) * ECL_MAXC + tid];
         }
-        y[c] = s0;
-        if (two) y[n + c] = s1;
-      }
-      cl.sync();
-      for (int p = 0; p < CL; ++p) {
-        if (p == rank) continue;
-        const int q0 = p * R, q1 = min(n, q0 + R);
-        const double* ry = cl.map_shared_rank(y, p);
-        for (int c = q0 + tid; c < q1; c += ECL_NT) {
-          y[c] = ry[c];
-          if (two) y[n + c] = ry[n + c];
-        }
+        es.own[0][tid] = s0;
+        es.own[1][tid] = s1;
       }
       __syncthreads();
+      for (int idx = tid; idx < nown * CL; idx += ECL_NT) {
+        const int p = idx / nown, oc = idx - p * nown;
+        double* ry = cl.map_shared_rank(y, p);
+        ry[c0 + oc] = es.own[0][oc];
+        if (two) ry[n + c0 + oc] = es.own[1][oc];
+      }
+      ECL_T(a3t);
+      cl.sync();
+      ECL_T(a4t);
+      ECL_ADD(7, a2t, a3t);
+      ECL_ADD(8, a3t, a4t);
     }
-    cl.sync();
-    est_after_adj_body(S, n, sweep, es.sa);
+    ECL_T(aa0);
+    est_after_adj_impl<CX>(S, n, sweep, es.sa);
     __syncthreads();
+    cl.sync();
+    ECL_T(aa1);
+    ECL_ADD(9, aa0, aa1);
   }
-  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+#ifdef ECL_PROF
+  if (blockIdx.x < (unsigned)CL && rank == 0 && tid == 0)
+    printf("ecl job0 cycles: load %lld fwd_comp %lld fwd_all %lld fwd_sync %lld after_fwd %lld adj_comp+push %lld "
+           "adj_sync1 %lld adj_owner+push %lld adj_sync2 %lld after_adj %lld (passes %d)\n", ecl_cyc[0], ecl_cyc[1],
+           ecl_cyc[2], ecl_cyc[3], ecl_cyc[4], ecl_cyc[5], ecl_cyc[6], ecl_cyc[7], ecl_cyc[8], ecl_cyc[9], S.passes);
+#endif
   if (rank == 0 && tid == 0) {
     G.est = S.est;
     G.best_j = S.best_j;
@@ -3203,7 +3396,6 @@ __global__ void __launch_bounds__(ECL_NT, 1) est_cluster_kernel(EstJob* jobs, in
     G.done = 1;
   }
 }
-inline size_t ecl_smem(int n) { return ((size_t)ECL_MAXR * n + 6 * (size_t)n) * 8; }
 
 // ------------------------------------------------------------------------------------------
 // Graph-polynomial GEMM: C = L * R, L = sum_t c_t * P_t + c0 * I built on the fly in the
@@ -4713,7 +4905,7 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
     return 0;
   }
   if (n > EST_FUSED_MAXN && n <= 512 && est_cluster_on()) {  // M1 resident in a cluster's smem
-    const int cl = n <= 256 ? 8 : 16;
+    const int cl = ecl_cl(n);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nj * cl);
     cfg.blockDim = dim3(ECL_NT);
@@ -4726,8 +4918,8 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cl == 8) CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<8>, C.c.est, n, rsum, C.itmax)));
-    else CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<16>, C.c.est, n, rsum, C.itmax)));
+    if (C.cplx) CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<true>, C.c.est, n, rsum, rsum_c, C.itmax)));
+    else CK((cap_launch(), cudaLaunchKernelEx(&cfg, est_cluster_kernel<false>, C.c.est, n, rsum, rsum_c, C.itmax)));
     return 0;
   }
   GL est_init_kernel<<<dim3((n + 255) / 256, nj), 256, 0, st>>>(C.c.est, n, rsum, rsum_c);
@@ -5280,9 +5472,10 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(expm_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(poly_gemm_kernel<false>, mx, (int)(2 * (size_t)(GP_A + GP_B) * 8)));
   CK(cudaFuncSetAttribute(gj_update2_tma_kernel, mx, (int)ut_smem()));
-  CK(cudaFuncSetAttribute(est_cluster_kernel<8>, mx, (int)ecl_smem(512)));
-  CK(cudaFuncSetAttribute(est_cluster_kernel<16>, mx, (int)ecl_smem(512)));
-  CK(cudaFuncSetAttribute(est_cluster_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<false>, mx, (int)ecl_smem(512)));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<true>, mx, (int)ecl_smem(512)));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(est_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(balance_kernel_g, mx, (int)bal_smem(n)));
   return 0;
 }

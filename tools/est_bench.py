@@ -20,7 +20,7 @@ B = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 p = int(sys.argv[3]) if len(sys.argv) > 3 else 7
 prod = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 5
-lib = _lib.load()
+lib = _lib.load(os.environ.get("LGM_LIB", _lib.LIB_PATH))
 A = synth.config(4, batch=B, n=n)
 A = A / np.abs(A).sum(axis=1).max(axis=1)[:, None, None] * 0.5  # A_I2-like scale
 M = torch.from_numpy(A).cuda()
