@@ -111,6 +111,16 @@ bool up2s_on() {
   return on;
 }
 
+// Two-rows-per-thread pair panel for 256 < n <= 512 (gj_panel_pair2_kernel; LGM_PANEL2=0 selects
+// the one-row-per-thread gj_panel_pair_kernel<512>; bit-identical results)
+bool panel2_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_PANEL2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // One-launch estimator for n <= EST_FUSED_MAXN (LGM_EST_FUSED=0 selects the per-step kernels)
 bool est_fused_on() {
   static const bool on = [] {  // thread-safe once-init
@@ -887,6 +897,233 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_panel_pair_kernel(const InvJo
   __threadfence_block();
   __syncthreads();
   panel_body<NT>(J, n, k0 + NB, NB, -1, a1_kind, ps, ptile);
+}
+
+// Two rows per thread (256 < n <= 512, n % 32 == 0, full 32-column panels): the pivot loop of
+// panel_body is bound by the shared-memory return path, not by latency -- every thread reads
+// the whole 256-byte pivot row each step (512 threads x 256 B = 128 KB = 1024 cycles at 128
+// B/clk/SM, the measured ~1.1k cycles per step), four times the FP64 pipe's 256 cycles.  Here
+// thread `tid` of 256 owns rows tid and tid + 256, so one set of pivot-row loads feeds two
+// rows' FMAs (64 KB per step).  Pivot rule, FMA chains, stage-1 DMMA products and the order
+// of the log|det| sum are those of panel_body<512>: results are bit-identical.
+struct Panel2Smem {
+  double prow[2][40];
+  unsigned wkey32[2][8];
+  double wval[2][8];
+  double red[16];
+  int piv_s[32];
+  double w1s[32][34];
+};
+__device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int a1_kind, int s1_a1kind, Panel2Smem& ps,
+                                            double* ptile) {
+  constexpr int NT2 = 256, NW = 8;
+  auto& prow = ps.prow;
+  auto& wkey32 = ps.wkey32;
+  auto& wval = ps.wval;
+  auto& red = ps.red;
+  auto& piv_s = ps.piv_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row0 = tid, row1 = tid + NT2;
+  const int base0 = warp * 32, base1 = NT2 + warp * 32;  // the warp's 32 rows in slot 0 / slot 1
+  const bool v1 = base1 < n;                            // warp-uniform (n % 32 == 0); slot 0 is always valid
+  bool used0 = J.rowstep[row0] >= 0;
+  bool used1 = v1 ? (J.rowstep[row1] >= 0) : true;
+  double r0[32], r1[32];
+  double* M = J.M;
+  const double* Mi = (J.Src && k0 < 2 * NB) ? J.Src : M;
+  double* T = ptile + warp * 32 * 33;
+  // both slots' global loads in flight first (r0 / r1 as transposed temporaries)
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) r0[rr] = Mi[(size_t)(base0 + rr) * n + k0 + lane];
+  if (v1) {
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) r1[rr] = Mi[(size_t)(base1 + rr) * n + k0 + lane];
+  }
+  if (s1_a1kind >= 0) {
+    auto& w1s = ps.w1s;
+    const int p1 = k0 - NB;
+    for (int idx = tid; idx < 32 * 32; idx += NT2) {
+      const int c1 = idx >> 5, c = idx & 31;
+      w1s[c1][c] = Mi[(size_t)J.piv[p1 + c1] * n + k0 + c];
+    }
+    __syncthreads();
+  }
+  // per slot: transpose through the warp's tile (with P1's stage-1 update on DMMA for P2)
+  auto stage = [&](double (&r)[32], int base) {
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = r[rr];
+    __syncwarp();
+    if (s1_a1kind >= 0) {
+      auto& w1s = ps.w1s;
+      const int p1 = k0 - NB;
+      const int g = lane >> 2, t4 = lane & 3;
+      double acc[4][4][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int rs = J.rowstep[base + mi * 8 + g];
+        const bool z1 = !(rs >= p1 && rs < k0);  // P1 pivot rows restart from zero
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc[mi][ni][e] = z1 ? T[(mi * 8 + g) * 33 + ni * 8 + 2 * t4 + e] : 0.0;
+      }
+      const double* a1 = wkind(J, s1_a1kind) + (size_t)base * NB;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = a1[(size_t)(mi * 8 + g) * NB + k + t4];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) b[ni] = w1s[k + t4][ni * 8 + g];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) T[(mi * 8 + g) * 33 + ni * 8 + 2 * t4 + e] = acc[mi][ni][e];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r[c] = T[lane * 33 + c];
+    __syncwarp();
+  };
+  stage(r0, base0);
+  if (v1) {
+    stage(r1, base1);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r1[c] = 0.0;
+  }
+  double rowscale0 = 1.0, rowscale1 = 1.0, mypiv0 = 1.0, mypiv1 = 1.0;
+  int my_step0 = -1, my_step1 = -1;
+  __syncthreads();
+#pragma unroll 1
+  for (int kk = 0; kk < 32; ++kk) {
+    const int par = kk & 1;
+    const double* pr = prow[par];
+    const double a0 = r0[0], a1 = r1[0];
+    const bool cand0 = !used0 && a0 != 0.0;
+    const bool cand1 = !used1 && a1 != 0.0;
+    const unsigned key0 =
+        cand0 ? ((((unsigned)__double2hiint(a0) & 0x7fffffffu) & ~0x3ffu) | (unsigned)(1023 - row0)) : 0u;
+    const unsigned key1 =
+        cand1 ? ((((unsigned)__double2hiint(a1) & 0x7fffffffu) & ~0x3ffu) | (unsigned)(1023 - row1)) : 0u;
+    const unsigned wk = __reduce_max_sync(0xffffffffu, key0 > key1 ? key0 : key1);
+    const int wrow = 1023 - (int)(wk & 0x3ffu);  // the warp's winning row (warp-uniform)
+    const double wv = __shfl_sync(0xffffffffu, wrow >= NT2 ? a1 : a0, wrow & 31);
+    if (lane == 0) {
+      wkey32[par][warp] = wk;
+      wval[par][warp] = wv;
+    }
+    __syncthreads();
+    const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par][lane] : 0u);
+    if (bk == 0u) {  // exact zero pivot (matcore.py:124-125)
+      if (tid == 0) *J.status = 1;
+      return false;
+    }
+    const int p = 1023 - (int)(bk & 0x3ffu);
+    const double rp = lgm_rcp(wval[par][(p & (NT2 - 1)) >> 5]);
+    const bool own0 = (row0 == p), own1 = (row1 == p);
+    if (own0) {
+      used0 = true;
+      mypiv0 = a0;
+      rowscale0 = rp;
+      double* pw = prow[par];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r0[c], r0[c + 1]);
+      my_step0 = k0 + kk;
+      piv_s[kk] = p;
+    }
+    if (own1) {
+      used1 = true;
+      mypiv1 = a1;
+      rowscale1 = rp;
+      double* pw = prow[par];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r1[c], r1[c + 1]);
+      my_step1 = k0 + kk;
+      piv_s[kk] = p;
+    }
+    __syncthreads();
+    const double g0 = own0 ? 0.0 : a0 * rp, g1 = own1 ? 0.0 : a1 * rp;
+    const double last0 = own0 ? 1.0 : -g0, last1 = own1 ? 1.0 : -g1;
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(pr + c);
+      if (c > 0) {
+        r0[c - 1] = fma(-g0, p2.x, r0[c]);
+        r1[c - 1] = fma(-g1, p2.x, r1[c]);
+      }
+      r0[c] = fma(-g0, p2.y, r0[c + 1]);
+      r1[c] = fma(-g1, p2.y, r1[c + 1]);
+    }
+    r0[31] = last0;
+    r1[31] = last1;
+  }
+  const bool ph0 = my_step0 >= 0, ph1 = my_step1 >= 0;
+  if (ph0) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r0[c] *= rowscale0;
+    J.rowstep[row0] = my_step0;
+  }
+  if (ph1) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) r1[c] *= rowscale1;
+    J.rowstep[row1] = my_step1;
+  }
+  if (tid < 32) J.piv[k0 + tid] = piv_s[tid];
+  double* A1 = a1_kind >= 0 ? wkind(J, a1_kind) : nullptr;  // rank-64 pair: P1's multipliers
+  auto unstage = [&](const double (&r)[32], int base) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) T[lane * 33 + c] = r[c];
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) {
+      const double v = T[rr * 33 + lane];
+      M[(size_t)(base + rr) * n + k0 + lane] = v;
+      if (A1) A1[(size_t)(base + rr) * NB + lane] = v;
+    }
+    __syncwarp();
+  };
+  unstage(r0, base0);
+  if (v1) unstage(r1, base1);
+  // log|det| of this panel's pivots: per 32-row group a butterfly sum, groups added in row
+  // order (panel_body<512>'s warp order), one update per panel
+  double lg0 = ph0 ? log(fabs(mypiv0)) : 0.0, lg1 = ph1 ? log(fabs(mypiv1)) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lg0 += __shfl_xor_sync(0xffffffffu, lg0, o);
+    lg1 += __shfl_xor_sync(0xffffffffu, lg1, o);
+  }
+  if (lane == 0) {
+    red[warp] = lg0;
+    red[NW + warp] = lg1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 2 * NW; ++w) t += red[w];
+    *J.logdet += t;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(256, 1) gj_panel_pair2_kernel(const InvJob* jobs, int n, int k0, int a1_kind) {
+  __shared__ __align__(16) Panel2Smem ps;
+  extern __shared__ __align__(16) double ptile[];
+  const InvJob J = jobs[blockIdx.x];
+  if (*J.status) return;
+  if (threadIdx.x < 80) (&ps.prow[0][0])[threadIdx.x] = 0.0;
+  if (!panel2_body(J, n, k0, a1_kind, -1, ps, ptile)) return;
+  __threadfence_block();
+  __syncthreads();
+  panel2_body(J, n, k0 + NB, -1, a1_kind, ps, ptile);
 }
 
 __global__ void __launch_bounds__(512) gj_panel_kernel(const InvJob* jobs, int n, int k0, int nb, int in_smem) {
@@ -5036,6 +5273,7 @@ int cap_invert(Cap& C, cudaStream_t st, int nj) {
     auto panel_pair = [&](int k0p, cudaStream_t s, int a1k) {  // both panels of a pair, one launch
       if (n <= 128) GL gj_panel_pair_kernel<128><<<nj, 128, 4 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
       else if (n <= 256) GL gj_panel_pair_kernel<256><<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
+      else if (panel2_on() && n % 32 == 0) GL gj_panel_pair2_kernel<<<nj, 256, 8 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
       else GL gj_panel_pair_kernel<512><<<nj, 512, 16 * 32 * 33 * 8, s>>>(d_jobs, n, k0p, a1k);
     };
     auto pass = [&](int k0p, int cb, int clo, int chi, int exlo, int exhi, int qq, bool narrow) {
@@ -5462,6 +5700,7 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(gj_panel_pair_kernel<128>, mx, 4 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_panel_pair_kernel<256>, mx, 8 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_panel_pair_kernel<512>, mx, 16 * 32 * 33 * 8));
+  CK(cudaFuncSetAttribute(gj_panel_pair2_kernel, mx, 8 * 32 * 33 * 8));
   CK(cudaFuncSetAttribute(gj_update2_kernel<64>, mx, (int)up2_smem<64>()));
   CK(cudaFuncSetAttribute(gj_update2_kernel<128>, mx, (int)up2_smem<128>()));
   CK(cudaFuncSetAttribute(gj_update2s_kernel<64>, mx, (int)up2s_smem<64>()));
