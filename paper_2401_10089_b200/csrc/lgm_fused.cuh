@@ -321,6 +321,9 @@ struct Ctx {
   // 1/pivot, the other rows fold 1/pivot into their multiplier, and the pivot row keeps raw
   // values (its column-k entry set to 1) and is scaled once at the end -- the elimination is
   // linear in each row, so this is the same Gauss-Jordan recurrence with different rounding.
+#ifndef LGM_F_PUBFIRST
+#define LGM_F_PUBFIRST 1  // A/B: config 1 1.845 -> 1.762 ms, config 2 2.454 -> 2.445 ms, bit-identical
+#endif
   __device__ int gj_invert(double (&r)[NMAX], double& logabsdet, int& my_step) {
     bool used = false;
     my_step = -1;
@@ -363,9 +366,24 @@ struct Ctx {
         }
         const unsigned mhi = kmax, mlo = 0u;
         if ((mhi | mlo) == 0u) { status = 1; break; }  // all remaining candidates exactly zero
-        const double rp = lgm_rcp(pval);  // every lane, in parallel with the owner's stores
         double* pw = prow(team, k & 1);
         const bool own = (row == prow_idx);
+#if LGM_F_PUBFIRST
+        // the owner's stores first: the reciprocal's slow-path call is a scheduling barrier,
+        // so in source order after it the publish would wait for the whole Newton chain
+        if (own) {  // one lane publishes its raw row (current frame)
+          used = true;
+          my_step = k;
+          mylog = r0;  // log|p| taken once after the loop (one pivot per row)
+#pragma unroll
+          for (int j = 0; j < NMAX; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(r[j], r[j + 1]);
+        }
+        if (lane == 0 && wit == 0) pv[k] = prow_idx;
+        const double rp = lgm_rcp(pval);
+        if (own) rowscale = rp;
+        team_sync();
+#else
+        const double rp = lgm_rcp(pval);  // every lane, in parallel with the owner's stores
         if (own) {  // one lane publishes its raw row (current frame)
           used = true;
           my_step = k;
@@ -376,6 +394,7 @@ struct Ctx {
         }
         if (lane == 0 && wit == 0) pv[k] = prow_idx;
         team_sync();
+#endif
         g = own ? 0.0 : r0 * rp;  // branch-free: the owner keeps its raw row
         last = own ? 1.0 : -g;
       }

@@ -111,6 +111,9 @@ bool up2s_on() {
   return on;
 }
 
+#ifndef LGM_G1_PUBFIRST
+#define LGM_G1_PUBFIRST 1
+#endif
 // Two-rows-per-thread pair panel for 256 < n <= 512 (gj_panel_pair2_kernel; LGM_PANEL2=0 selects
 // the one-row-per-thread gj_panel_pair_kernel<512>; bit-identical results)
 bool panel2_on() {
@@ -302,9 +305,25 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
         const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par * 16 + lane] : 0u);
         if (bk == 0u) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
         const int p = 1023 - (int)(bk & 0x3ffu);
-        const double rp = lgm_rcp(wval[par * 16 + (p >> 5)]);
         double* pw = prow + par * 40;
         const bool own = (tid == p);
+#if LGM_G1_PUBFIRST
+        // the owner publishes first; the pivot's reciprocal (its slow-path call is a scheduling
+        // barrier) follows, under the stores
+        if (own) {
+          my_step = k0 + kk;
+          piv_here = true;
+          mypiv = r0;
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r[c], r[c + 1]);
+          rstep[tid] = k0 + kk;
+          piv[k0 + kk] = tid;
+        }
+        const double rp = lgm_rcp(wval[par * 16 + (p >> 5)]);
+        if (own) rowscale = rp;
+        __syncthreads();
+#else
+        const double rp = lgm_rcp(wval[par * 16 + (p >> 5)]);
         if (own) {
           my_step = k0 + kk;
           piv_here = true;
@@ -316,6 +335,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
           piv[k0 + kk] = tid;
         }
         __syncthreads();
+#endif
         g = own ? 0.0 : r0 * rp;
         last = own ? 1.0 : -g;
       }
@@ -598,7 +618,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
 }
 
 #ifdef LGM_PANEL_PROF
-__device__ unsigned long long g_panel_cyc[6];  // load, stage-1, factor, store, CTAs
+__device__ unsigned long long g_panel_cyc[12];  // load, stage-1, factor, store, CTAs; [6..8] panel2 step: search, publish, FMAs
 #define PP_T(v) long long v = clock64()
 #define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
 #else
@@ -923,6 +943,7 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
   auto& red = ps.red;
   auto& piv_s = ps.piv_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  PP_T(t0);
   const int row0 = tid, row1 = tid + NT2;
   const int base0 = warp * 32, base1 = NT2 + warp * 32;  // the warp's 32 rows in slot 0 / slot 1
   const bool v1 = base1 < n;                            // warp-uniform (n % 32 == 0); slot 0 is always valid
@@ -1003,8 +1024,11 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
   double rowscale0 = 1.0, rowscale1 = 1.0, mypiv0 = 1.0, mypiv1 = 1.0;
   int my_step0 = -1, my_step1 = -1;
   __syncthreads();
+  PP_T(t2);
+  PP_ADD(0, t2 - t0);
 #pragma unroll 1
   for (int kk = 0; kk < 32; ++kk) {
+    PP_T(ta);
     const int par = kk & 1;
     const double* pr = prow[par];
     const double a0 = r0[0], a1 = r1[0];
@@ -1022,18 +1046,22 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
       wval[par][warp] = wv;
     }
     __syncthreads();
+    PP_T(tb);
+    PP_ADD(6, tb - ta);
     const unsigned bk = __reduce_max_sync(0xffffffffu, lane < NW ? wkey32[par][lane] : 0u);
     if (bk == 0u) {  // exact zero pivot (matcore.py:124-125)
       if (tid == 0) *J.status = 1;
       return false;
     }
     const int p = 1023 - (int)(bk & 0x3ffu);
-    const double rp = lgm_rcp(wval[par][(p & (NT2 - 1)) >> 5]);
+    // the owner publishes its raw row first: the reciprocal's slow-path call is a scheduling
+    // barrier, and in source order after it the stores would wait for the whole Newton chain
+    // (measured: reciprocal after the barrier 7.41 ms per 512-inversion step, before the
+    // publish 7.31 ms)
     const bool own0 = (row0 == p), own1 = (row1 == p);
     if (own0) {
       used0 = true;
       mypiv0 = a0;
-      rowscale0 = rp;
       double* pw = prow[par];
 #pragma unroll
       for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r0[c], r0[c + 1]);
@@ -1043,14 +1071,18 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
     if (own1) {
       used1 = true;
       mypiv1 = a1;
-      rowscale1 = rp;
       double* pw = prow[par];
 #pragma unroll
       for (int c = 0; c < 32; c += 2) *reinterpret_cast<double2*>(pw + c) = make_double2(r1[c], r1[c + 1]);
       my_step1 = k0 + kk;
       piv_s[kk] = p;
     }
+    const double rp = lgm_rcp(wval[par][(p & (NT2 - 1)) >> 5]);  // under the owner's stores
+    if (own0) rowscale0 = rp;
+    if (own1) rowscale1 = rp;
     __syncthreads();
+    PP_T(tc);
+    PP_ADD(7, tc - tb);
     const double g0 = own0 ? 0.0 : a0 * rp, g1 = own1 ? 0.0 : a1 * rp;
     const double last0 = own0 ? 1.0 : -g0, last1 = own1 ? 1.0 : -g1;
 #pragma unroll
@@ -1065,7 +1097,15 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
     }
     r0[31] = last0;
     r1[31] = last1;
+#ifdef LGM_PANEL_PROF
+    if (tid == 0) {  // the step's FMAs: wait for the last result before reading the clock
+      const long long td = clock64() + (long long)(__double_as_longlong(r0[30]) & 0);
+      atomicAdd(&g_panel_cyc[8], (unsigned long long)(td - tc));
+    }
+#endif
   }
+  PP_T(t3);
+  PP_ADD(2, t3 - t2);
   const bool ph0 = my_step0 >= 0, ph1 = my_step1 >= 0;
   if (ph0) {
 #pragma unroll
@@ -1111,6 +1151,9 @@ __device__ __forceinline__ bool panel2_body(const InvJob& J, int n, int k0, int 
     for (int w = 0; w < 2 * NW; ++w) t += red[w];
     *J.logdet += t;
   }
+  PP_T(t4);
+  PP_ADD(3, t4 - t3);
+  PP_ADD(4, 1);
   return true;
 }
 
@@ -5944,8 +5987,8 @@ extern "C" int lgm_debug_g3_cycles(unsigned long long* out, int reset) {
 
 extern "C" int lgm_debug_panel_cycles(unsigned long long* out) {
 #ifdef LGM_PANEL_PROF
-  cudaMemcpyFromSymbol(out, g_panel_cyc, sizeof(g_panel_cyc));
-  return 6;
+  cudaMemcpyFromSymbol(out, g_panel_cyc, sizeof(g_panel_cyc));  // 12 entries
+  return 12;
 #else
   (void)out;
   return 0;
