@@ -496,6 +496,14 @@ __global__ void gj_init_kernel(const InvJob* jobs, int n) {
 // (shift-in-FMA pivot frame as in Engine F).  Per pivot step: block argmax, each CTA
 // publishes its candidate (key, row values) in its own shared memory, one cluster barrier,
 // every CTA reads the 8 candidates over DSMEM and applies the winner.  No grid-wide sync.
+#ifdef LGM_PANEL_PROF
+__device__ unsigned long long g_panel_cyc[12];  // load, stage-1, factor, store, CTAs; [6..8] panel2 step: search, publish, FMAs
+#define PP_T(v) long long v = clock64()
+#define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
+#else
+#define PP_T(v)
+#define PP_ADD(i, val)
+#endif
 constexpr int CL = 8;
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     gj_panel_cluster_kernel(const InvJob* jobs, int n, int k0, int nb) {
@@ -517,11 +525,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
   if (tid < 2 * 34) (&s_prow[0][0])[tid] = 0.0;  // pure-rotation steps read it with g = 0
   cl.sync();
   if (st0) return;  // whole cluster = this job: uniform
+  PP_T(t0);
   double r[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) r[c] = (valid && c < nb) ? J.M[(size_t)row * n + k0 + c] : 0.0;
   bool used = valid ? (J.rowstep[row] >= 0) : true;
   bool piv_here = false;
+#ifdef LGM_PANEL_PROF
+  long long t1 = clock64() + (__double_as_longlong(r[31]) & 0);
+  PP_ADD(0, t1 - t0);
+#endif
   double rowscale = 1.0, mypiv = 1.0;
   int status = 0;
   // packed pivot key: high word of |r0|; low word with its 12 low bits replaced by 4095 - row
@@ -545,9 +558,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     const double* pr = s_prow[par];
     if (kk < nb) {
       // block argmax: warp redux, then every warp reduces the 16 warp keys itself
+      PP_T(ta);
       const unsigned long long wk = warp_max(pack(r0, valid && !used));
       if (lane == 0) s_wkey[par][warp] = wk;
       __syncthreads();
+      PP_T(tb);
+      PP_ADD(6, tb - ta);
       const unsigned long long bk = warp_max(lane < 16 ? s_wkey[par][lane] : 0ull);
       const int brow = 4095 - (int)(bk & 0xfffu);
       if (tid == 0) s_key[par] = bk;
@@ -555,13 +571,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) s_cand[par][c] = r[c];
       }
+      PP_T(tc0);
       cl.sync();
+      PP_T(tc);
+      PP_ADD(9, tc0 - tb);
+      PP_ADD(7, tc - tc0);
       // cluster winner: lanes q < CL of every warp read CTA q's key over DSMEM
       const unsigned long long ck = warp_max(lane < CL ? *cl.map_shared_rank(&s_key[par], lane) : 0ull);
       if (ck == 0ull) { status = 1; break; }  // exact zero pivot (matcore.py:124-125)
       const int p = 4095 - (int)(ck & 0xfffu);
       if (tid < 32) s_prow[par][tid] = cl.map_shared_rank(&s_cand[par][0], p / rpc)[tid];
       __syncthreads();
+      PP_T(td);
+      PP_ADD(10, td - tc);
       const double rp = lgm_rcp(pr[0]);  // the winner's exact pivot (its row in its frame)
       const bool own = valid && (row == p);  // (idle threads' row ids alias other CTAs' rows)
       if (own) {
@@ -583,6 +605,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     }
     r[31] = last;
   }
+#ifdef LGM_PANEL_PROF
+  long long t2 = clock64() + (__double_as_longlong(r[30]) & 0);
+  PP_ADD(2, t2 - t1);
+#endif
   if (status) {
     if (part == 0 && tid == 0) *J.status = 1;
     cl.sync();
@@ -615,16 +641,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     *J.logdet += t;
   }
   cl.sync();
+#ifdef LGM_PANEL_PROF
+  PP_T(t3);
+  PP_ADD(3, t3 - t2);
+  PP_ADD(4, 1);
+#endif
 }
 
-#ifdef LGM_PANEL_PROF
-__device__ unsigned long long g_panel_cyc[12];  // load, stage-1, factor, store, CTAs; [6..8] panel2 step: search, publish, FMAs
-#define PP_T(v) long long v = clock64()
-#define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
-#else
-#define PP_T(v)
-#define PP_ADD(i, val)
-#endif
 // G2 panel for n <= 512 (many jobs): one CTA of NT >= n threads per inversion, row `tid`
 // of the 32-column panel in registers, the pivot rule and shift-in-FMA frame of G1
 // (gj_inv_cta_kernel).  No cluster: with hundreds of jobs the 8-CTA cluster panel's
