@@ -219,6 +219,14 @@ __device__ __forceinline__ double* wkind(const InvJob& J, int k) { return J.Wb +
 // After all panels, storage R satisfies R[piv[k]][j] = Minv[k][piv[j]], i.e.
 // Minv[a][c] = R[piv[a]][rowstep[c]].
 
+#ifdef LGM_PANEL_PROF
+__device__ unsigned long long g_panel_cyc[12];  // load, stage-1, factor, store, CTAs; [6..8] panel2 step: search, publish, FMAs
+#define PP_T(v) long long v = clock64()
+#define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
+#else
+#define PP_T(v)
+#define PP_ADD(i, val)
+#endif
 // ------------------------------------------------------------------------------------------
 // G1: the whole blocked Gauss-Jordan inversion of one matrix per CTA (64 < n <= NT <= 512).
 // Thread `tid` owns row `tid` of the current 32-column panel in registers (static register
@@ -268,6 +276,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     // (the first panel reads the source matrix when inverting out of place: every element of
     // M is written during panel 0 -- K columns by the panel store, the rest by its update)
     const double* Mr = (k0 == 0 && J.Src) ? J.Src : M;
+    PP_T(g0);
 #pragma unroll
     for (int c = 0; c < 32; c += 2) {
       if (tid < n && c + 1 < nb && (n & 1) == 0) {
@@ -281,6 +290,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     }
     double rowscale = 1.0;
     bool piv_here = false;
+#ifdef LGM_PANEL_PROF
+    long long g1 = clock64() + (__double_as_longlong(r[31]) & 0);
+    PP_ADD(0, g1 - g0);
+#endif
 #pragma unroll 1
     for (int kk = 0; kk < 32; ++kk) {  // shift-in-FMA pivot frame: the pivot column is r[0]
       const int par = kk & 1;
@@ -347,6 +360,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       }
       r[31] = last;
     }
+#ifdef LGM_PANEL_PROF
+    long long g2 = clock64() + (__double_as_longlong(r[30]) & 0);
+    PP_ADD(2, g2 - g1);
+#endif
     if (status) break;
     if (piv_here) {  // deferred scaling of this panel's pivot row
 #pragma unroll
@@ -402,6 +419,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     int buf = 0;
     if (jcur < n) snap(jcur, Ws);
     __syncthreads();
+    PP_T(g3);
+    PP_ADD(3, g3 - g2);
     while (jcur < n) {
       int jnext = jcur + 32;
       if (jnext == k0) jnext += 32;
@@ -463,6 +482,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       jcur = jnext;
       buf ^= 1;
     }
+    PP_T(g4);
+    PP_ADD(1, g4 - g3);
+    PP_ADD(4, 1);
   }
   // publish pivots, log|det|, status
   for (int i = tid; i < n; i += NT) { J.piv[i] = piv[i]; J.rowstep[i] = rstep[i]; }
@@ -496,14 +518,6 @@ __global__ void gj_init_kernel(const InvJob* jobs, int n) {
 // (shift-in-FMA pivot frame as in Engine F).  Per pivot step: block argmax, each CTA
 // publishes its candidate (key, row values) in its own shared memory, one cluster barrier,
 // every CTA reads the 8 candidates over DSMEM and applies the winner.  No grid-wide sync.
-#ifdef LGM_PANEL_PROF
-__device__ unsigned long long g_panel_cyc[12];  // load, stage-1, factor, store, CTAs; [6..8] panel2 step: search, publish, FMAs
-#define PP_T(v) long long v = clock64()
-#define PP_ADD(i, val) if (threadIdx.x == 0) atomicAdd(&g_panel_cyc[i], (unsigned long long)(val))
-#else
-#define PP_T(v)
-#define PP_ADD(i, val)
-#endif
 constexpr int CL = 8;
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1)
     gj_panel_cluster_kernel(const InvJob* jobs, int n, int k0, int nb) {

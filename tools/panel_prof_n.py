@@ -23,5 +23,9 @@ buf = (ctypes.c_ulonglong * 12)()
 lib.lgm_debug_panel_cycles(buf)
 v = list(buf); c = max(v[4], 1)
 print("n", n, "panel CTAs", c, "cycles/CTA: load %.0f factor %.0f store %.0f" % (v[0] / c, v[2] / c, v[3] / c))
+if n <= 256:  # G1: per 32-column panel of gj_inv_cta_kernel
+    print("G1 per panel: load %.0f  32 pivot steps %.0f  store+stage+first snapshot %.0f  trailing update %.0f" %
+          (v[0] / c, v[2] / c, v[3] / c, v[1] / c))
+    sys.exit(0)
 print("per pivot step: search+block barrier %.0f  candidate publish %.0f  cluster barrier %.0f  winner fetch+barrier %.0f"
       % (v[6] / c / 32, v[9] / c / 32, v[7] / c / 32, v[10] / c / 32))
