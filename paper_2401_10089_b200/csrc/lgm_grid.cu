@@ -111,6 +111,17 @@ bool up2s_on() {
   return on;
 }
 
+// G1 warp-level panels for n <= 128, n % 32 == 0 (gj_inv_cta_kernel<128, true>): opt-in with
+// LGM_G1_WP=1.  Bit-identical to the block-level panels but measured slower (n = 128, 2048
+// inversions: 1.44 vs 0.96 ms): one warp alone exposes every latency of its pivot steps.
+bool g1_warp_panel_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("LGM_G1_WP");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 #ifndef LGM_G1_PUBFIRST
 #define LGM_G1_PUBFIRST 1
 #endif
@@ -246,8 +257,145 @@ struct G1Smem {
   static constexpr size_t bytes = (A + W + PR) * 8 + 2 * (size_t)NT * 4 + 64 * 16;
 };
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* jobs, int n) {
+// G1 warp panel (n <= 128, n % 32 == 0; gj_inv_cta_kernel<128, true>): warp 0 factors the whole
+// 32-column panel alone, lane l holding rows l, l + 32, l + 64, l + 96 of one 16-column half in
+// registers.  The pivot search is a warp redux + shuffle -- no shared-memory exchange and no
+// block barrier per pivot step (the block version spends ~1.7k cycles per step under load:
+// two barriers, the key exchange, and the broadcast loads of a full 32-column pivot row per
+// thread).  The 32 steps run as: 16 searched steps on columns 0-15 (multipliers g kept in
+// shared memory), their replay on columns 16-31 (no search: stored g and pivot order), 16
+// searched steps on columns 16-31, their replay on columns 0-15, then the deferred scaling of
+// the panel's pivot rows.  Per element this is the block version's sequence of FMAs
+// r <- fma(-g_k, p_k, r), k = 0..31, with the same g_k and pivot-row values: bit-identical.
+// As: transposed panel As[c * lda + row]; Gs[16][128], pivval[128], rsc[128] live in the (idle)
+// snapshot buffer.  Returns 1 on an exact zero pivot (warp-uniform).
+__device__ __forceinline__ int g1_warp_panel(double* As, int lda, double* Gs, double* pivval, double* rsc, double* prow,
+                                             int* rstep, int* piv, int n, int k0, int lane) {
+  constexpr int H = 16;
+  bool valid[4], used[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int row = lane + 32 * q;
+    valid[q] = row < n;
+    used[q] = valid[q] ? (rstep[row] >= 0) : true;
+  }
+  double x[4][H];
+  auto load_half = [&](int h) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < H; ++j) x[q][j] = valid[q] ? As[(H * h + j) * lda + lane + 32 * q] : 0.0;
+  };
+  auto store_half = [&](int h) {  // with the deferred scaling of this panel's pivot rows
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!valid[q]) continue;
+      const int row = lane + 32 * q;
+      const int rs = rstep[row];
+      const double sc = (rs >= k0 && rs < k0 + 32) ? rsc[row] : 1.0;
+#pragma unroll
+      for (int j = 0; j < H; ++j) As[(H * h + j) * lda + row] = (sc != 1.0) ? x[q][j] * sc : x[q][j];
+    }
+  };
+  auto publish = [&](int slot, double* pw) {  // owner lane: its row `slot` of the live half
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (slot == q) {
+#pragma unroll
+        for (int j = 0; j < H; j += 2) *reinterpret_cast<double2*>(pw + j) = make_double2(x[q][j], x[q][j + 1]);
+      }
+  };
+  auto replay = [&](int hs) {  // the 16 steps of half hs applied to the other half's columns (in x)
+#pragma unroll 1
+    for (int kk = 0; kk < H; ++kk) {
+      const int p = piv[k0 + H * hs + kk];
+      double* pw = prow + (kk & 1) * 40;
+      if (lane == (p & 31)) publish(p >> 5, pw);
+      __syncwarp();
+      double g[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) g[q] = valid[q] ? Gs[kk * 128 + lane + 32 * q] : 0.0;
+#pragma unroll
+      for (int j = 0; j < H; j += 2) {
+        const double2 p2 = *reinterpret_cast<const double2*>(pw + j);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          x[q][j] = fma(-g[q], p2.x, x[q][j]);
+          x[q][j + 1] = fma(-g[q], p2.y, x[q][j + 1]);
+        }
+      }
+    }
+  };
+  auto search = [&](int h) -> int {  // 16 pivot steps on the live half (shift-in-FMA frame)
+#pragma unroll 1
+    for (int kk = 0; kk < H; ++kk) {
+      double* pw = prow + (kk & 1) * 40;
+      unsigned key = 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double a = x[q][0];
+        const bool cand = valid[q] && !used[q] && a != 0.0;
+        const unsigned kq =
+            cand ? ((((unsigned)__double2hiint(a) & 0x7fffffffu) & ~0x3ffu) | (unsigned)(1023 - (lane + 32 * q))) : 0u;
+        key = kq > key ? kq : key;
+      }
+      const unsigned wk = __reduce_max_sync(0xffffffffu, key);
+      if (wk == 0u) return 1;  // exact zero pivot (matcore.py:124-125)
+      const int p = 1023 - (int)(wk & 0x3ffu);
+      const int slot = p >> 5, ol = p & 31;
+      const double asel = slot == 0 ? x[0][0] : (slot == 1 ? x[1][0] : (slot == 2 ? x[2][0] : x[3][0]));
+      const double pv = __shfl_sync(0xffffffffu, asel, ol);
+      if (lane == ol) {
+        publish(slot, pw);
+        rstep[p] = k0 + H * h + kk;
+        piv[k0 + H * h + kk] = p;
+        pivval[p] = pv;
+      }
+      const double rp = lgm_rcp(pv);
+      if (lane == ol) rsc[p] = rp;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool own = (lane + 32 * q) == p;
+        const double g = own ? 0.0 : x[q][0] * rp;
+        const double last = own ? 1.0 : -g;
+        if (valid[q]) Gs[kk * 128 + lane + 32 * q] = g;
+        used[q] = used[q] || own;
+#pragma unroll
+        for (int c = 0; c < H; c += 2) {
+          const double2 p2 = *reinterpret_cast<const double2*>(pw + c);
+          if (c > 0) x[q][c - 1] = fma(-g, p2.x, x[q][c]);
+          x[q][c] = fma(-g, p2.y, x[q][c + 1 < H ? c + 1 : c]);
+        }
+        x[q][H - 1] = last;
+      }
+    }
+    return 0;
+  };
+  load_half(0);
+  if (search(0)) return 1;
+  // columns 0-15 wait (unscaled) in As for the second half's steps
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (valid[q]) {
+#pragma unroll
+      for (int j = 0; j < H; ++j) As[j * lda + lane + 32 * q] = x[q][j];
+    }
+  __syncwarp();
+  load_half(1);
+  replay(0);
+  __syncwarp();  // replay's last reads of Gs before search overwrites it
+  if (search(1)) return 1;
+  __syncwarp();
+  store_half(1);
+  load_half(0);
+  replay(1);
+  store_half(0);
+  return 0;
+}
+
+template <int NT, bool WP = false>
+__global__ void __launch_bounds__(NT, WP ? 2 : 512 / NT) gj_inv_cta_kernel(const InvJob* jobs, int n) {
   extern __shared__ __align__(16) double g1sm[];
   double* As = g1sm;
   double* Ws = As + G1Smem<NT>::A;
@@ -294,6 +442,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
     long long g1 = clock64() + (__double_as_longlong(r[31]) & 0);
     PP_ADD(0, g1 - g0);
 #endif
+    if constexpr (WP) {
+      // the panel moves to warp 0 through the transposed staging buffer and back
+#pragma unroll
+      for (int c = 0; c < 32; ++c) As[c * (NT + 4) + tid] = r[c];
+      __syncthreads();
+      if (warp == 0) {
+        const int st = g1_warp_panel(As, NT + 4, Ws, Ws + 16 * 128, Ws + 17 * 128, prow, rstep, piv, n, k0, lane);
+        if (lane == 0) wkey32[0] = (unsigned)st;
+      }
+      __syncthreads();
+      if (wkey32[0]) status = 1;
+      if (status == 0) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = As[c * (NT + 4) + tid];
+        const int rs = rstep[tid];
+        if (my_step < 0 && rs >= k0) {
+          my_step = rs;
+          mypiv = (Ws + 16 * 128)[tid];
+        }
+      }
+    } else {
 #pragma unroll 1
     for (int kk = 0; kk < 32; ++kk) {  // shift-in-FMA pivot frame: the pivot column is r[0]
       const int par = kk & 1;
@@ -360,6 +529,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) gj_inv_cta_kernel(const InvJob* 
       }
       r[31] = last;
     }
+    }  // !WP
 #ifdef LGM_PANEL_PROF
     long long g2 = clock64() + (__double_as_longlong(r[30]) & 0);
     PP_ADD(2, g2 - g1);
@@ -5271,6 +5441,12 @@ int cap_alpha(Cap& C, cudaStream_t st, int lst, int maxq) {
 template <int NT>
 int launch_g1(Cap& C, cudaStream_t st, int nj) {
   const size_t sm = G1Smem<NT>::bytes;
+  if constexpr (NT == 128) {
+    if (g1_warp_panel_on() && C.n % 32 == 0) {  // warp-level panels (opt-in LGM_G1_WP=1; bit-identical, slower)
+      GL gj_inv_cta_kernel<128, true><<<nj, NT, sm, st>>>(C.c.jobs, C.n);
+      return 0;
+    }
+  }
   GL gj_inv_cta_kernel<NT><<<nj, NT, sm, st>>>(C.c.jobs, C.n);
   return 0;
 }
@@ -5772,6 +5948,7 @@ int set_attrs(int n) {
   CK(cudaFuncSetAttribute(est_fused_kernel<false>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
   CK(cudaFuncSetAttribute(est_fused_kernel<true>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128>, mx, (int)G1Smem<128>::bytes));
+  CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128, true>, mx, (int)G1Smem<128>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<256>, mx, (int)G1Smem<256>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<512>, mx, (int)G1Smem<512>::bytes));
   CK(cudaFuncSetAttribute(gj_panel_cta_kernel<128>, mx, 4 * 32 * 33 * 8));
