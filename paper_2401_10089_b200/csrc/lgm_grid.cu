@@ -3474,6 +3474,173 @@ __global__ void __launch_bounds__(256) est_after_adj_kernel(EstJob* jobs, int n,
 // lane-strided FMAs + butterfly; adjoint: thread per column, 64-row slabs with 4 accumulators,
 // slab partials summed in order; the after-bodies are shared), so the two paths agree bit for bit.
 constexpr int EST_FUSED_MAXN = 160;
+#ifndef EST_FUSED_V2
+#define EST_FUSED_V2 1
+#endif
+#if EST_FUSED_V2
+// Version 2 (default; -DEST_FUSED_V2=0 builds the first version): the same sums in the same
+// order, arranged for the single CTA that runs them --
+//  * the job state and the two ping-pong vectors live in shared memory (a shared EstJob copy
+//    whose V0 / V1 point at shared buffers; the shared after-bodies work on it unchanged) and
+//    the state is written back once at the end: no L2 round trip per dependent step;
+//  * forward: a warp accumulates 16 of its rows at a time (lane-strided FMAs, one x load per
+//    16 rows) and reduces them with a butterfly reduce-scatter (stages 16, 8, 4, 2, then the
+//    final xor 1): per row the additions pair the same lane subsets in the same order as the
+//    plain butterfly, with 32 shuffles per 16 rows instead of 160;
+//  * adjoint: two threads per column, thread h forming (a_2h + a_2h+1) of each 64-row slab
+//    (rows = 2h, 2h + 1 mod 4; the remainder rows join a_0 as in est_adj_kernel), the column
+//    owner adding the halves and the slabs in order.
+template <bool CX>
+__global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
+  extern __shared__ __align__(16) double Ms[];
+  __shared__ double sred[8];
+  __shared__ EstAdjSmem sa;
+  __shared__ EstJob Js;
+  __shared__ __align__(16) double Vs[2][2 * EST_FUSED_MAXN];
+  EstJob& Jg = jobs[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (!Jg.live) {  // unused slot of a device-built table
+    if (tid == 0) Jg.done = 1;
+    return;
+  }
+  const bool skip = Jg.zchk && !Jg.nzf;  // (uniform: set before the launch)
+  if (tid == 0) {
+    Js = Jg;
+    Js.V0 = Vs[0];
+    Js.V1 = Vs[1];
+  }
+  __syncthreads();
+  EstJob& J = Js;
+  {  // est_init_kernel
+    const int t = est_x0(J, n, rsum, rsum_c, tid, 256);
+    if (tid == 0) {
+      J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
+      J.total = J.p1 + (J.M2 ? 1 : 0);
+      J.done = skip ? 1 : 0;
+    }
+  }
+  auto write_back = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      Jg.est = J.est; Jg.best_j = J.best_j; Jg.ncols = J.ncols; Jg.done = J.done; Jg.nhist = J.nhist;
+      Jg.passes = J.passes; Jg.total = J.total; Jg.mm = J.mm;
+    }
+  };
+  if (skip) { write_back(); return; }
+  for (int idx = tid; idx < n * n; idx += 256) Ms[idx] = J.M1[idx];
+  __syncthreads();
+  const int total = J.p1 + (J.M2 ? 1 : 0);
+  const int splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  for (int sweep = 0; sweep < itmax; ++sweep) {
+    if (J.done) break;
+    const int nc = J.ncols;
+    for (int q = 0; q < total; ++q) {  // forward (est_fwd_kernel's sums)
+      const double* M = (J.M2 && q == 0) ? J.M2 : Ms;
+      const double* x = (q & 1) ? J.V1 : J.V0;
+      double* y = (q & 1) ? J.V0 : J.V1;
+      for (int ib = warp; ib < n; ib += 8 * 16) {  // rows ib + 8 r, r = 0..15
+        double a0[16], a1[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) a0[r] = a1[r] = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          const double x0 = x[j], x1 = nc > 1 ? x[n + j] : 0.0;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int i = ib + 8 * r;
+            const double m = i < n ? M[(size_t)i * n + j] : 0.0;
+            a0[r] = fma(m, x0, a0[r]);
+            a1[r] = fma(m, x1, a1[r]);
+          }
+        }
+        // reduce-scatter: after the stages with offsets 16, 8, 4, 2 lane l holds row
+        // r = 8 b4 + 4 b3 + 2 b2 + b1 (b_k = bit k of l) summed over the lanes that differ from l
+        // in those bits; the xor-1 stage completes it
+#pragma unroll
+        for (int off = 16, len = 16; off >= 2; off >>= 1, len >>= 1) {
+          const bool up = (lane & off) != 0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            if (r < len / 2) {
+              const double s0 = up ? a0[r] : a0[r + len / 2], k0 = up ? a0[r + len / 2] : a0[r];
+              const double s1 = up ? a1[r] : a1[r + len / 2], k1 = up ? a1[r + len / 2] : a1[r];
+              a0[r] = k0 + __shfl_xor_sync(0xffffffffu, s0, off);
+              a1[r] = k1 + __shfl_xor_sync(0xffffffffu, s1, off);
+            }
+          }
+        }
+        a0[0] += __shfl_xor_sync(0xffffffffu, a0[0], 1);
+        a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 1);
+        const int i = ib + 8 * (lane >> 1);
+        if ((lane & 1) == 0 && i < n) {
+          y[i] = a0[0];
+          if (nc > 1) y[n + i] = a1[0];
+        }
+      }
+      __syncthreads();
+    }
+    est_after_fwd_impl<CX>(J, n, sweep, sred);
+    __syncthreads();
+    if (J.done) break;
+    const bool two = J.ncols > 1;
+    for (int q = 0; q < total; ++q) {  // adjoint (est_adj_kernel + est_adj_reduce_kernel's sums)
+      const double* M = (q < J.p1) ? Ms : J.M2;
+      const double* x = (q & 1) ? J.V1 : J.V0;
+      double* y = (q & 1) ? J.V0 : J.V1;
+      double s0v[2] = {0.0, 0.0}, s1v[2] = {0.0, 0.0};  // two (column, half) pairs per thread: 2 x 8 warps x 16 columns >= 160
+#pragma unroll
+      for (int rep = 0; rep < 2; ++rep) {
+        // lanes 0-15 of a warp: half 0 of 16 consecutive columns, lanes 16-31: half 1 of the same
+        // columns (each half-warp reads one contiguous 128-byte row segment: no bank conflicts)
+        const int j = (warp + 8 * rep) * 16 + (lane & 15), h = lane >> 4;
+        const bool ok = j < n;
+        double s0 = 0.0, s1 = 0.0;
+        for (int sl = 0; sl < splits; ++sl) {
+          const int r0 = sl * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
+          double b0[2] = {0.0, 0.0}, b1[2] = {0.0, 0.0};
+          if (ok) {
+            int r = r0;
+            for (; r + 3 < r1; r += 4) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int rr = r + 2 * h + u;
+                const double m = M[(size_t)rr * n + j];
+                b0[u] = fma(m, x[rr], b0[u]);
+                if (two) b1[u] = fma(m, x[n + rr], b1[u]);
+              }
+            }
+            if (h == 0) {
+              for (; r < r1; ++r) {
+                const double m = M[(size_t)r * n + j];
+                b0[0] = fma(m, x[r], b0[0]);
+                if (two) b1[0] = fma(m, x[n + r], b1[0]);
+              }
+            }
+          }
+          const double p0 = b0[0] + b0[1], p1 = b1[0] + b1[1];
+          const double o0 = __shfl_xor_sync(0xffffffffu, p0, 16), o1 = __shfl_xor_sync(0xffffffffu, p1, 16);
+          s0 += p0 + o0;  // h = 0: (a0 + a1) + (a2 + a3)
+          s1 += p1 + o1;
+        }
+        s0v[rep] = s0;
+        s1v[rep] = s1;
+      }
+      __syncthreads();  // every thread has read x before y (the other buffer) is written
+#pragma unroll
+      for (int rep = 0; rep < 2; ++rep) {
+        const int j = (warp + 8 * rep) * 16 + (lane & 15), h = lane >> 4;
+        if (h == 0 && j < n) {
+          y[j] = s0v[rep];
+          if (two) y[n + j] = s1v[rep];
+        }
+      }
+      __syncthreads();
+    }
+    est_after_adj_impl<CX>(J, n, sweep, sa);
+    __syncthreads();
+  }
+  write_back();
+}
+#else
 template <bool CX>
 __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
   extern __shared__ __align__(16) double Ms[];
@@ -3568,6 +3735,8 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
     __syncthreads();
   }
 }
+
+#endif  // EST_FUSED_V2
 
 // ------------------------------------------------------------------------------------------
 // The whole estimate of one job per thread-block cluster (EST_FUSED_MAXN < n <= 512), M1
