@@ -3478,6 +3478,11 @@ constexpr int EST_FUSED_MAXN = 160;
 #define EST_FUSED_V2 1
 #endif
 #if EST_FUSED_V2
+constexpr int ESTF_THREADS = 512;
+#else
+constexpr int ESTF_THREADS = 256;
+#endif
+#if EST_FUSED_V2
 // Version 2 (default; -DEST_FUSED_V2=0 builds the first version): the same sums in the same
 // order, arranged for the single CTA that runs them --
 //  * the job state and the two ping-pong vectors live in shared memory (a shared EstJob copy
@@ -3490,15 +3495,19 @@ constexpr int EST_FUSED_MAXN = 160;
 //  * adjoint: two threads per column, thread h forming (a_2h + a_2h+1) of each 64-row slab
 //    (rows = 2h, 2h + 1 mod 4; the remainder rows join a_0 as in est_adj_kernel), the column
 //    owner adding the halves and the slabs in order.
+constexpr int ESTF_NT = 512;  // 16 warps: the thread count only adds zero terms to the after-bodies' sums (n <= 160 < 256)
 template <bool CX>
-__global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
+__global__ void __launch_bounds__(ESTF_NT) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
   extern __shared__ __align__(16) double Ms[];
-  __shared__ double sred[8];
+  __shared__ double sred[ESTF_NT / 32];
   __shared__ EstAdjSmem sa;
   __shared__ EstJob Js;
   __shared__ __align__(16) double Vs[2][2 * EST_FUSED_MAXN];
+  constexpr int MAXSPL = (EST_FUSED_MAXN + ADJ_ROWS - 1) / ADJ_ROWS;
+  __shared__ double parts[MAXSPL][2][EST_FUSED_MAXN];  // adjoint slab partials (est_adj_reduce_kernel's inputs)
   EstJob& Jg = jobs[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = ESTF_NT / 32;
   if (!Jg.live) {  // unused slot of a device-built table
     if (tid == 0) Jg.done = 1;
     return;
@@ -3512,7 +3521,7 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
   __syncthreads();
   EstJob& J = Js;
   {  // est_init_kernel
-    const int t = est_x0(J, n, rsum, rsum_c, tid, 256);
+    const int t = est_x0(J, n, rsum, rsum_c, tid, ESTF_NT);
     if (tid == 0) {
       J.est = 0.0; J.best_j = 0; J.ncols = t; J.nhist = 0; J.passes = 0; J.mm = INFINITY;
       J.total = J.p1 + (J.M2 ? 1 : 0);
@@ -3527,39 +3536,39 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
     }
   };
   if (skip) { write_back(); return; }
-  for (int idx = tid; idx < n * n; idx += 256) Ms[idx] = J.M1[idx];
+  for (int idx = tid; idx < n * n; idx += ESTF_NT) Ms[idx] = J.M1[idx];
   __syncthreads();
   const int total = J.p1 + (J.M2 ? 1 : 0);
   const int splits = (n + ADJ_ROWS - 1) / ADJ_ROWS;
+  const int cblocks = (n + 15) / 16;
   for (int sweep = 0; sweep < itmax; ++sweep) {
     if (J.done) break;
     const int nc = J.ncols;
     for (int q = 0; q < total; ++q) {  // forward (est_fwd_kernel's sums)
       const double* M = (J.M2 && q == 0) ? J.M2 : Ms;
-      const double* x = (q & 1) ? J.V1 : J.V0;
-      double* y = (q & 1) ? J.V0 : J.V1;
-      for (int ib = warp; ib < n; ib += 8 * 16) {  // rows ib + 8 r, r = 0..15
-        double a0[16], a1[16];
+      const double* x = (q & 1) ? Vs[1] : Vs[0];
+      double* y = (q & 1) ? Vs[0] : Vs[1];
+      for (int ib = warp; ib < n; ib += NW * 8) {  // rows ib + NW r, r = 0..7
+        double a0[8], a1[8];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) a0[r] = a1[r] = 0.0;
+        for (int r = 0; r < 8; ++r) a0[r] = a1[r] = 0.0;
         for (int j = lane; j < n; j += 32) {
           const double x0 = x[j], x1 = nc > 1 ? x[n + j] : 0.0;
 #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const int i = ib + 8 * r;
+          for (int r = 0; r < 8; ++r) {
+            const int i = ib + NW * r;
             const double m = i < n ? M[(size_t)i * n + j] : 0.0;
             a0[r] = fma(m, x0, a0[r]);
             a1[r] = fma(m, x1, a1[r]);
           }
         }
-        // reduce-scatter: after the stages with offsets 16, 8, 4, 2 lane l holds row
-        // r = 8 b4 + 4 b3 + 2 b2 + b1 (b_k = bit k of l) summed over the lanes that differ from l
-        // in those bits; the xor-1 stage completes it
+        // reduce-scatter with offsets 16, 8, 4 (lane l then holds row r = 4 b4 + 2 b3 + b2, b_k =
+        // bit k of l), then the plain xor-2 and xor-1 stages: the butterfly's pairings in its order
 #pragma unroll
-        for (int off = 16, len = 16; off >= 2; off >>= 1, len >>= 1) {
+        for (int off = 16, len = 8; off >= 4; off >>= 1, len >>= 1) {
           const bool up = (lane & off) != 0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
+          for (int r = 0; r < 4; ++r) {
             if (r < len / 2) {
               const double s0 = up ? a0[r] : a0[r + len / 2], k0 = up ? a0[r + len / 2] : a0[r];
               const double s1 = up ? a1[r] : a1[r + len / 2], k1 = up ? a1[r + len / 2] : a1[r];
@@ -3568,10 +3577,13 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
             }
           }
         }
-        a0[0] += __shfl_xor_sync(0xffffffffu, a0[0], 1);
-        a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 1);
-        const int i = ib + 8 * (lane >> 1);
-        if ((lane & 1) == 0 && i < n) {
+#pragma unroll
+        for (int off = 2; off >= 1; off >>= 1) {
+          a0[0] += __shfl_xor_sync(0xffffffffu, a0[0], off);
+          a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], off);
+        }
+        const int i = ib + NW * (lane >> 2);
+        if ((lane & 3) == 0 && i < n) {
           y[i] = a0[0];
           if (nc > 1) y[n + i] = a1[0];
         }
@@ -3584,54 +3596,49 @@ __global__ void __launch_bounds__(256) est_fused_kernel(EstJob* jobs, int n, dou
     const bool two = J.ncols > 1;
     for (int q = 0; q < total; ++q) {  // adjoint (est_adj_kernel + est_adj_reduce_kernel's sums)
       const double* M = (q < J.p1) ? Ms : J.M2;
-      const double* x = (q & 1) ? J.V1 : J.V0;
-      double* y = (q & 1) ? J.V0 : J.V1;
-      double s0v[2] = {0.0, 0.0}, s1v[2] = {0.0, 0.0};  // two (column, half) pairs per thread: 2 x 8 warps x 16 columns >= 160
+      const double* x = (q & 1) ? Vs[1] : Vs[0];
+      double* y = (q & 1) ? Vs[0] : Vs[1];
+      // one warp task = (64-row slab, 16 columns): lanes 0-15 form a0 + a1 of their column over the
+      // slab, lanes 16-31 a2 + a3 (each half-warp reads one contiguous 128-byte row segment)
+      for (int task = warp; task < splits * cblocks; task += NW) {
+        const int sl = task / cblocks, j = (task - sl * cblocks) * 16 + (lane & 15), h = lane >> 4;
+        const int r0 = sl * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
+        double b0[2] = {0.0, 0.0}, b1[2] = {0.0, 0.0};
+        if (j < n) {
+          int r = r0;
+          for (; r + 3 < r1; r += 4) {
 #pragma unroll
-      for (int rep = 0; rep < 2; ++rep) {
-        // lanes 0-15 of a warp: half 0 of 16 consecutive columns, lanes 16-31: half 1 of the same
-        // columns (each half-warp reads one contiguous 128-byte row segment: no bank conflicts)
-        const int j = (warp + 8 * rep) * 16 + (lane & 15), h = lane >> 4;
-        const bool ok = j < n;
-        double s0 = 0.0, s1 = 0.0;
-        for (int sl = 0; sl < splits; ++sl) {
-          const int r0 = sl * ADJ_ROWS, r1 = min(n, r0 + ADJ_ROWS);
-          double b0[2] = {0.0, 0.0}, b1[2] = {0.0, 0.0};
-          if (ok) {
-            int r = r0;
-            for (; r + 3 < r1; r += 4) {
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int rr = r + 2 * h + u;
-                const double m = M[(size_t)rr * n + j];
-                b0[u] = fma(m, x[rr], b0[u]);
-                if (two) b1[u] = fma(m, x[n + rr], b1[u]);
-              }
-            }
-            if (h == 0) {
-              for (; r < r1; ++r) {
-                const double m = M[(size_t)r * n + j];
-                b0[0] = fma(m, x[r], b0[0]);
-                if (two) b1[0] = fma(m, x[n + r], b1[0]);
-              }
+            for (int u = 0; u < 2; ++u) {
+              const int rr = r + 2 * h + u;
+              const double m = M[(size_t)rr * n + j];
+              b0[u] = fma(m, x[rr], b0[u]);
+              if (two) b1[u] = fma(m, x[n + rr], b1[u]);
             }
           }
-          const double p0 = b0[0] + b0[1], p1 = b1[0] + b1[1];
-          const double o0 = __shfl_xor_sync(0xffffffffu, p0, 16), o1 = __shfl_xor_sync(0xffffffffu, p1, 16);
-          s0 += p0 + o0;  // h = 0: (a0 + a1) + (a2 + a3)
-          s1 += p1 + o1;
+          if (h == 0) {
+            for (; r < r1; ++r) {
+              const double m = M[(size_t)r * n + j];
+              b0[0] = fma(m, x[r], b0[0]);
+              if (two) b1[0] = fma(m, x[n + r], b1[0]);
+            }
+          }
         }
-        s0v[rep] = s0;
-        s1v[rep] = s1;
-      }
-      __syncthreads();  // every thread has read x before y (the other buffer) is written
-#pragma unroll
-      for (int rep = 0; rep < 2; ++rep) {
-        const int j = (warp + 8 * rep) * 16 + (lane & 15), h = lane >> 4;
+        const double p0 = b0[0] + b0[1], p1 = b1[0] + b1[1];
+        const double o0 = __shfl_xor_sync(0xffffffffu, p0, 16), o1 = __shfl_xor_sync(0xffffffffu, p1, 16);
         if (h == 0 && j < n) {
-          y[j] = s0v[rep];
-          if (two) y[n + j] = s1v[rep];
+          parts[sl][0][j] = p0 + o0;  // (a0 + a1) + (a2 + a3)
+          parts[sl][1][j] = p1 + o1;
         }
+      }
+      __syncthreads();  // partials complete; every thread has read x before y (the other buffer) is written
+      if (tid < n) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int sl = 0; sl < splits; ++sl) {
+          s0 += parts[sl][0][tid];
+          s1 += parts[sl][1][tid];
+        }
+        y[tid] = s0;
+        if (two) y[n + tid] = s1;
       }
       __syncthreads();
     }
@@ -5556,8 +5563,8 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
   GL est_nz_kernel<<<dim3(std::max(1, std::min(32, n * n / 4096)), nj), 256, 0, st>>>(C.c.est, n);
   if (n <= EST_FUSED_MAXN && est_fused_on()) {
     const int sm = n * n * 8;
-    if (C.cplx) GL est_fused_kernel<true><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
-    else GL est_fused_kernel<false><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
+    if (C.cplx) GL est_fused_kernel<true><<<nj, ESTF_THREADS, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
+    else GL est_fused_kernel<false><<<nj, ESTF_THREADS, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
     return 0;
   }
   if (n > EST_FUSED_MAXN && n <= 512 && est_cluster_on()) {  // M1 resident in a cluster's smem
