@@ -3495,8 +3495,10 @@ constexpr int ESTF_THREADS = 256;
 //  * adjoint: two threads per column, thread h forming (a_2h + a_2h+1) of each 64-row slab
 //    (rows = 2h, 2h + 1 mod 4; the remainder rows join a_0 as in est_adj_kernel), the column
 //    owner adding the halves and the slabs in order.
-constexpr int ESTF_NT = 512;  // 16 warps: the thread count only adds zero terms to the after-bodies' sums (n <= 160 < 256)
-template <bool CX>
+// ESTF_NT threads (512 for n > ESTF_SMALL_N, else 256): the thread count only adds zero terms to
+// the after-bodies' block sums (n <= 160 < 256), so every variant gives the same bits
+constexpr int ESTF_SMALL_N = 96;
+template <bool CX, int ESTF_NT = 512>
 __global__ void __launch_bounds__(ESTF_NT) est_fused_kernel(EstJob* jobs, int n, double rsum, double rsum_c, int itmax) {
   extern __shared__ __align__(16) double Ms[];
   __shared__ double sred[ESTF_NT / 32];
@@ -5563,6 +5565,13 @@ int cap_estimate(Cap& C, cudaStream_t st, int maxq) {
   GL est_nz_kernel<<<dim3(std::max(1, std::min(32, n * n / 4096)), nj), 256, 0, st>>>(C.c.est, n);
   if (n <= EST_FUSED_MAXN && est_fused_on()) {
     const int sm = n * n * 8;
+#if EST_FUSED_V2
+    if (n <= ESTF_SMALL_N) {  // fewer, busier warps for the small matrices (same bits)
+      if (C.cplx) GL est_fused_kernel<true, 256><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
+      else GL est_fused_kernel<false, 256><<<nj, 256, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
+      return 0;
+    }
+#endif
     if (C.cplx) GL est_fused_kernel<true><<<nj, ESTF_THREADS, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
     else GL est_fused_kernel<false><<<nj, ESTF_THREADS, sm, st>>>(C.c.est, n, rsum, rsum_c, C.itmax);
     return 0;
@@ -6123,6 +6132,10 @@ int set_attrs(int n) {
   const cudaFuncAttribute mx = cudaFuncAttributeMaxDynamicSharedMemorySize;
   CK(cudaFuncSetAttribute(est_fused_kernel<false>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
   CK(cudaFuncSetAttribute(est_fused_kernel<true>, mx, EST_FUSED_MAXN * EST_FUSED_MAXN * 8));
+#if EST_FUSED_V2
+  CK(cudaFuncSetAttribute(est_fused_kernel<false, 256>, mx, ESTF_SMALL_N * ESTF_SMALL_N * 8));
+  CK(cudaFuncSetAttribute(est_fused_kernel<true, 256>, mx, ESTF_SMALL_N * ESTF_SMALL_N * 8));
+#endif
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128>, mx, (int)G1Smem<128>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<128, true>, mx, (int)G1Smem<128>::bytes));
   CK(cudaFuncSetAttribute(gj_inv_cta_kernel<256>, mx, (int)G1Smem<256>::bytes));
