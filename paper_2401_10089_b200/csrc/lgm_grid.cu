@@ -5025,8 +5025,15 @@ __global__ void poly_start_kernel(PolyArgs a, DList L) {
 
 // GEMM j: P_{j+3} = L_j R_j (64 x 64 tiles, K in chunks of 32 staged by a two-stage cp.async
 // pipeline, DMMA core; scalar loads for odd n), fused epilogue as above
+// POLY_1STAGE (default 1; -DPOLY_1STAGE=0 builds the two-stage cp.async ring at 3 CTAs/SM): one
+// K-chunk buffer per CTA and 4 CTAs/SM (120 registers, 36 KB) -- the single-slot idea of
+// gj_update2s_kernel: the co-resident CTAs' loads overlap each other's products.  Same sums
+// (bit-identical); config 4 polynomial phase 14.1 -> 13.0 ms, config 3b 43.40 -> 43.08 ms.
+#ifndef POLY_1STAGE
+#define POLY_1STAGE 1
+#endif
 template <bool EVEN>
-__global__ void __launch_bounds__(128) poly_gemm_kernel(PolyArgs a, DList L, int j) {
+__global__ void __launch_bounds__(128, POLY_1STAGE ? 4 : 1) poly_gemm_kernel(PolyArgs a, DList L, int j) {
   extern __shared__ __align__(16) double gsm[];
   if (blockIdx.z >= *L.cnt) return;
   const int b = L.ids[blockIdx.z];
@@ -5061,6 +5068,15 @@ __global__ void __launch_bounds__(128) poly_gemm_kernel(PolyArgs a, DList L, int
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
   const int nk = (n + TK - 1) / TK;
+#if POLY_1STAGE
+  for (int kc = 0; kc < nk; ++kc) {
+    stage(kc * TK, 0);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    tile_mma(gsm, gsm + GP_A, acc);
+    __syncthreads();
+  }
+#else
   stage(0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     if (kc + 1 < nk) {
@@ -5074,6 +5090,7 @@ __global__ void __launch_bounds__(128) poly_gemm_kernel(PolyArgs a, DList L, int
     tile_mma(As, As + GP_A, acc);
     __syncthreads();
   }
+#endif
   const int k = a.ms[b].k;
   const LgmParams& P = a.d->P;
   const int pn = j + 3;                 // this product is node P_{j+3}
@@ -5933,7 +5950,7 @@ int cap_poly(Cap& C, cudaStream_t st, bool logm) {
   a.logm = logm ? 1 : 0;
   GL poly_start_kernel<<<ew_blocks(), 256, 0, st>>>(a, C.c.list(LS_SEL));
   const int tiles = (n + TM - 1) / TM;
-  const size_t gsm = 2 * (size_t)(GP_A + GP_B) * 8;
+  const size_t gsm = (POLY_1STAGE ? 1 : 2) * (size_t)(GP_A + GP_B) * 8;
   for (int j = 1; j < LGM_K_MAX; ++j) {
     if ((n & 1) == 0) GL poly_gemm_kernel<true><<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(a, C.c.list(LS_POLY0 + j), j);
     else GL poly_gemm_kernel<false><<<dim3(tiles, tiles, C.batch), 128, gsm, st>>>(a, C.c.list(LS_POLY0 + j), j);
