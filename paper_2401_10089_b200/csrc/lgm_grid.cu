@@ -1657,6 +1657,20 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
   if (tid < NB) p1s[tid] = J.piv[k0 + tid];
   else if (tid < 2 * NB) p2s[tid - NB] = J.piv[k0 + tid];
   __syncthreads();
+  // the accumulators' P2 rows need only p2s: issued with the A1 / W1 staging loads (one global
+  // round trip less per CTA)
+  const int g8 = lane >> 2, t4 = lane & 3, wc = warp * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int jc = j0 + wc + ni * 8 + 2 * t4;
+      const double* Ms = (J.Src && k0 == 0 && jc >= 2 * NB) ? J.Src : J.M;
+      const double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)p2s[mi * 8 + g8] * n + jc]);
+      acc[mi][ni][0] = v.x;
+      acc[mi][ni][1] = v.y;
+    }
   for (int idx = tid; idx < NB * NB; idx += 128) {
     const int c = idx >> 5, cc = idx & 31;
     a1s[c][cc] = A1[(size_t)p2s[c] * NB + cc];
@@ -1677,18 +1691,6 @@ __global__ void __launch_bounds__(128) gj_w2_mma_kernel(const InvJob* jobs, int 
       W1[(size_t)(j0 + jj) * NB + cc] = w1s[cc][jj];
     }
   }
-  const int g8 = lane >> 2, t4 = lane & 3, wc = warp * 16;
-  double acc[4][2][2];
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) {
-      const int jc = j0 + wc + ni * 8 + 2 * t4;
-      const double* Ms = (J.Src && k0 == 0 && jc >= 2 * NB) ? J.Src : J.M;
-      const double2 v = *reinterpret_cast<const double2*>(&Ms[(size_t)p2s[mi * 8 + g8] * n + jc]);
-      acc[mi][ni][0] = v.x;
-      acc[mi][ni][1] = v.y;
-    }
 #pragma unroll
   for (int k = 0; k < NB; k += 4) {
     double a[4], b[2];
